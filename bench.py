@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Optimizer-step benchmark for the B200 MemAscend hot path.
+
+One step = the reference's per-step optimizer pass (simulator.cpp:427-492)
+over one rank's flat partition: K1 fused overflow check over all scaled bf16
+gradients -> (N>1: NCCL all-reduce(max) of the flag) -> K2 unscale + AdamW +
+bf16 cast-back over every 100M-param sub-group -> device-side LossScaler.
+
+Default workload = BASELINE.json configs[1]: Llama-3-8B-shaped optimizer
+state, 8,030,261,248 params per GPU (model.cpp:233), resident in HBM
+(fp32 master/m/v + bf16 grads + bf16 working weights = 128.5 GB), 81
+sub-groups of 100,000,000 params.  Weak scaling under torchrun: every rank
+owns one such partition (global element index = rank * n + i).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Rank 0 prints one JSON line.  Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks.  Inputs (128.5 GB) are
+far larger than L2 (126 MB), so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "optimizer-step params/sec (overflow check+AdamW) and HBM GB/s vs B200 peak"
+LLAMA3_8B = 8_030_261_248       # proj/src/model.cpp:233
+CFG1 = 67_108_864               # configs[0]: one 64M-param sub-group
+SUBGROUP = 100_000_000          # optimizer sub-group
+BYTES_PER_PARAM = 28            # 2 g + 12 pmv read + 12 pmv write + 2 w16
+HYPER = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["cfg2", "cfg1"], default="cfg2")
+    ap.add_argument("--params", type=int, default=0, help="override params per GPU (debug)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=CFG1,
+                    help="params in the CPU baseline's bounded sample")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        except Exception:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][2]),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit()),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- CPU arms
+def cpu_reference_run(n, steps, warmup, threads):
+    """The reference's own CPU path (oracle/_ref: fused_overflow_check +
+    adam_step_fp32 per sub-group + cast, simulator.cpp:431-469 composition)
+    on a bounded sample of the same workload.  Falls back to the restated
+    oracle only if the reference library was not built."""
+    from oracle import oracle as ora
+
+    p, w = ora.fill_weights(n, seed=1, w_kind="bf16", threads=threads)
+    _, g32 = ora.fill_grads(w, 0, seed=1, scale=65536.0, g_kind="bf16", w_kind="bf16",
+                            threads=threads)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    h = ora.hyper(**HYPER)
+    kind = "reference" if ora.ref_available() else "port"
+    times = []
+    for s in range(warmup + steps):
+        if kind == "reference":
+            of, secs = ora.ref_bench_step(g32, p, m, v, w, "bf16", SUBGROUP, s + 1, h, 65536.0,
+                                          threads)
+        else:
+            t0 = time.perf_counter()
+            of, _ = ora.overflow_check(g32, "f32")
+            w[:] = ora.adam_step(p, m, v, g32, s + 1, h, 65536.0, "f32", "bf16")
+            secs = time.perf_counter() - t0
+        assert not of
+        if s >= warmup:
+            times.append(secs)
+    t = float(np.median(times))
+    return {"value": n / t, "unit": "params/s", "cores": threads, "kind": kind,
+            "sample": f"{n} params (bf16-rounded grads widened to the reference's fp32 flat "
+                      f"buffer), {SUBGROUP // 1_000_000}M sub-groups, median of {steps} steps "
+                      f"after {warmup} warm-up, {threads} threads",
+            "seconds_per_step": t}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def reference_arm(args, n_per_gpu, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = min(args.cpu_sample, n_per_gpu)
+    res = cpu_reference_run(sample, max(1, args.steps), max(1, args.warmup), threads)
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": "params/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": res["seconds_per_step"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args, n_per_gpu, world),
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "params/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "host": {"cpu": cpu_model(), "nproc": threads},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, n, world):
+    name = ("llama3-8b-optimizer-state-hbm" if args.config == "cfg2" and not args.params
+            else "cfg1-64M-subgroup" if args.config == "cfg1" and not args.params
+            else f"custom-{n}")
+    return {"workload": name, "params_per_gpu": n, "subgroup_params": min(SUBGROUP, n),
+            "grads": "bf16", "working_weights": "bf16", "state": "fp32 master/m/v in HBM",
+            "optimizer": "AdamW lr=1e-3 b1=0.9 b2=0.999 eps=1e-8 wd=0.01, loss scale 65536",
+            "parallelism": f"zero-partition x{world} (flag all-reduce only)",
+            "l2": "inputs larger than L2 (no flush needed)" if n * 28 > 4 * 126e6
+            else "L2 flushed between steps"}
+
+
+# --------------------------------------------------------------- our arm
+def ours(args, n, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_23254_b200 as mab
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    free, total = torch.cuda.mem_get_info()
+    need = n * 16 + (1 << 30)
+    if need > free:
+        raise SystemExit(f"rank {rank}: need {need / 1e9:.1f} GB of HBM, {free / 1e9:.1f} free")
+    p = torch.empty(n, dtype=torch.float32, device=dev)
+    m = torch.zeros(n, dtype=torch.float32, device=dev)
+    v = torch.zeros(n, dtype=torch.float32, device=dev)
+    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    base = rank * n
+    mab.gen_seeded_weights(p, w, base=base, seed=1)
+    mab.gen_pseudo_grads(g, w, step=0, base=base, seed=1, scale=65536.0)
+    st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "bf16", device=dev)
+    sub = min(SUBGROUP, n)
+    groups = mab.Stepper.subgroups(
+        [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub], w[o:o + sub])
+         for o in range(0, n, sub)])
+    stream = torch.cuda.current_stream(dev)
+    flush = None
+    if n * BYTES_PER_PARAM < 4 * 126e6:  # small configs: flush L2 between steps
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def allreduce(flag):
+        if world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+
+    def one_step(rec=None):
+        if flush is not None:
+            flush.zero_()
+        if rec:
+            rec[0].record(stream)
+        st.check(g)
+        if rec:
+            rec[1].record(stream)
+        allreduce(st.flag)
+        if rec:
+            rec[2].record(stream)
+        st.apply(groups)
+        st.finish()
+        if rec:
+            rec[3].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(args.steps):
+            one_step(ev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    elapsed_ms = t0.elapsed_time(t1)
+    k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+    state = st.state()
+    assert state["steps"] == args.warmup + args.steps and state["last_overflow"] == 0
+
+    # max over ranks
+    t = torch.tensor([elapsed_ms, k1_ms, k2_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms, k1_ms, k2_ms = t.tolist()
+    ms_per_step = elapsed_ms / args.steps
+
+    # ---- e2e: gradients from pinned host memory through the public API
+    e2e = None
+    if args.e2e_steps > 0:
+        g_host = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+        g_host.view(torch.int16).copy_(g.view(torch.int16), non_blocking=False)
+        res_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
+
+        def e2e_step():
+            st.check_from_host(g_host, g)
+            allreduce(st.flag)
+            st.apply(groups)
+            st.finish()
+            res_host.copy_(st.state_t[:16], non_blocking=True)  # flag/scale readback
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([a.elapsed_time(b) / args.e2e_steps], dtype=torch.float64,
+                              device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e_ms = float(e2e_ms.item())
+        e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "params/s",
+               "h2d_bytes_per_step": n * 2, "d2h_bytes_per_step": 16,
+               "ms_per_step": e2e_ms,
+               "path": "pinned host bf16 grads -> chunked H2D overlapped with K1 "
+                       "(ma_stepper_check_host_async) -> K2 over HBM-resident state -> "
+                       "D2H of the step's flag/loss-scale"}
+        del g_host
+
+    if rank != 0:
+        return
+    peak, peak_kind = peaks()
+    alg_bytes = BYTES_PER_PARAM * n
+    k2_gbs = alg_bytes / (k2_ms / 1e3) / 1e9
+    launches_per_step = 1 + (len(groups) + 95) // 96 + 1
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(workload_config(args, n, world)["workload"])
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC,
+        "value": n * world / (ms_per_step / 1e3),
+        "unit": "params/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (reference generators seeded_weight/pseudo_gradient)",
+        "config": workload_config(args, n, world),
+        "hbm_gbs_per_gpu": alg_bytes / (ms_per_step / 1e3) / 1e9,
+        "roofline": {"bound": "hbm", "kernel": "k2_adam (K2 fused unscale+AdamW+cast)",
+                     "achieved": k2_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": k2_gbs / peak, "traffic": traffic,
+                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                     "bytes_per_param": BYTES_PER_PARAM, "params_per_launch": n,
+                     "k2_ms": k2_ms, "k1_ms": k1_ms,
+                     "k1_gbs": 2 * n / (k1_ms / 1e3) / 1e9,
+                     "step_frac": alg_bytes / (ms_per_step / 1e3) / 1e9 / peak},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        cb = cpu_reference_run(min(args.cpu_sample, n), 3, 1, threads)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["host"] = {"cpu": cpu_model(), "nproc": threads}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.params or (LLAMA3_8B if args.config == "cfg2" else CFG1)
+    if args.impl == "reference":
+        reference_arm(args, n, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        ours(args, n, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+/*
+ * memascend_b200.h — C ABI of the B200-native MemAscend optimizer hot path.
+ *
+ * libmemascend_b200.so exports exactly the functions below (plain pointers,
+ * sizes and status codes; no C++ or torch types).  It replaces, on sm_100a,
+ * the reference's CPU hot path in /root/reference/proj:
+ *
+ *   fused_overflow_check   proj/include/memascend/overflow.hpp:56-62, proj/src/overflow.cpp:73-145
+ *   adam_step_fp32         proj/include/memascend/optimizer.hpp:48-50, proj/src/optimizer.cpp:103-109
+ *   adam_step_bf16         proj/include/memascend/optimizer.hpp:54-57, proj/src/optimizer.cpp:111-118
+ *   fp16/bf16 cast-back    proj/include/memascend/halfprec.hpp:25-74, proj/src/simulator.cpp:461-467
+ *   LossScaler + step loop proj/include/memascend/optimizer.hpp:19-35, proj/src/simulator.cpp:427-492
+ *   PinnedAllocator        proj/src/pinned.cpp:98-148 ("registered" becomes cudaHostRegister)
+ *   pseudo_gradient etc.   proj/include/memascend/simulator.hpp:23-42 (synthetic workload)
+ *
+ * The drop-in C++ API (include/memascend/*.hpp, namespace memascend) is a
+ * thin layer over these entry points; INTEGRATION.md shows the ctypes / C++
+ * bindings a maintainer adds.
+ *
+ * Conventions
+ *  - Every function returns 0 (MA_OK) or a status.  Statuses 1..17 are
+ *    1 + memascend::ErrorCode (proj/include/memascend/error.hpp:9-27) so the
+ *    C++ layer rethrows memascend::Error with the same code; MA_ERR_CUDA and
+ *    MA_ERR_NO_DEVICE extend it.  ma_last_error() describes the last failure
+ *    on the calling thread.
+ *  - "_async" functions take a cudaStream_t (as void*) and return once the
+ *    work is enqueued; their pointers must be device-accessible (device
+ *    memory, or host memory registered through ma_host_register /
+ *    cudaHostRegister).  The functions without the suffix are synchronous
+ *    like the reference: they accept device, registered-host or pageable-host
+ *    pointers and return with results visible on the host.
+ *  - Element kinds: MA_DT_F32 / MA_DT_BF16 / MA_DT_F16 (MA_DT_NONE = absent).
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point fails with MA_ERR_NO_DEVICE.
+ */
+#ifndef MEMASCEND_B200_H
+#define MEMASCEND_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define MA_API __attribute__((visibility("default")))
+#else
+#define MA_API
+#endif
+
+enum ma_status {
+    MA_OK = 0,
+    MA_ERR_INVALID_ARGUMENT = 1, /* ErrorCode::invalid_argument */
+    MA_ERR_OUT_OF_MEMORY = 2,
+    MA_ERR_OVERFLOW = 3,
+    MA_ERR_LIFECYCLE = 4,
+    MA_ERR_UNKNOWN_REGION = 5,
+    MA_ERR_POOL_EXHAUSTED = 6,
+    MA_ERR_SIZE_VIOLATION = 7,
+    MA_ERR_ALREADY_CHECKED_OUT = 8,
+    MA_ERR_NOT_FOUND = 9,
+    MA_ERR_STORAGE_FULL = 10,
+    MA_ERR_DEVICE_ERROR = 11,
+    MA_ERR_CAPABILITY = 12,
+    MA_ERR_IO_ERROR = 13,
+    MA_ERR_ALIGNMENT = 14,
+    MA_ERR_BUSY = 15,
+    MA_ERR_UNCALIBRATED = 16,
+    MA_ERR_BAD_CONFIG = 17,
+    MA_ERR_CUDA = 100,      /* a CUDA runtime call failed */
+    MA_ERR_NO_DEVICE = 101  /* no usable sm_100 device: there is no CPU fallback */
+};
+
+enum ma_dtype { MA_DT_F32 = 0, MA_DT_BF16 = 1, MA_DT_F16 = 2, MA_DT_NONE = 3 };
+
+/* AdamHyper, proj/include/memascend/optimizer.hpp:9-15 */
+typedef struct ma_adam_hyper {
+    float lr;
+    float beta1;
+    float beta2;
+    float eps;
+    float weight_decay;
+} ma_adam_hyper;
+
+/* ------------------------------------------------------------------ */
+/* library / device                                                   */
+MA_API const char* ma_last_error(void);
+MA_API int ma_abi_version(void);
+/* Current device ordinal, SM count and compute capability. */
+MA_API int ma_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ------------------------------------------------------------------ */
+/* K1 — fused overflow check (overflow.cpp:73-145).
+ * ORs "all exponent bits set" over n elements of kind g_dtype into *d_flag
+ * (device uint32, NOT cleared here: accumulate several buffers into one flag
+ * and clear it yourself).  d_first_index (device uint64 initialised to
+ * UINT64_MAX, may be NULL) receives atomicMin of the offending indices. */
+MA_API int ma_overflow_check_async(const void* grads, uint64_t n, int g_dtype, uint32_t* d_flag,
+                            uint64_t* d_first_index, void* stream);
+
+/* Synchronous form with the reference's OverflowResult semantics. */
+MA_API int ma_overflow_check(const void* grads, uint64_t n, int g_dtype, int track_first_index,
+                      int* overflow, uint64_t* first_index);
+
+/* ------------------------------------------------------------------ */
+/* K2 — fused unscale + Adam/AdamW + cast-back (optimizer.cpp:26-44,
+ * 103-109; halfprec.hpp:25-74).  p, m, v fp32 in place; g of kind g_dtype;
+ * w_out (kind w_dtype, or MA_DT_NONE) receives the rounded working weights.
+ * bc1/bc2 = 1 - powf(beta, t) are computed on the host with glibc powf
+ * exactly as optimizer.cpp:20-24.  If d_skip_flag != NULL and *d_skip_flag
+ * != 0 when the kernel runs, nothing is touched (the skip step). */
+MA_API int ma_adam_step_async(float* p, float* m, float* v, const void* g, int g_dtype, uint64_t n,
+                       uint64_t t, const ma_adam_hyper* h, float loss_scale, void* w_out,
+                       int w_dtype, const uint32_t* d_skip_flag, void* stream);
+
+/* Synchronous, any memory (device / registered host / pageable host). */
+MA_API int ma_adam_step(float* p, float* m, float* v, const void* g, int g_dtype, uint64_t n,
+                 uint64_t t, const ma_adam_hyper* h, float loss_scale, void* w_out, int w_dtype);
+
+/* K3 — bf16 optimizer state (optimizer.cpp:83-93,111-118), synchronous. */
+MA_API int ma_adam_step_bf16(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
+                      uint64_t t, const ma_adam_hyper* h, float loss_scale);
+
+/* ------------------------------------------------------------------ */
+/* Step driver: the composition of simulator.cpp:427-492 with the loss
+ * scaler kept on the device, so a whole step (check -> optional cross-rank
+ * OR -> update -> scaler) is enqueued without a host round trip.
+ *
+ *   per step:  ma_stepper_check_async(...)   for every gradient buffer
+ *              [allreduce(max) of *ma_stepper_flag(s) across ranks]
+ *              ma_stepper_apply_async(...)   for every sub-group
+ *              ma_stepper_finish_async(...)  scaler + counters, re-arms
+ *
+ * t (the Adam step) counts APPLIED updates, not steps
+ * (simulator.cpp:360,444,456).  bc1/bc2 come from a host-computed glibc-powf
+ * table indexed on the device by t. */
+typedef struct ma_stepper ma_stepper;
+
+typedef struct ma_subgroup {
+    float* p;         /* fp32 master */
+    float* m;         /* fp32 momentum */
+    float* v;         /* fp32 variance */
+    const void* g;    /* scaled gradients, stepper g_dtype */
+    void* w;          /* working weights, stepper w_dtype (NULL if MA_DT_NONE) */
+    uint64_t n;
+} ma_subgroup;
+
+typedef struct ma_step_state {
+    float scale;           /* LossScaler::scale after the last finished step */
+    uint32_t clean_steps;  /* LossScaler::clean_steps */
+    uint64_t updates;      /* applied updates (Adam t of the last update) */
+    uint64_t steps;        /* finished steps */
+    uint32_t last_overflow;
+    uint32_t growth_interval;
+} ma_step_state;
+
+/* d_state: optional caller-owned device buffer of MA_STEPPER_STATE_BYTES
+ * (e.g. a framework tensor, so the flag can be all-reduced in place); NULL
+ * lets the library allocate it.  Layout: uint32 flag at byte 0, float scale
+ * at byte 8 (see ma_stepper_flag / ma_stepper_scale). */
+#define MA_STEPPER_STATE_BYTES 64
+MA_API int ma_stepper_create(const ma_adam_hyper* h, float init_scale, uint32_t growth_interval,
+                      int g_dtype, int w_dtype, void* d_state, ma_stepper** out);
+MA_API int ma_stepper_destroy(ma_stepper* s);
+MA_API int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void* stream);
+/* Host-buffer ingest: copies the step's gradients from PINNED host memory
+ * into dev_g on copy_stream in chunk_elems pieces and runs K1 on each piece
+ * on `stream` as soon as it lands, so the check overlaps the PCIe transfer
+ * (the staged H2D of PAPER.md §4.4 / north-star item (1)). */
+MA_API int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
+                                       uint64_t chunk_elems, void* stream, void* copy_stream);
+/* Device uint32 holding this step's overflow flag (for the cross-rank OR). */
+MA_API uint32_t* ma_stepper_flag(ma_stepper* s);
+/* Device float holding the current loss scale (gradient producers read it). */
+MA_API float* ma_stepper_scale(ma_stepper* s);
+MA_API int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
+                           void* stream);
+MA_API int ma_stepper_finish_async(ma_stepper* s, void* stream);
+/* Synchronises the stepper's last stream and reads the scaler state. */
+MA_API int ma_stepper_state(ma_stepper* s, ma_step_state* out);
+/* Per-step log (overflow flag, scale after the step) of the most recent
+ * min(count, 65536) steps, oldest first. */
+MA_API int ma_stepper_history(ma_stepper* s, uint8_t* overflow, float* scale_after, uint64_t cap,
+                       uint64_t* count);
+
+/* ------------------------------------------------------------------ */
+/* Synthetic workload generators, bit-exact with simulator.hpp:23-42.
+ * Element i of the buffer is global element (base + i). */
+MA_API int ma_gen_seeded_weights_async(float* p, void* w, int w_dtype, uint64_t n, uint64_t base,
+                                uint64_t seed, void* stream);
+/* g[i] = cast(pseudo_gradient(seed, step, base+i, widen(w[i])) * scale);
+ * scale is read from d_scale when non-NULL (e.g. ma_stepper_scale). */
+MA_API int ma_gen_pseudo_grads_async(void* g, int g_dtype, const void* w, int w_dtype, uint64_t n,
+                              uint64_t base, uint64_t seed, uint64_t step,
+                              const float* d_scale, float scale, void* stream);
+/* Plants one raw bit pattern (32-bit for F32, low 16 bits otherwise). */
+MA_API int ma_plant_bits_async(void* buf, int dtype, uint64_t index, uint32_t bits, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Host memory (PinnedAllocator, pinned.cpp:98-148): page-lock an existing
+ * allocation for DMA and device access (cudaHostRegisterPortable|Mapped). */
+MA_API int ma_host_register(void* ptr, uint64_t bytes);
+MA_API int ma_host_unregister(void* ptr);
+/* 1 if ptr is device memory, 2 registered/pinned host, 0 pageable host. */
+MA_API int ma_pointer_kind(const void* ptr, int* kind);
+
+/* ------------------------------------------------------------------ */
+/* Verification hooks (used by tests/; they run the product device code). */
+/* FNV-1a-64 of every 2^block_log2 consecutive fp32->kind conversions over
+ * all 2^32 inputs, through the same device cast K2 uses; out_host has
+ * 2^(32-block_log2) entries. */
+MA_API int ma_debug_cast_sweep(int kind, int block_log2, uint64_t* out_host);
+/* Number of 32-bit (kind F32) or 16-bit patterns where K1's predicate
+ * disagrees with !isfinite(); exhaustive. */
+MA_API int ma_debug_mask_sweep(int kind, uint64_t* mismatches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MEMASCEND_B200_H */

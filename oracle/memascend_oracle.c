@@ -496,3 +496,80 @@ void ora_adversarial_buffer(ora_mt64* rng, uint32_t* out, uint64_t n, int inject
         out[where] = bad[which];
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Bulk fills (CPU baseline inputs); elementwise, so thread splits do not
+ * change the values. */
+typedef struct {
+    int what;
+    float* p;
+    uint16_t* w;
+    void* g;
+    float* g32;
+    const uint16_t* wr;
+    uint64_t lo, hi, base, seed, step;
+    float scale;
+    int g_kind, w_kind;
+} fill_job;
+
+static void* fill_worker(void* arg) {
+    fill_job* j = (fill_job*)arg;
+    for (uint64_t i = j->lo; i < j->hi; ++i) {
+        if (j->what == 0) {
+            const float x = ora_seeded_weight(j->seed, j->base + i);
+            if (j->p) j->p[i] = x;
+            if (j->w) j->w[i] = narrow(x, j->w_kind);
+        } else {
+            const float pg = ora_pseudo_gradient(j->seed, j->step, j->base + i,
+                                                 widen(j->wr[i], j->w_kind));
+            const float gs = pg * j->scale;
+            float wide = gs;
+            if (j->g_kind == ORA_F32) {
+                if (j->g) ((float*)j->g)[i] = gs;
+            } else {
+                const uint16_t b = ora_bf16_from_float(gs);
+                if (j->g) ((uint16_t*)j->g)[i] = b;
+                wide = ora_bf16_to_float(b);
+            }
+            if (j->g32) j->g32[i] = wide;
+        }
+    }
+    return NULL;
+}
+
+static void run_fill(fill_job proto, uint64_t n, int threads) {
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t tid[256];
+    fill_job jobs[256];
+    const uint64_t per = (n + (uint64_t)threads - 1) / (uint64_t)threads;
+    int k = 0;
+    for (int t = 0; t < threads; ++t) {
+        const uint64_t lo = (uint64_t)t * per;
+        const uint64_t hi = lo + per < n ? lo + per : n;
+        if (lo >= hi) break;
+        jobs[t] = proto;
+        jobs[t].lo = lo;
+        jobs[t].hi = hi;
+        pthread_create(&tid[t], NULL, fill_worker, &jobs[t]);
+        ++k;
+    }
+    for (int t = 0; t < k; ++t) pthread_join(tid[t], NULL);
+}
+
+void ora_fill_weights(float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed, int w_kind,
+                      int threads) {
+    fill_job j;
+    memset(&j, 0, sizeof j);
+    j.what = 0; j.p = p; j.w = w; j.base = base; j.seed = seed; j.w_kind = w_kind;
+    run_fill(j, n, threads);
+}
+
+void ora_fill_grads(void* g, float* g32, const uint16_t* w, uint64_t n, uint64_t base,
+                    uint64_t seed, uint64_t step, float scale, int g_kind, int w_kind, int threads) {
+    fill_job j;
+    memset(&j, 0, sizeof j);
+    j.what = 1; j.g = g; j.g32 = g32; j.wr = w; j.base = base; j.seed = seed; j.step = step;
+    j.scale = scale; j.g_kind = g_kind; j.w_kind = w_kind;
+    run_fill(j, n, threads);
+}

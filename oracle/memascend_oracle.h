@@ -146,6 +146,15 @@ int ora_train(const ora_train_cfg* cfg, ora_train_out* out);
 int ora_train_sample(const ora_train_cfg* cfg, const uint64_t* indices, uint64_t k,
                      const uint8_t* decisions, float* p, float* m, float* v, uint16_t* w);
 
+/* Bulk workload fill for the CPU baseline (threads > 1 splits the range):
+ * p[i] = seeded_weight(seed, base+i) (p may be NULL), w[i] = cast(p[i]);
+ * g[i] = stored pseudo-gradient (g_kind ORA_F32: fp32, ORA_BF16: bf16 bits),
+ * and, when g32 != NULL, its exact fp32 widening (the reference flat buffer). */
+void ora_fill_weights(float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed, int w_kind,
+                      int threads);
+void ora_fill_grads(void* g, float* g32, const uint16_t* w, uint64_t n, uint64_t base,
+                    uint64_t seed, uint64_t step, float scale, int g_kind, int w_kind, int threads);
+
 /* ---- misc -------------------------------------------------------------- */
 uint64_t ora_fnv1a64(const void* data, uint64_t bytes);                  /* simulator.cpp:182-192 */
 uint64_t ora_fnv1a64_continue(uint64_t h, const void* data, uint64_t bytes);

@@ -109,6 +109,10 @@ def lib():
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ora_fnv1a64.restype = C.c_uint64
         L.ora_fnv1a64.argtypes = [C.c_void_p, C.c_uint64]
+        L.ora_fill_weights.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                       C.c_int, C.c_int]
+        L.ora_fill_grads.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                     C.c_uint64, C.c_uint64, C.c_float, C.c_int, C.c_int, C.c_int]
         L.ora_mt64_seed.argtypes = [C.POINTER(MT64), C.c_uint64]
         L.ora_mt64_next.restype = C.c_uint64
         L.ora_mt64_next.argtypes = [C.POINTER(MT64)]
@@ -237,6 +241,24 @@ def train_sample(indices, decisions, steps, seed, g_kind="bf16", w_kind="bf16", 
         raise ValueError(f"ora_train_sample failed: {r}")
     del keep
     return {"p": p, "m": m, "v": v, "w": w}
+
+
+def fill_weights(n, base=0, seed=1, w_kind="bf16", threads=None):
+    p = np.empty(n, np.float32)
+    w = np.empty(n, np.uint16)
+    lib().ora_fill_weights(_ptr(p), _ptr(w), n, base, seed, KIND[w_kind], threads or os.cpu_count())
+    return p, w
+
+
+def fill_grads(w, step, base=0, seed=1, scale=65536.0, g_kind="bf16", w_kind="bf16",
+               widened=True, threads=None):
+    """Returns (stored grads, fp32 widening or None)."""
+    n = w.size
+    g = np.empty(n, np.float32 if g_kind == "f32" else np.uint16)
+    g32 = np.empty(n, np.float32) if widened else None
+    lib().ora_fill_grads(_ptr(g), _ptr(g32), _ptr(w), n, base, seed, step, scale, KIND[g_kind],
+                         KIND[w_kind], threads or os.cpu_count())
+    return g, g32
 
 
 class MT19937_64:

@@ -1,0 +1,289 @@
+"""Python mirror of the reference hot-path interface over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference's C++ API
+(proj/include/memascend/{overflow,optimizer}.hpp) so tests read like the
+reference's own tests; tensors are torch tensors (device or host) or numpy
+arrays (host).  Everything computes in libmemascend_b200.so on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import capi
+from .capi import AdamHyper, MemAscendError, check  # noqa: F401  (re-exported)
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+_TORCH_DT = {}
+if torch is not None:
+    _TORCH_DT = {torch.float32: capi.DT_F32, torch.bfloat16: capi.DT_BF16,
+                 torch.float16: capi.DT_F16}
+_NP_DT = {np.dtype(np.float32): capi.DT_F32, np.dtype(np.float16): capi.DT_F16}
+
+
+def _info(x, kind=None):
+    """(pointer, element count, dtype code) of a tensor / array / None."""
+    if x is None:
+        return None, 0, capi.DT_NONE
+    if torch is not None and isinstance(x, torch.Tensor):
+        if not x.is_contiguous():
+            raise MemAscendError(1, "tensor must be contiguous")
+        dt = capi.DTYPES[kind] if kind else _TORCH_DT.get(x.dtype)
+        if dt is None:
+            raise MemAscendError(1, f"unsupported dtype {x.dtype} (pass kind=)")
+        return x.data_ptr(), x.numel(), dt
+    a = x
+    if not a.flags["C_CONTIGUOUS"]:
+        raise MemAscendError(1, "array must be C-contiguous")
+    dt = capi.DTYPES[kind] if kind else _NP_DT.get(a.dtype)
+    if dt is None:
+        raise MemAscendError(1, f"unsupported dtype {a.dtype} (pass kind=)")
+    return a.ctypes.data, a.size, dt
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream if torch is not None else None
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+# ----------------------------------------------------------------- K1
+@dataclass
+class OverflowResult:
+    """overflow.hpp:41-44"""
+
+    overflow: bool = False
+    first_offending_index: int | None = None
+
+
+def fused_overflow_check(values, track_first_index: bool = False, kind: str | None = None):
+    """overflow.hpp:56-62 / overflow.cpp:73-145 on the GPU (K1)."""
+    ptr, n, dt = _info(values, kind)
+    of, first = C.c_int(), C.c_uint64()
+    check(capi.lib().ma_overflow_check(ptr, n, dt, int(track_first_index), C.byref(of),
+                                       C.byref(first)))
+    res = OverflowResult(bool(of.value))
+    if track_first_index and of.value:
+        res.first_offending_index = first.value
+    return res
+
+
+def overflow_check_async(values, d_flag, d_first=None, kind=None, stream=None):
+    ptr, n, dt = _info(values, kind)
+    check(capi.lib().ma_overflow_check_async(ptr, n, dt, d_flag.data_ptr(),
+                                             d_first.data_ptr() if d_first is not None else None,
+                                             _stream_ptr(stream)))
+
+
+# ----------------------------------------------------------------- K2/K3
+def adam_step_fp32(params, momentum, variance, grads, t: int, hyper: AdamHyper | None = None,
+                   loss_scale: float = 1.0, w_out=None, grad_kind=None, w_kind=None):
+    """optimizer.hpp:48-50 / optimizer.cpp:103-109 (+ the cast-back into w_out)."""
+    hyper = hyper or AdamHyper()
+    pp, n, _ = _info(params)
+    mp, nm, _ = _info(momentum)
+    vp, nv, _ = _info(variance)
+    gp, ng, gdt = _info(grads, grad_kind)
+    wp, nw, wdt = _info(w_out, w_kind)
+    if not (n == nm == nv == ng) or (w_out is not None and nw != n):
+        raise MemAscendError(1, "adam_step: parameter/state/grad lengths differ")
+    check(capi.lib().ma_adam_step(pp, mp, vp, gp, gdt, n, t, C.byref(hyper), loss_scale, wp,
+                                  wdt))
+
+
+def adam_step_fp32_async(params, momentum, variance, grads, t, hyper=None, loss_scale=1.0,
+                         w_out=None, skip_flag=None, stream=None, grad_kind=None, w_kind=None):
+    hyper = hyper or AdamHyper()
+    gp, n, gdt = _info(grads, grad_kind)
+    wp, _, wdt = _info(w_out, w_kind)
+    check(capi.lib().ma_adam_step_async(params.data_ptr(), momentum.data_ptr(),
+                                        variance.data_ptr(), gp, gdt, n, t, C.byref(hyper),
+                                        loss_scale, wp, wdt,
+                                        skip_flag.data_ptr() if skip_flag is not None else None,
+                                        _stream_ptr(stream)))
+
+
+def adam_step_bf16(params, momentum, variance, grads, t: int, hyper: AdamHyper | None = None,
+                   loss_scale: float = 1.0):
+    """optimizer.hpp:54-57 / optimizer.cpp:111-118 (bf16 state as raw uint16 bits)."""
+    hyper = hyper or AdamHyper()
+    pp, n, _ = _info(params, "bf16")
+    mp, nm, _ = _info(momentum, "bf16")
+    vp, nv, _ = _info(variance, "bf16")
+    gp, ng, _ = _info(grads, "f32")
+    if not (n == nm == nv == ng):
+        raise MemAscendError(1, "adam_step: parameter/state/grad lengths differ")
+    check(capi.lib().ma_adam_step_bf16(pp, mp, vp, gp, n, t, C.byref(hyper), loss_scale))
+
+
+@dataclass
+class OptimizerState:
+    """optimizer.hpp:60-66"""
+
+    master_params: object
+    momentum_m: object
+    variance_v: object
+    step_t: int = 0
+    hyper: AdamHyper | None = None
+
+
+def adam_step(state: OptimizerState, grads, scale: float) -> None:
+    """optimizer.cpp:120-124: increments step_t, then the fp32 step."""
+    state.step_t += 1
+    adam_step_fp32(state.master_params, state.momentum_m, state.variance_v, grads, state.step_t,
+                   state.hyper or AdamHyper(), scale)
+
+
+# ----------------------------------------------------------------- step driver
+class Stepper:
+    """Device-resident composition of simulator.cpp:427-492 (see the header).
+
+    The scaler state lives in a 64-byte torch uint8 tensor so the overflow
+    flag can be all-reduced in place (``flag`` is an int32 view of byte 0).
+    """
+
+    def __init__(self, hyper: AdamHyper | None = None, init_scale: float = 65536.0,
+                 growth_interval: int = 2000, g_dtype: str = "bf16", w_dtype: str = "bf16",
+                 device=None):
+        self.hyper = hyper or AdamHyper()
+        self.g_dtype, self.w_dtype = g_dtype, w_dtype
+        self.state_t = torch.zeros(capi.STEPPER_STATE_BYTES, dtype=torch.uint8,
+                                   device=device or "cuda")
+        self.flag = self.state_t[0:4].view(torch.int32)
+        self.scale_t = self.state_t[8:12].view(torch.float32)
+        h = C.c_void_p()
+        check(capi.lib().ma_stepper_create(C.byref(self.hyper), init_scale, growth_interval,
+                                           capi.DTYPES[g_dtype], capi.DTYPES[w_dtype],
+                                           self.state_t.data_ptr(), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if self._h:
+            capi.lib().ma_stepper_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, grads, stream=None):
+        check(capi.lib().ma_stepper_check_async(self._h, grads.data_ptr(), grads.numel(),
+                                                _stream_ptr(stream)))
+
+    def check_from_host(self, host_g, dev_g, chunk_elems=64 << 20, stream=None,
+                        copy_stream=None):
+        """H2D of pinned host gradients into dev_g, K1 overlapped per chunk."""
+        if copy_stream is None:
+            copy_stream = self._copy_stream = getattr(self, "_copy_stream", None) or \
+                torch.cuda.Stream(device=dev_g.device)
+        check(capi.lib().ma_stepper_check_host_async(
+            self._h, host_g.data_ptr(), dev_g.data_ptr(), dev_g.numel(), chunk_elems,
+            _stream_ptr(stream), _stream_ptr(copy_stream)))
+
+    @staticmethod
+    def subgroups(groups):
+        arr = (capi.Subgroup * len(groups))()
+        for k, (p, m, v, g, w) in enumerate(groups):
+            arr[k] = capi.Subgroup(p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
+                                   w.data_ptr() if w is not None else None, p.numel())
+        return arr
+
+    def apply(self, groups, stream=None):
+        """groups: list of (p, m, v, g, w) tensors, or a prebuilt subgroups() array."""
+        arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
+        check(capi.lib().ma_stepper_apply_async(self._h, arr, len(arr), _stream_ptr(stream)))
+
+    def finish(self, stream=None):
+        check(capi.lib().ma_stepper_finish_async(self._h, _stream_ptr(stream)))
+
+    def step(self, grads_list, groups, allreduce=None, stream=None):
+        """One full step: check every grad buffer, optional cross-rank OR, update, scaler."""
+        for g in grads_list:
+            self.check(g, stream)
+        if allreduce is not None:
+            allreduce(self.flag)
+        self.apply(groups, stream)
+        self.finish(stream)
+
+    def state(self) -> dict:
+        s = capi.StepState()
+        check(capi.lib().ma_stepper_state(self._h, C.byref(s)))
+        return {"scale": s.scale, "clean_steps": s.clean_steps, "updates": s.updates,
+                "steps": s.steps, "last_overflow": s.last_overflow,
+                "growth_interval": s.growth_interval}
+
+    def history(self, cap: int = 65536):
+        of = np.zeros(cap, np.uint8)
+        sc = np.zeros(cap, np.float32)
+        cnt = C.c_uint64()
+        check(capi.lib().ma_stepper_history(self._h, of.ctypes.data, sc.ctypes.data, cap,
+                                            C.byref(cnt)))
+        return of[:cnt.value].astype(bool), sc[:cnt.value]
+
+
+# ----------------------------------------------------------------- workload
+def gen_seeded_weights(p, w, n=None, base=0, seed=1, w_kind=None, stream=None):
+    wp, _, wdt = _info(w, w_kind)
+    n = n if n is not None else (p.numel() if p is not None else w.numel())
+    check(capi.lib().ma_gen_seeded_weights_async(p.data_ptr() if p is not None else None, wp,
+                                                 wdt, n, base, seed, _stream_ptr(stream)))
+
+
+def gen_pseudo_grads(g, w, step, base=0, seed=1, scale=65536.0, d_scale=None, g_kind=None,
+                     w_kind=None, stream=None):
+    gp, n, gdt = _info(g, g_kind)
+    wp, _, wdt = _info(w, w_kind)
+    check(capi.lib().ma_gen_pseudo_grads_async(gp, gdt, wp, wdt, n, base, seed, step,
+                                               d_scale.data_ptr() if d_scale is not None else None,
+                                               scale, _stream_ptr(stream)))
+
+
+def plant_bits(buf, index, bits, kind=None, stream=None):
+    bp, _, dt = _info(buf, kind)
+    check(capi.lib().ma_plant_bits_async(bp, dt, index, bits, _stream_ptr(stream)))
+
+
+# ----------------------------------------------------------------- host memory
+def host_register(array) -> None:
+    """PinnedAllocator's "registered" state, made real (pinned.cpp:122-124)."""
+    ptr, n, _ = _info(array)
+    nbytes = array.nbytes if hasattr(array, "nbytes") else array.numel() * array.element_size()
+    check(capi.lib().ma_host_register(ptr, nbytes))
+
+
+def host_unregister(array) -> None:
+    ptr, _, _ = _info(array)
+    check(capi.lib().ma_host_unregister(ptr))
+
+
+def pointer_kind(x) -> int:
+    ptr, _, _ = _info(x)
+    k = C.c_int()
+    check(capi.lib().ma_pointer_kind(ptr, C.byref(k)))
+    return k.value
+
+
+def device_info() -> dict:
+    d, s, a, b = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    check(capi.lib().ma_device_info(C.byref(d), C.byref(s), C.byref(a), C.byref(b)))
+    return {"device": d.value, "sm_count": s.value, "cc": (a.value, b.value)}
+
+
+def debug_cast_sweep(kind: str, block_log2: int = 20) -> np.ndarray:
+    out = np.zeros(1 << (32 - block_log2), np.uint64)
+    check(capi.lib().ma_debug_cast_sweep(capi.DTYPES[kind], block_log2, out.ctypes.data))
+    return out
+
+
+def debug_mask_sweep(kind: str) -> int:
+    mm = C.c_uint64()
+    check(capi.lib().ma_debug_mask_sweep(capi.DTYPES[kind], C.byref(mm)))
+    return mm.value

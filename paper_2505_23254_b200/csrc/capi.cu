@@ -1,0 +1,879 @@
+// Host side of the C ABI declared in include/memascend_b200.h.
+//
+// Launch planning, memory classification (device / registered host /
+// pageable host), the staging path for pageable spans, and the device-
+// resident step driver.  Every entry point converts failures to a status
+// code plus a thread-local message; nothing here falls back to the CPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstddef>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "memascend_b200.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Status {
+    int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+    g_err = msg;
+    throw Status{code};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(e == cudaErrorMemoryAllocation ? MA_ERR_OUT_OF_MEMORY : MA_ERR_CUDA,
+             std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+#define CK(call) cuda_check((call), #call)
+
+template <typename F>
+int guarded(F&& fn) {
+    try {
+        fn();
+        return MA_OK;
+    } catch (const Status& s) {
+        return s.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MA_ERR_DEVICE_ERROR;
+    }
+}
+
+struct DeviceInfo {
+    int device = -1;
+    int sms = 0;
+    int major = 0;
+    int minor = 0;
+};
+
+DeviceInfo device_info() {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        fail(MA_ERR_NO_DEVICE,
+             "no CUDA device visible: the memascend B200 path has no CPU fallback");
+    }
+    DeviceInfo d;
+    CK(cudaGetDevice(&d.device));
+    static std::mutex mu;
+    static std::vector<DeviceInfo> cache(64);
+    std::lock_guard<std::mutex> lock(mu);
+    DeviceInfo& c = cache[static_cast<size_t>(d.device) % cache.size()];
+    if (c.device != d.device) {
+        CK(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, d.device));
+        CK(cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, d.device));
+        CK(cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, d.device));
+        if (d.major != 10) {
+            fail(MA_ERR_CAPABILITY, "device " + std::to_string(d.device) + " is sm_" +
+                                        std::to_string(d.major * 10 + d.minor) +
+                                        "; this build targets sm_100a (B200) only");
+        }
+        c = d;
+    }
+    return c;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int elem_bytes(int dt) { return dt == MA_DT_F32 ? 4 : 2; }
+
+void check_grad_dtype(int dt) {
+    if (dt != MA_DT_F32 && dt != MA_DT_BF16 && dt != MA_DT_F16)
+        fail(MA_ERR_INVALID_ARGUMENT, "gradient dtype must be F32, BF16 or F16");
+}
+
+void check_w_dtype(int dt) {
+    if (dt != MA_DT_NONE && dt != MA_DT_BF16 && dt != MA_DT_F16)
+        fail(MA_ERR_INVALID_ARGUMENT, "working-weight dtype must be BF16, F16 or NONE");
+}
+
+// 0 pageable host, 1 device/managed, 2 registered host; *dev gets the
+// device-accessible alias.
+int classify(const void* p, const void** dev) {
+    *dev = p;
+    if (p == nullptr) return 1;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    switch (at.type) {
+        case cudaMemoryTypeDevice:
+        case cudaMemoryTypeManaged:
+            return 1;
+        case cudaMemoryTypeHost:
+            *dev = at.devicePointer ? at.devicePointer : p;
+            return 2;
+        default:
+            return 0;
+    }
+}
+
+// ------------------------------------------------------------ scratch
+// Grow-only device scratch + a library stream for the synchronous entry
+// points (pageable staging, result flags).
+struct Scratch {
+    std::mutex mu;
+    void* dev = nullptr;
+    size_t bytes = 0;
+    cudaStream_t stream = nullptr;
+    int device = -1;
+
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (dev) CK(cudaFree(dev));
+            dev = nullptr;
+            bytes = 0;
+            CK(cudaMalloc(&dev, need));
+            bytes = need;
+        }
+        return dev;
+    }
+    cudaStream_t strm() {
+        if (!stream) CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        return stream;
+    }
+};
+
+Scratch& scratch() {
+    static Scratch s[16];
+    int d = 0;
+    cudaGetDevice(&d);
+    return s[d % 16];
+}
+
+// ------------------------------------------------------------ K1 launch
+void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* first,
+               uint64_t index_base, bool early_exit, cudaStream_t st) {
+    if (n == 0) return;
+    const DeviceInfo d = device_info();
+    const uint32_t es = static_cast<uint32_t>(elem_bytes(dt));
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(data);
+    if (addr % es) fail(MA_ERR_ALIGNMENT, "gradient buffer is not element-aligned");
+    ma::K1Args a{};
+    a.raw = data;
+    a.n = n;
+    a.head = std::min<uint64_t>(((16 - (addr & 15)) & 15) / es, n);
+    a.nvec = (n - a.head) * es / 16;
+    a.body = reinterpret_cast<const uint4*>(addr + a.head * es);
+    a.index_base = index_base;
+    a.flag = flag;
+    a.first = first;
+    a.kind = dt;
+    a.elem_bytes = es;
+    a.early_exit = early_exit ? 1 : 0;
+    const uint64_t per_cta = static_cast<uint64_t>(ma::kK1Threads) * ma::kK1Unroll;
+    const uint64_t want = std::max<uint64_t>(1, (a.nvec + per_cta - 1) / per_cta);
+    const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(d.sms) * 8);
+    if (first) {
+        ma::k1_overflow<true><<<static_cast<unsigned>(grid), ma::kK1Threads, 0, st>>>(a);
+    } else {
+        ma::k1_overflow<false><<<static_cast<unsigned>(grid), ma::kK1Threads, 0, st>>>(a);
+    }
+    CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ K2 planning
+int k2_vec() {
+    static const int v = [] {
+        const char* e = std::getenv("MA_K2_VEC");
+        return (e && std::atoi(e) == 4) ? 4 : 8;
+    }();
+    return v;
+}
+
+bool aligned(const void* p, uint64_t h, uint32_t es, uint32_t need) {
+    return p == nullptr || ((reinterpret_cast<uintptr_t>(p) + h * es) % need) == 0;
+}
+
+ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, uint64_t tile_begin) {
+    ma::Seg s{};
+    s.p = g.p;
+    s.m = g.m;
+    s.v = g.v;
+    s.g = g.g;
+    s.w = wdt == MA_DT_NONE ? nullptr : g.w;
+    s.n = g.n;
+    const uint32_t ges = static_cast<uint32_t>(elem_bytes(gdt));
+    const uint32_t gneed = ges * static_cast<uint32_t>(vec) >= 16 ? 16u : ges * vec;
+    const uint32_t wneed = 2u * static_cast<uint32_t>(vec) >= 16 ? 16u : 2u * vec;
+    s.vector_ok = 0;
+    for (uint64_t h = 0; h < static_cast<uint64_t>(vec) && h <= g.n; ++h) {
+        if (aligned(g.p, h, 4, 16) && aligned(g.m, h, 4, 16) && aligned(g.v, h, 4, 16) &&
+            aligned(g.g, h, ges, gneed) && aligned(s.w, h, 2, wneed)) {
+            s.vector_ok = 1;
+            s.head = h;
+            break;
+        }
+    }
+    const uint64_t tile_elems = static_cast<uint64_t>(ma::kK2Threads) * vec;
+    uint64_t tiles;
+    if (s.vector_ok) {
+        s.nvec = (g.n - s.head) / vec;
+        tiles = std::max<uint64_t>(1, (s.nvec + ma::kK2Threads - 1) / ma::kK2Threads);
+    } else {
+        s.nvec = 0;
+        tiles = (g.n + tile_elems - 1) / tile_elems;
+    }
+    s.tile_begin = tile_begin;
+    s.tile_end = tile_begin + tiles;
+    return s;
+}
+
+template <int GK, int WK, int VEC>
+void launch_k2_t(const ma::SegTable& tab, const ma::AdamArgs& a, cudaStream_t st, int sms) {
+    static int blocks_per_sm = [] {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ma::k2_adam<GK, WK, VEC>,
+                                                      ma::kK2Threads, 0);
+        return std::max(1, b);
+    }();
+    const uint64_t grid = std::min<uint64_t>(tab.total_tiles,
+                                             static_cast<uint64_t>(sms) * blocks_per_sm);
+    ma::k2_adam<GK, WK, VEC><<<static_cast<unsigned>(grid), ma::kK2Threads, 0, st>>>(tab, a);
+}
+
+template <int GK, int WK>
+void launch_k2_w(const ma::SegTable& tab, const ma::AdamArgs& a, cudaStream_t st, int sms,
+                 int vec) {
+    if (vec == 4) {
+        launch_k2_t<GK, WK, 4>(tab, a, st, sms);
+    } else {
+        launch_k2_t<GK, WK, 8>(tab, a, st, sms);
+    }
+}
+
+template <int GK>
+void launch_k2_g(int wdt, const ma::SegTable& tab, const ma::AdamArgs& a, cudaStream_t st,
+                 int sms, int vec) {
+    switch (wdt) {
+        case MA_DT_NONE: launch_k2_w<GK, ma::kNone>(tab, a, st, sms, vec); break;
+        case MA_DT_BF16: launch_k2_w<GK, ma::kBF16>(tab, a, st, sms, vec); break;
+        default: launch_k2_w<GK, ma::kF16>(tab, a, st, sms, vec); break;
+    }
+}
+
+void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, const ma::AdamArgs& a,
+               cudaStream_t st) {
+    const DeviceInfo d = device_info();
+    const int vec = k2_vec();
+    for (uint32_t first = 0; first < count; first += ma::kMaxSegs) {
+        ma::SegTable tab{};
+        uint64_t tiles = 0;
+        const uint32_t last = std::min<uint32_t>(count, first + ma::kMaxSegs);
+        for (uint32_t k = first; k < last; ++k) {
+            if (groups[k].n == 0) continue;
+            if (!groups[k].p || !groups[k].m || !groups[k].v || !groups[k].g)
+                fail(MA_ERR_INVALID_ARGUMENT, "sub-group with a null state/grad pointer");
+            if (wdt != MA_DT_NONE && !groups[k].w)
+                fail(MA_ERR_INVALID_ARGUMENT, "sub-group without a working-weight buffer");
+            tab.seg[tab.count] = plan_seg(groups[k], gdt, wdt, vec, tiles);
+            tiles = tab.seg[tab.count].tile_end;
+            tab.count += 1;
+        }
+        if (tab.count == 0) continue;
+        tab.total_tiles = tiles;
+        switch (gdt) {
+            case MA_DT_F32: launch_k2_g<ma::kF32>(wdt, tab, a, st, d.sms, vec); break;
+            case MA_DT_BF16: launch_k2_g<ma::kBF16>(wdt, tab, a, st, d.sms, vec); break;
+            default: launch_k2_g<ma::kF16>(wdt, tab, a, st, d.sms, vec); break;
+        }
+        CK(cudaGetLastError());
+    }
+}
+
+// optimizer.cpp:20-24 on the host: glibc powf, float exponent.
+void bias_corrections(uint64_t t, float b1, float b2, float* bc1, float* bc2) {
+    const float tf = static_cast<float>(t);
+    *bc1 = 1.0f - std::pow(b1, tf);
+    *bc2 = 1.0f - std::pow(b2, tf);
+}
+
+ma::AdamConsts make_consts(const ma_adam_hyper* h) {
+    if (!h) fail(MA_ERR_INVALID_ARGUMENT, "null hyper-parameters");
+    ma::AdamConsts c{};
+    c.lr = h->lr;
+    c.beta1 = h->beta1;
+    c.beta2 = h->beta2;
+    c.eps = h->eps;
+    // (1.0f - beta) and lr * wd as the reference evaluates them (fp32)
+    volatile float one = 1.0f;
+    c.one_minus_b1 = one - h->beta1;
+    c.one_minus_b2 = one - h->beta2;
+    volatile float lr = h->lr;
+    c.lr_wd = lr * h->weight_decay;
+    return c;
+}
+
+ma::AdamArgs explicit_args(const ma_adam_hyper* h, uint64_t t, float scale, const uint32_t* skip) {
+    if (t == 0) fail(MA_ERR_INVALID_ARGUMENT, "adam step count t must be >= 1");
+    ma::AdamArgs a{};
+    a.c = make_consts(h);
+    a.scale = scale;
+    bias_corrections(t, h->beta1, h->beta2, &a.bc1, &a.bc2);
+    a.skip = skip;
+    return a;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+struct ma_stepper {
+    ma::AdamConsts c{};
+    ma_adam_hyper h{};
+    int g_dtype = MA_DT_BF16;
+    int w_dtype = MA_DT_BF16;
+    ma::StepDev* d_st = nullptr;
+    ma::StepLog* d_log = nullptr;
+    float2* d_bc = nullptr;
+    uint64_t bc_cap = 0;
+    uint64_t issued = 0;  // finish calls enqueued
+    cudaStream_t last = nullptr;
+    int device = 0;
+    bool owns_state = true;
+    std::vector<cudaEvent_t> events;
+
+    cudaEvent_t event(uint64_t i) {
+        while (events.size() <= i) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            events.push_back(e);
+        }
+        return events[i];
+    }
+    ~ma_stepper() {
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+void stepper_grow_bc(ma_stepper* s, uint64_t need) {
+    if (need <= s->bc_cap) return;
+    uint64_t cap = std::max<uint64_t>(s->bc_cap ? s->bc_cap * 2 : 65536, need);
+    std::vector<float2> host(cap);
+    for (uint64_t t = 1; t <= cap; ++t) {
+        bias_corrections(t, s->h.beta1, s->h.beta2, &host[t - 1].x, &host[t - 1].y);
+    }
+    float2* fresh = nullptr;
+    CK(cudaMalloc(&fresh, cap * sizeof(float2)));
+    CK(cudaMemcpy(fresh, host.data(), cap * sizeof(float2), cudaMemcpyHostToDevice));
+    if (s->d_bc) {
+        CK(cudaDeviceSynchronize());  // in-flight steps may still read the old table
+        CK(cudaFree(s->d_bc));
+    }
+    s->d_bc = fresh;
+    s->bc_cap = cap;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ma_last_error(void) { return g_err.c_str(); }
+
+int ma_abi_version(void) { return MA_ABI_VERSION; }
+
+int ma_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor) {
+    return guarded([&] {
+        const DeviceInfo d = device_info();
+        if (device) *device = d.device;
+        if (sm_count) *sm_count = d.sms;
+        if (cc_major) *cc_major = d.major;
+        if (cc_minor) *cc_minor = d.minor;
+    });
+}
+
+int ma_overflow_check_async(const void* grads, uint64_t n, int g_dtype, uint32_t* d_flag,
+                            uint64_t* d_first_index, void* stream) {
+    return guarded([&] {
+        check_grad_dtype(g_dtype);
+        if (!d_flag) fail(MA_ERR_INVALID_ARGUMENT, "null flag pointer");
+        if (n && !grads) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
+        launch_k1(grads, n, g_dtype, d_flag, d_first_index, 0, d_first_index == nullptr,
+                  as_stream(stream));
+    });
+}
+
+int ma_overflow_check(const void* grads, uint64_t n, int g_dtype, int track_first_index,
+                      int* overflow, uint64_t* first_index) {
+    return guarded([&] {
+        check_grad_dtype(g_dtype);
+        if (!overflow) fail(MA_ERR_INVALID_ARGUMENT, "null result pointer");
+        *overflow = 0;
+        if (first_index) *first_index = UINT64_MAX;
+        if (n == 0) return;  // overflow.cpp:77-79
+        if (!grads) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
+        device_info();
+        Scratch& sc = scratch();
+        std::lock_guard<std::mutex> lock(sc.mu);
+        const uint64_t es = elem_bytes(g_dtype);
+        const void* dev = nullptr;
+        const int kind = classify(grads, &dev);
+        const uint64_t chunk = kind == 0 ? (64ull << 20) / es : n;  // 64 MiB staging chunks
+        const size_t need = 256 + (kind == 0 ? chunk * es : 0);
+        uint8_t* base = static_cast<uint8_t*>(sc.get(need));
+        uint32_t* d_flag = reinterpret_cast<uint32_t*>(base);
+        uint64_t* d_first = reinterpret_cast<uint64_t*>(base + 64);
+        cudaStream_t st = sc.strm();
+        CK(cudaMemsetAsync(d_flag, 0, 4, st));
+        CK(cudaMemsetAsync(d_first, 0xFF, 8, st));
+        for (uint64_t off = 0; off < n; off += chunk) {
+            const uint64_t len = std::min(chunk, n - off);
+            const void* src;
+            if (kind == 0) {
+                CK(cudaMemcpyAsync(base + 256, static_cast<const uint8_t*>(grads) + off * es,
+                                   len * es, cudaMemcpyHostToDevice, st));
+                src = base + 256;
+            } else {
+                src = static_cast<const uint8_t*>(dev) + off * es;
+            }
+            launch_k1(src, len, g_dtype, d_flag, track_first_index ? d_first : nullptr, off,
+                      !track_first_index, st);
+        }
+        uint32_t flag = 0;
+        uint64_t first = UINT64_MAX;
+        CK(cudaMemcpyAsync(&flag, d_flag, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&first, d_first, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        *overflow = flag ? 1 : 0;
+        if (first_index && track_first_index && flag) *first_index = first;
+    });
+}
+
+int ma_adam_step_async(float* p, float* m, float* v, const void* g, int g_dtype, uint64_t n,
+                       uint64_t t, const ma_adam_hyper* h, float loss_scale, void* w_out,
+                       int w_dtype, const uint32_t* d_skip_flag, void* stream) {
+    return guarded([&] {
+        check_grad_dtype(g_dtype);
+        check_w_dtype(w_dtype);
+        const ma::AdamArgs a = explicit_args(h, t, loss_scale, d_skip_flag);
+        ma_subgroup grp{p, m, v, g, w_out, n};
+        launch_k2(&grp, 1, g_dtype, w_dtype, a, as_stream(stream));
+    });
+}
+
+int ma_adam_step(float* p, float* m, float* v, const void* g, int g_dtype, uint64_t n,
+                 uint64_t t, const ma_adam_hyper* h, float loss_scale, void* w_out, int w_dtype) {
+    return guarded([&] {
+        check_grad_dtype(g_dtype);
+        check_w_dtype(w_dtype);
+        const ma::AdamArgs a = explicit_args(h, t, loss_scale, nullptr);
+        if (n == 0) return;
+        device_info();
+        Scratch& sc = scratch();
+        std::lock_guard<std::mutex> lock(sc.mu);
+        cudaStream_t st = sc.strm();
+        const uint64_t ges = elem_bytes(g_dtype);
+        void* ptrs[5] = {p, m, v, const_cast<void*>(g), w_dtype == MA_DT_NONE ? nullptr : w_out};
+        const uint64_t esz[5] = {4, 4, 4, ges, 2};
+        const void* dev[5];
+        int kinds[5];
+        bool any_pageable = false;
+        for (int k = 0; k < 5; ++k) {
+            kinds[k] = classify(ptrs[k], &dev[k]);
+            any_pageable |= kinds[k] == 0;
+        }
+        if (!any_pageable) {
+            ma_subgroup grp{const_cast<float*>(static_cast<const float*>(dev[0])),
+                            const_cast<float*>(static_cast<const float*>(dev[1])),
+                            const_cast<float*>(static_cast<const float*>(dev[2])), dev[3],
+                            const_cast<void*>(dev[4]), n};
+            launch_k2(&grp, 1, g_dtype, w_dtype, a, st);
+            CK(cudaStreamSynchronize(st));
+            return;
+        }
+        // stage pageable spans through device scratch in 16 Mi-element chunks
+        const uint64_t chunk = std::min<uint64_t>(n, 16ull << 20);
+        uint64_t offs[5], total = 0;
+        for (int k = 0; k < 5; ++k) {
+            offs[k] = total;
+            if (kinds[k] == 0 && ptrs[k]) total += (chunk * esz[k] + 255) / 256 * 256;
+        }
+        uint8_t* base = static_cast<uint8_t*>(sc.get(std::max<uint64_t>(total, 256)));
+        for (uint64_t off = 0; off < n; off += chunk) {
+            const uint64_t len = std::min(chunk, n - off);
+            void* cur[5];
+            for (int k = 0; k < 5; ++k) {
+                if (!ptrs[k]) {
+                    cur[k] = nullptr;
+                } else if (kinds[k] == 0) {
+                    cur[k] = base + offs[k];
+                    if (k < 4) {  // inputs: p, m, v, g
+                        CK(cudaMemcpyAsync(cur[k], static_cast<uint8_t*>(ptrs[k]) + off * esz[k],
+                                           len * esz[k], cudaMemcpyHostToDevice, st));
+                    }
+                } else {
+                    cur[k] = const_cast<uint8_t*>(static_cast<const uint8_t*>(dev[k])) + off * esz[k];
+                }
+            }
+            ma_subgroup grp{static_cast<float*>(cur[0]), static_cast<float*>(cur[1]),
+                            static_cast<float*>(cur[2]), cur[3], cur[4], len};
+            launch_k2(&grp, 1, g_dtype, w_dtype, a, st);
+            for (int k : {0, 1, 2, 4}) {  // outputs: p, m, v, w
+                if (ptrs[k] && kinds[k] == 0) {
+                    CK(cudaMemcpyAsync(static_cast<uint8_t*>(ptrs[k]) + off * esz[k], cur[k],
+                                       len * esz[k], cudaMemcpyDeviceToHost, st));
+                }
+            }
+            CK(cudaStreamSynchronize(st));
+        }
+    });
+}
+
+int ma_adam_step_bf16(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
+                      uint64_t t, const ma_adam_hyper* h, float loss_scale) {
+    return guarded([&] {
+        const ma::AdamArgs a = explicit_args(h, t, loss_scale, nullptr);
+        if (n == 0) return;
+        const DeviceInfo d = device_info();
+        Scratch& sc = scratch();
+        std::lock_guard<std::mutex> lock(sc.mu);
+        cudaStream_t st = sc.strm();
+        const void* dp;
+        const void* dm;
+        const void* dv;
+        const void* dg;
+        const int kp = classify(p, &dp), km = classify(m, &dm), kv = classify(v, &dv),
+                  kg = classify(g, &dg);
+        // K3 is the "next" row: stage everything that is not device-accessible
+        const uint64_t bytes = n * (2 + 2 + 2 + 4);
+        uint8_t* base = static_cast<uint8_t*>(sc.get(bytes));
+        uint16_t* sp = kp ? const_cast<uint16_t*>(static_cast<const uint16_t*>(dp))
+                          : reinterpret_cast<uint16_t*>(base);
+        uint16_t* sm = km ? const_cast<uint16_t*>(static_cast<const uint16_t*>(dm))
+                          : reinterpret_cast<uint16_t*>(base + 2 * n);
+        uint16_t* sv = kv ? const_cast<uint16_t*>(static_cast<const uint16_t*>(dv))
+                          : reinterpret_cast<uint16_t*>(base + 4 * n);
+        const float* sg = kg ? static_cast<const float*>(dg) : reinterpret_cast<float*>(base + 6 * n);
+        if (!kp) CK(cudaMemcpyAsync(sp, p, 2 * n, cudaMemcpyHostToDevice, st));
+        if (!km) CK(cudaMemcpyAsync(sm, m, 2 * n, cudaMemcpyHostToDevice, st));
+        if (!kv) CK(cudaMemcpyAsync(sv, v, 2 * n, cudaMemcpyHostToDevice, st));
+        if (!kg) CK(cudaMemcpyAsync(const_cast<float*>(sg), g, 4 * n, cudaMemcpyHostToDevice, st));
+        const uint64_t grid = std::min<uint64_t>((n + ma::kK2Threads - 1) / ma::kK2Threads,
+                                                 static_cast<uint64_t>(d.sms) * 8);
+        ma::k3_adam_bf16<<<static_cast<unsigned>(grid), ma::kK2Threads, 0, st>>>(sp, sm, sv, sg, n, a);
+        CK(cudaGetLastError());
+        if (!kp) CK(cudaMemcpyAsync(p, sp, 2 * n, cudaMemcpyDeviceToHost, st));
+        if (!km) CK(cudaMemcpyAsync(m, sm, 2 * n, cudaMemcpyDeviceToHost, st));
+        if (!kv) CK(cudaMemcpyAsync(v, sv, 2 * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+// ------------------------------------------------------------ stepper
+int ma_stepper_create(const ma_adam_hyper* h, float init_scale, uint32_t growth_interval,
+                      int g_dtype, int w_dtype, void* d_state, ma_stepper** out) {
+    return guarded([&] {
+        check_grad_dtype(g_dtype);
+        check_w_dtype(w_dtype);
+        if (!out) fail(MA_ERR_INVALID_ARGUMENT, "null output pointer");
+        if (!(init_scale > 0.0f)) fail(MA_ERR_INVALID_ARGUMENT, "loss scale must be > 0");
+        if (growth_interval == 0) fail(MA_ERR_INVALID_ARGUMENT, "growth_interval must be >= 1");
+        const DeviceInfo d = device_info();
+        auto* s = new ma_stepper();
+        try {
+            s->h = *h;
+            s->c = make_consts(h);
+            s->g_dtype = g_dtype;
+            s->w_dtype = w_dtype;
+            s->device = d.device;
+            static_assert(sizeof(ma::StepDev) <= MA_STEPPER_STATE_BYTES, "state layout");
+            static_assert(offsetof(ma::StepDev, scale) == 8, "scale offset");
+            if (d_state) {
+                if (reinterpret_cast<uintptr_t>(d_state) % 8)
+                    fail(MA_ERR_ALIGNMENT, "stepper state must be 8-byte aligned");
+                s->d_st = static_cast<ma::StepDev*>(d_state);
+                s->owns_state = false;
+            } else {
+                CK(cudaMalloc(&s->d_st, sizeof(ma::StepDev)));
+            }
+            CK(cudaMalloc(&s->d_log, sizeof(ma::StepLog) * ma::kHistory));
+            ma::StepDev init{};
+            init.scale = init_scale;
+            init.growth_interval = growth_interval;
+            CK(cudaMemcpy(s->d_st, &init, sizeof init, cudaMemcpyHostToDevice));
+            CK(cudaMemset(s->d_log, 0, sizeof(ma::StepLog) * ma::kHistory));
+            stepper_grow_bc(s, 1024);
+        } catch (...) {
+            if (s->d_st && s->owns_state) cudaFree(s->d_st);
+            if (s->d_log) cudaFree(s->d_log);
+            if (s->d_bc) cudaFree(s->d_bc);
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+int ma_stepper_destroy(ma_stepper* s) {
+    return guarded([&] {
+        if (!s) return;
+        cudaDeviceSynchronize();
+        if (s->owns_state) cudaFree(s->d_st);
+        cudaFree(s->d_log);
+        cudaFree(s->d_bc);
+        delete s;
+    });
+}
+
+int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void* stream) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        if (n && !g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
+        launch_k1(g, n, s->g_dtype, &s->d_st->flag, nullptr, 0, true, as_stream(stream));
+        s->last = as_stream(stream);
+    });
+}
+
+int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
+                                uint64_t chunk_elems, void* stream, void* copy_stream) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        if (n == 0) return;
+        if (!host_g || !dev_g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
+        const void* alias;
+        if (classify(host_g, &alias) != 2)
+            fail(MA_ERR_INVALID_ARGUMENT, "host gradients must be pinned (registered) memory");
+        if (chunk_elems == 0) chunk_elems = 64ull << 20;
+        const uint64_t es = elem_bytes(s->g_dtype);
+        cudaStream_t cs = as_stream(copy_stream);
+        cudaStream_t st = as_stream(stream);
+        // the copy stream must not overwrite dev_g before earlier work on it retired
+        cudaEvent_t ready = s->event(0);
+        CK(cudaEventRecord(ready, st));
+        CK(cudaStreamWaitEvent(cs, ready, 0));
+        uint64_t k = 0;
+        for (uint64_t off = 0; off < n; off += chunk_elems, ++k) {
+            const uint64_t len = std::min(chunk_elems, n - off);
+            CK(cudaMemcpyAsync(static_cast<uint8_t*>(dev_g) + off * es,
+                               static_cast<const uint8_t*>(host_g) + off * es, len * es,
+                               cudaMemcpyHostToDevice, cs));
+            cudaEvent_t landed = s->event(1 + k);
+            CK(cudaEventRecord(landed, cs));
+            CK(cudaStreamWaitEvent(st, landed, 0));
+            launch_k1(static_cast<uint8_t*>(dev_g) + off * es, len, s->g_dtype, &s->d_st->flag,
+                      nullptr, 0, true, st);
+        }
+        s->last = st;
+    });
+}
+
+uint32_t* ma_stepper_flag(ma_stepper* s) { return s ? &s->d_st->flag : nullptr; }
+
+float* ma_stepper_scale(ma_stepper* s) { return s ? &s->d_st->scale : nullptr; }
+
+int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
+                           void* stream) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
+        stepper_grow_bc(s, s->issued + 1);  // t <= finished steps + 1
+        ma::AdamArgs a{};
+        a.c = s->c;
+        a.skip = &s->d_st->flag;
+        a.st = s->d_st;
+        a.bc_table = s->d_bc;
+        launch_k2(groups, count, s->g_dtype, s->w_dtype, a, as_stream(stream));
+        s->last = as_stream(stream);
+    });
+}
+
+int ma_stepper_finish_async(ma_stepper* s, void* stream) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        ma::k_step_finish<<<1, 32, 0, as_stream(stream)>>>(s->d_st, s->d_log);
+        CK(cudaGetLastError());
+        s->issued += 1;
+        s->last = as_stream(stream);
+    });
+}
+
+int ma_stepper_state(ma_stepper* s, ma_step_state* out) {
+    return guarded([&] {
+        if (!s || !out) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
+        CK(cudaStreamSynchronize(s->last));
+        ma::StepDev st{};
+        CK(cudaMemcpy(&st, s->d_st, sizeof st, cudaMemcpyDeviceToHost));
+        out->scale = st.scale;
+        out->clean_steps = st.clean_steps;
+        out->updates = st.updates;
+        out->steps = st.steps;
+        out->last_overflow = st.last_overflow;
+        out->growth_interval = st.growth_interval;
+    });
+}
+
+int ma_stepper_history(ma_stepper* s, uint8_t* overflow, float* scale_after, uint64_t cap,
+                       uint64_t* count) {
+    return guarded([&] {
+        if (!s || !count) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
+        CK(cudaStreamSynchronize(s->last));
+        ma::StepDev st{};
+        CK(cudaMemcpy(&st, s->d_st, sizeof st, cudaMemcpyDeviceToHost));
+        std::vector<ma::StepLog> log(ma::kHistory);
+        CK(cudaMemcpy(log.data(), s->d_log, sizeof(ma::StepLog) * ma::kHistory,
+                      cudaMemcpyDeviceToHost));
+        const uint64_t avail = std::min<uint64_t>(st.steps, ma::kHistory);
+        const uint64_t k = std::min<uint64_t>(avail, cap);
+        const uint64_t first = st.steps - k;
+        for (uint64_t i = 0; i < k; ++i) {
+            const ma::StepLog& e = log[(first + i) % ma::kHistory];
+            if (overflow) overflow[i] = static_cast<uint8_t>(e.overflow);
+            if (scale_after) scale_after[i] = e.scale_after;
+        }
+        *count = k;
+    });
+}
+
+// ------------------------------------------------------------ generators
+int ma_gen_seeded_weights_async(float* p, void* w, int w_dtype, uint64_t n, uint64_t base,
+                                uint64_t seed, void* stream) {
+    return guarded([&] {
+        check_w_dtype(w_dtype);
+        if (n == 0) return;
+        const DeviceInfo d = device_info();
+        const unsigned grid = static_cast<unsigned>(
+            std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(d.sms) * 16));
+        auto* w16 = static_cast<uint16_t*>(w);
+        cudaStream_t st = as_stream(stream);
+        if (w_dtype == MA_DT_NONE || !w) {
+            ma::k_gen_weights<ma::kNone><<<grid, 256, 0, st>>>(p, nullptr, n, base, seed);
+        } else if (w_dtype == MA_DT_BF16) {
+            ma::k_gen_weights<ma::kBF16><<<grid, 256, 0, st>>>(p, w16, n, base, seed);
+        } else {
+            ma::k_gen_weights<ma::kF16><<<grid, 256, 0, st>>>(p, w16, n, base, seed);
+        }
+        CK(cudaGetLastError());
+    });
+}
+
+int ma_gen_pseudo_grads_async(void* g, int g_dtype, const void* w, int w_dtype, uint64_t n,
+                              uint64_t base, uint64_t seed, uint64_t step, const float* d_scale,
+                              float scale, void* stream) {
+    return guarded([&] {
+        check_grad_dtype(g_dtype);
+        if (w_dtype != MA_DT_BF16 && w_dtype != MA_DT_F16)
+            fail(MA_ERR_INVALID_ARGUMENT, "working weights must be BF16 or F16");
+        if (n == 0) return;
+        const DeviceInfo d = device_info();
+        const unsigned grid = static_cast<unsigned>(
+            std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(d.sms) * 16));
+        const auto* w16 = static_cast<const uint16_t*>(w);
+        cudaStream_t st = as_stream(stream);
+#define MA_GEN(GK, WK) ma::k_gen_grads<GK, WK><<<grid, 256, 0, st>>>(g, w16, n, base, seed, step, d_scale, scale)
+        if (w_dtype == MA_DT_BF16) {
+            if (g_dtype == MA_DT_F32) MA_GEN(ma::kF32, ma::kBF16);
+            else if (g_dtype == MA_DT_BF16) MA_GEN(ma::kBF16, ma::kBF16);
+            else MA_GEN(ma::kF16, ma::kBF16);
+        } else {
+            if (g_dtype == MA_DT_F32) MA_GEN(ma::kF32, ma::kF16);
+            else if (g_dtype == MA_DT_BF16) MA_GEN(ma::kBF16, ma::kF16);
+            else MA_GEN(ma::kF16, ma::kF16);
+        }
+#undef MA_GEN
+        CK(cudaGetLastError());
+    });
+}
+
+int ma_plant_bits_async(void* buf, int dtype, uint64_t index, uint32_t bits, void* stream) {
+    return guarded([&] {
+        check_grad_dtype(dtype);
+        device_info();
+        ma::k_plant<<<1, 1, 0, as_stream(stream)>>>(buf, dtype, index, bits);
+        CK(cudaGetLastError());
+    });
+}
+
+// ------------------------------------------------------------ host memory
+int ma_host_register(void* ptr, uint64_t bytes) {
+    return guarded([&] {
+        if (!ptr || bytes == 0) fail(MA_ERR_INVALID_ARGUMENT, "empty host region");
+        device_info();
+        CK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+    });
+}
+
+int ma_host_unregister(void* ptr) {
+    return guarded([&] {
+        if (!ptr) fail(MA_ERR_INVALID_ARGUMENT, "null host region");
+        device_info();
+        const cudaError_t e = cudaHostUnregister(ptr);
+        if (e == cudaErrorHostMemoryNotRegistered) {
+            cudaGetLastError();
+            fail(MA_ERR_UNKNOWN_REGION, "host region was never registered");
+        }
+        CK(e);
+    });
+}
+
+int ma_pointer_kind(const void* ptr, int* kind) {
+    return guarded([&] {
+        if (!kind) fail(MA_ERR_INVALID_ARGUMENT, "null output");
+        device_info();
+        const void* dev;
+        const int k = classify(ptr, &dev);
+        *kind = k;
+    });
+}
+
+// ------------------------------------------------------------ verification
+int ma_debug_cast_sweep(int kind, int block_log2, uint64_t* out_host) {
+    return guarded([&] {
+        if (kind != MA_DT_BF16 && kind != MA_DT_F16)
+            fail(MA_ERR_INVALID_ARGUMENT, "cast sweep kind must be BF16 or F16");
+        if (block_log2 < 8 || block_log2 > 24) fail(MA_ERR_INVALID_ARGUMENT, "block_log2 in [8, 24]");
+        device_info();
+        const uint64_t nb = 1ull << (32 - block_log2);
+        uint64_t* d = nullptr;
+        CK(cudaMalloc(&d, nb * 8));
+        const unsigned grid = static_cast<unsigned>((nb + 63) / 64);
+        if (kind == MA_DT_BF16) {
+            ma::k_cast_sweep<ma::kBF16><<<grid, 64>>>(block_log2, d, nb);
+        } else {
+            ma::k_cast_sweep<ma::kF16><<<grid, 64>>>(block_log2, d, nb);
+        }
+        const cudaError_t e = cudaGetLastError();
+        const cudaError_t e2 = cudaMemcpy(out_host, d, nb * 8, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+        CK(e2);
+    });
+}
+
+int ma_debug_mask_sweep(int kind, uint64_t* mismatches) {
+    return guarded([&] {
+        check_grad_dtype(kind);
+        const DeviceInfo dv = device_info();
+        unsigned long long* d = nullptr;
+        CK(cudaMalloc(&d, 8));
+        CK(cudaMemset(d, 0, 8));
+        ma::k_mask_sweep<<<dv.sms * 8, 256>>>(kind, d);
+        const cudaError_t e = cudaGetLastError();
+        unsigned long long h = 0;
+        const cudaError_t e2 = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+        CK(e2);
+        *mismatches = h;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,402 @@
+// sm_100a kernels of the MemAscend optimizer hot path.
+//
+//   K1  k1_overflow        fused overflow check   (proj/src/overflow.cpp:45-145)
+//   K2  k2_adam            unscale + AdamW + cast (proj/src/optimizer.cpp:26-44,103-109,
+//                                                  proj/src/simulator.cpp:461-467)
+//   K3  k3_adam_bf16       bf16-state Adam        (proj/src/optimizer.cpp:83-93,111-118)
+//       k_step_finish      LossScaler + counters  (optimizer.hpp:19-35, simulator.cpp:438-491)
+//       k_gen_*            synthetic workload     (simulator.hpp:23-42)
+//
+// All three are HBM-streaming kernels (no data reuse, no tensor-core work):
+// 128-bit coalesced loads/stores, persistent grid-stride launches sized to
+// the SM count, streaming cache hints (.cs = evict-first) so 10^2 GB of
+// one-touch state does not thrash L2.
+#include "kernels.cuh"
+
+namespace ma {
+
+// ============================================================== K1
+// One pass over the raw bits; each thread ORs (w & MASK) + INC over its
+// 16-byte vectors, one warp vote at the end, one plain store of 1 by the
+// first lane of any warp that saw a non-finite lane (idempotent, no atomics).
+// Early exit (ScanConfig::early_exit, overflow.cpp:88-114): warps poll the
+// flag once per unrolled batch and stop once any CTA has set it.
+template <bool kTrack>
+__global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
+    const ScanWord sw = scan_word(a.kind);
+    const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t per_vec = 16u / a.elem_bytes;  // elements per uint4
+    uint32_t acc = 0;
+
+    for (uint64_t base = tid; base < a.nvec; base += stride * kK1Unroll) {
+        uint4 q[kK1Unroll];
+#pragma unroll
+        for (int u = 0; u < kK1Unroll; ++u) {
+            const uint64_t i = base + u * stride;
+            q[u] = i < a.nvec ? __ldcs(a.body + i) : make_uint4(0, 0, 0, 0);
+        }
+        uint32_t batch = 0;
+#pragma unroll
+        for (int u = 0; u < kK1Unroll; ++u) {
+            batch |= ((q[u].x & sw.mask) + sw.inc) | ((q[u].y & sw.mask) + sw.inc) |
+                     ((q[u].z & sw.mask) + sw.inc) | ((q[u].w & sw.mask) + sw.inc);
+        }
+        if (kTrack && (batch & sw.top)) {
+            // exact lowest offending index within this thread's vectors
+#pragma unroll
+            for (int u = 0; u < kK1Unroll; ++u) {
+                const uint64_t i = base + u * stride;
+                if (i >= a.nvec) continue;
+                const uint32_t w4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+                for (uint32_t e = 0; e < per_vec; ++e) {
+                    const uint32_t word = w4[(e * a.elem_bytes) >> 2];
+                    const uint32_t bits =
+                        a.elem_bytes == 4 ? word : (word >> (16 * (e & 1u))) & 0xFFFFu;
+                    if (elem_non_finite(bits, a.kind)) {
+                        atomicMin(reinterpret_cast<unsigned long long*>(a.first),
+                                  static_cast<unsigned long long>(a.index_base + a.head +
+                                                                  i * per_vec + e));
+                        break;
+                    }
+                }
+            }
+        }
+        acc |= batch;
+        if (!kTrack && a.early_exit) {
+            uint32_t seen = 0;
+            if (lane == 0) seen = *reinterpret_cast<volatile uint32_t*>(a.flag);
+            if (__shfl_sync(0xFFFFFFFFu, seen, 0) != 0) break;
+        }
+    }
+    // unaligned head / tail elements (fewer than 16 bytes each) on CTA 0
+    if (blockIdx.x == 0) {
+        const uint64_t tail_begin = a.head + a.nvec * per_vec;
+        const uint64_t extra = a.head + (a.n - tail_begin);
+        for (uint64_t k = threadIdx.x; k < extra; k += blockDim.x) {
+            const uint64_t e = k < a.head ? k : tail_begin + (k - a.head);
+            const uint32_t bits = a.elem_bytes == 4
+                                      ? reinterpret_cast<const uint32_t*>(a.raw)[e]
+                                      : reinterpret_cast<const uint16_t*>(a.raw)[e];
+            if (elem_non_finite(bits, a.kind)) {
+                acc |= sw.top;
+                if (kTrack) {
+                    atomicMin(reinterpret_cast<unsigned long long*>(a.first),
+                              static_cast<unsigned long long>(a.index_base + e));
+                }
+            }
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, (acc & sw.top) != 0u) && lane == 0) *a.flag = 1u;
+}
+
+template __global__ void k1_overflow<false>(K1Args);
+template __global__ void k1_overflow<true>(K1Args);
+
+// ============================================================== K2
+__device__ __forceinline__ bool resolve_step(const AdamArgs& a, StepScalars& s) {
+    if (a.skip != nullptr && *a.skip != 0u) return false;
+    if (a.st != nullptr) {
+        // device-resident scaler: t = applied updates + 1
+        const unsigned long long t = a.st->updates + 1ull;
+        const float2 bc = a.bc_table[t - 1ull];
+        s.scale = a.st->scale;
+        s.bc1 = bc.x;
+        s.bc2 = bc.y;
+    } else {
+        s.scale = a.scale;
+        s.bc1 = a.bc1;
+        s.bc2 = a.bc2;
+    }
+    s.scale_pow2 = exact_reciprocal(s.scale, &s.inv_scale);
+    return true;
+}
+
+// vector of VEC fp32 lanes through float4 (VEC = 4 or 8)
+template <int VEC>
+__device__ __forceinline__ void ld_f32(const float* p, float (&x)[VEC]) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int k = 0; k < VEC / 4; ++k) {
+        const float4 t = __ldcs(q + k);
+        x[4 * k + 0] = t.x;
+        x[4 * k + 1] = t.y;
+        x[4 * k + 2] = t.z;
+        x[4 * k + 3] = t.w;
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void st_f32(float* p, const float (&x)[VEC]) {
+    float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+    for (int k = 0; k < VEC / 4; ++k) {
+        __stcs(q + k, make_float4(x[4 * k + 0], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]));
+    }
+}
+
+// VEC 16-bit lanes: VEC=8 -> one uint4, VEC=4 -> one uint2
+template <int VEC>
+__device__ __forceinline__ void ld_u16(const uint16_t* p, uint32_t (&h)[VEC]) {
+    if constexpr (VEC == 8) {
+        const uint4 t = __ldcs(reinterpret_cast<const uint4*>(p));
+        const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            h[2 * k] = w[k] & 0xFFFFu;
+            h[2 * k + 1] = w[k] >> 16;
+        }
+    } else {
+        const uint2 t = __ldcs(reinterpret_cast<const uint2*>(p));
+        h[0] = t.x & 0xFFFFu;
+        h[1] = t.x >> 16;
+        h[2] = t.y & 0xFFFFu;
+        h[3] = t.y >> 16;
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void st_u16(uint16_t* p, const uint32_t (&h)[VEC]) {
+    if constexpr (VEC == 8) {
+        __stcs(reinterpret_cast<uint4*>(p),
+               make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16),
+                          h[6] | (h[7] << 16)));
+    } else {
+        __stcs(reinterpret_cast<uint2*>(p), make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16)));
+    }
+}
+
+template <int GK>
+__device__ __forceinline__ float load_grad1(const void* g, uint64_t e) {
+    if constexpr (GK == kF32) return reinterpret_cast<const float*>(g)[e];
+    return widen<GK>(reinterpret_cast<const uint16_t*>(g)[e]);
+}
+
+template <int GK, int WK>
+__device__ __forceinline__ void adam_scalar(const Seg& sg, uint64_t e, const AdamConsts& c,
+                                            const StepScalars& s) {
+    float p = sg.p[e], m = sg.m[e], v = sg.v[e];
+    adam_elem(p, m, v, load_grad1<GK>(sg.g, e), c, s);
+    sg.p[e] = p;
+    sg.m[e] = m;
+    sg.v[e] = v;
+    if constexpr (WK != kNone) reinterpret_cast<uint16_t*>(sg.w)[e] = narrow<WK>(p);
+}
+
+template <int GK, int WK, int VEC>
+__device__ __forceinline__ void adam_vector(const Seg& sg, uint64_t e, const AdamConsts& c,
+                                            const StepScalars& s) {
+    float p[VEC], m[VEC], v[VEC], g[VEC];
+    ld_f32<VEC>(sg.p + e, p);
+    ld_f32<VEC>(sg.m + e, m);
+    ld_f32<VEC>(sg.v + e, v);
+    if constexpr (GK == kF32) {
+        ld_f32<VEC>(reinterpret_cast<const float*>(sg.g) + e, g);
+    } else {
+        uint32_t h[VEC];
+        ld_u16<VEC>(reinterpret_cast<const uint16_t*>(sg.g) + e, h);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) g[k] = widen<GK>(h[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) adam_elem(p[k], m[k], v[k], g[k], c, s);
+    st_f32<VEC>(sg.p + e, p);
+    st_f32<VEC>(sg.m + e, m);
+    st_f32<VEC>(sg.v + e, v);
+    if constexpr (WK != kNone) {
+        uint32_t w[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) w[k] = narrow<WK>(p[k]);
+        st_u16<VEC>(reinterpret_cast<uint16_t*>(sg.w) + e, w);
+    }
+}
+
+// Persistent grid-stride walk over the tiles of up to kMaxSegs sub-groups.
+// A tile is kK2Threads vectors of VEC elements.  Tile 0 of a vectorised
+// sub-group also handles its unaligned head and its tail scalar-wise; a
+// sub-group whose pointers cannot be co-aligned runs scalar tiles.
+template <int GK, int WK, int VEC>
+__global__ void __launch_bounds__(kK2Threads) k2_adam(SegTable tab, AdamArgs a) {
+    StepScalars s;
+    if (!resolve_step(a, s)) return;  // skipped step: no state touched
+    const AdamConsts c = a.c;
+    uint32_t si = 0;
+    for (uint64_t tile = blockIdx.x; tile < tab.total_tiles; tile += gridDim.x) {
+        while (tile >= tab.seg[si].tile_end) ++si;  // tiles are visited in increasing order
+        const Seg& sg = tab.seg[si];
+        const uint64_t lt = tile - sg.tile_begin;
+        if (sg.vector_ok) {
+            const uint64_t j = lt * kK2Threads + threadIdx.x;
+            if (j < sg.nvec) adam_vector<GK, WK, VEC>(sg, sg.head + j * VEC, c, s);
+            if (lt == 0) {
+                const uint64_t tail_begin = sg.head + sg.nvec * VEC;
+                const uint64_t extra = sg.head + (sg.n - tail_begin);
+                for (uint64_t k = threadIdx.x; k < extra; k += kK2Threads) {
+                    adam_scalar<GK, WK>(sg, k < sg.head ? k : tail_begin + (k - sg.head), c, s);
+                }
+            }
+        } else {
+            const uint64_t e0 = lt * static_cast<uint64_t>(kK2Threads) * VEC;
+#pragma unroll
+            for (int r = 0; r < VEC; ++r) {
+                const uint64_t e = e0 + static_cast<uint64_t>(r) * kK2Threads + threadIdx.x;
+                if (e < sg.n) adam_scalar<GK, WK>(sg, e, c, s);
+            }
+        }
+    }
+}
+
+#define MA_INST_K2(GK, WK)                                        \
+    template __global__ void k2_adam<GK, WK, 4>(SegTable, AdamArgs); \
+    template __global__ void k2_adam<GK, WK, 8>(SegTable, AdamArgs);
+MA_INST_K2(kF32, kNone)
+MA_INST_K2(kF32, kBF16)
+MA_INST_K2(kF32, kF16)
+MA_INST_K2(kBF16, kNone)
+MA_INST_K2(kBF16, kBF16)
+MA_INST_K2(kBF16, kF16)
+MA_INST_K2(kF16, kNone)
+MA_INST_K2(kF16, kBF16)
+MA_INST_K2(kF16, kF16)
+#undef MA_INST_K2
+
+// ============================================================== K3
+// bf16 state (Bf16Access, optimizer.cpp:83-93): widen, same fp32 update,
+// round each stored quantity back with the reference's bf16 rounding.
+__global__ void __launch_bounds__(kK2Threads) k3_adam_bf16(uint16_t* __restrict__ p,
+                                                           uint16_t* __restrict__ m,
+                                                           uint16_t* __restrict__ v,
+                                                           const float* __restrict__ g,
+                                                           uint64_t n, AdamArgs a) {
+    StepScalars s;
+    if (!resolve_step(a, s)) return;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += stride) {
+        float pf = widen_bf16(p[i]), mf = widen_bf16(m[i]), vf = widen_bf16(v[i]);
+        adam_elem(pf, mf, vf, g[i], a.c, s);
+        p[i] = bf16_bits(pf);
+        m[i] = bf16_bits(mf);
+        v[i] = bf16_bits(vf);
+    }
+}
+
+// ============================================================== step finish
+// LossScaler::on_overflow / on_clean_step (optimizer.hpp:24-34) and the
+// update counter (simulator.cpp:438-444,491); re-arms the flag.
+__global__ void k_step_finish(StepDev* st, StepLog* log) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t of = st->flag != 0u;
+    if (of) {
+        st->scale = st->scale * 0.5f;
+        st->clean_steps = 0;
+    } else {
+        st->updates += 1ull;
+        st->clean_steps += 1u;
+        if (st->clean_steps >= st->growth_interval) {
+            st->scale = st->scale * 2.0f;
+            st->clean_steps = 0;
+        }
+    }
+    log[st->steps % kHistory] = StepLog{st->scale, of};
+    st->steps += 1ull;
+    st->last_overflow = of;
+    st->flag = 0u;
+}
+
+// ============================================================== generators
+template <int WK>
+__global__ void k_gen_weights(float* __restrict__ p, uint16_t* __restrict__ w, uint64_t n,
+                              uint64_t base, uint64_t seed) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += stride) {
+        const float x = seeded_weight(seed, base + i);
+        if (p) p[i] = x;
+        if constexpr (WK != kNone) w[i] = narrow<WK>(x);
+    }
+}
+template __global__ void k_gen_weights<kNone>(float*, uint16_t*, uint64_t, uint64_t, uint64_t);
+template __global__ void k_gen_weights<kBF16>(float*, uint16_t*, uint64_t, uint64_t, uint64_t);
+template __global__ void k_gen_weights<kF16>(float*, uint16_t*, uint64_t, uint64_t, uint64_t);
+
+template <int GK, int WK>
+__global__ void k_gen_grads(void* __restrict__ g, const uint16_t* __restrict__ w, uint64_t n,
+                            uint64_t base, uint64_t seed, uint64_t step, const float* d_scale,
+                            float scale) {
+    const float sc = d_scale ? *d_scale : scale;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += stride) {
+        const float gs = __fmul_rn(pseudo_gradient(seed, step, base + i, widen<WK>(w[i])), sc);
+        if constexpr (GK == kF32) {
+            reinterpret_cast<float*>(g)[i] = gs;
+        } else {
+            reinterpret_cast<uint16_t*>(g)[i] = narrow<GK>(gs);
+        }
+    }
+}
+template __global__ void k_gen_grads<kF32, kBF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
+template __global__ void k_gen_grads<kF32, kF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
+template __global__ void k_gen_grads<kBF16, kBF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
+template __global__ void k_gen_grads<kBF16, kF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
+template __global__ void k_gen_grads<kF16, kBF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
+template __global__ void k_gen_grads<kF16, kF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
+
+__global__ void k_plant(void* buf, int dtype, uint64_t index, uint32_t bits) {
+    if (dtype == kF32) {
+        reinterpret_cast<uint32_t*>(buf)[index] = bits;
+    } else {
+        reinterpret_cast<uint16_t*>(buf)[index] = static_cast<uint16_t>(bits);
+    }
+}
+
+// ============================================================== verification
+// FNV-1a-64 over each 2^log2 block of fp32->kind conversions (one thread per
+// block), through the same narrow<>() K2 uses.
+template <int K>
+__global__ void k_cast_sweep(int log2, uint64_t* out, uint64_t nblocks) {
+    const uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nblocks) return;
+    uint64_t h = 1469598103934665603ull;
+    const uint64_t len = 1ull << log2;
+    for (uint64_t k = 0; k < len; ++k) {
+        const uint16_t r = narrow<K>(__uint_as_float(static_cast<uint32_t>((b << log2) + k)));
+        h = (h ^ (r & 0xFFu)) * 1099511628211ull;
+        h = (h ^ (r >> 8)) * 1099511628211ull;
+    }
+    out[b] = h;
+}
+template __global__ void k_cast_sweep<kBF16>(int, uint64_t*, uint64_t);
+template __global__ void k_cast_sweep<kF16>(int, uint64_t*, uint64_t);
+
+// K1's word test applied to every pattern vs the IEEE classification.
+__global__ void k_mask_sweep(int kind, unsigned long long* mismatches) {
+    const ScanWord sw = scan_word(kind);
+    const uint64_t total = kind == kF32 ? (1ull << 32) : (1ull << 16);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    unsigned long long bad = 0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += stride) {
+        const uint32_t bits = static_cast<uint32_t>(i);
+        bool nonfinite;
+        uint32_t word;
+        if (kind == kF32) {
+            nonfinite = !isfinite(__uint_as_float(bits));
+            word = bits;
+        } else if (kind == kBF16) {
+            nonfinite = !isfinite(widen_bf16(bits));
+            word = bits << 16;  // test it in the upper lane; lower lane 0 (finite)
+        } else {
+            nonfinite = !isfinite(widen_f16(bits));
+            word = bits << 16;
+        }
+        const bool vec = (((word & sw.mask) + sw.inc) & sw.top) != 0u;
+        const bool scalar = elem_non_finite(bits, kind);
+        bad += (vec != nonfinite) + (scalar != nonfinite);
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
+}  // namespace ma
