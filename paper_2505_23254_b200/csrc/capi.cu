@@ -182,11 +182,7 @@ void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* f
     const uint64_t per_cta = static_cast<uint64_t>(ma::kK1Threads) * ma::kK1Unroll;
     const uint64_t want = std::max<uint64_t>(1, (a.nvec + per_cta - 1) / per_cta);
     const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(d.sms) * 8);
-    if (first) {
-        ma::k1_overflow<true><<<static_cast<unsigned>(grid), ma::kK1Threads, 0, st>>>(a);
-    } else {
-        ma::k1_overflow<false><<<static_cast<unsigned>(grid), ma::kK1Threads, 0, st>>>(a);
-    }
+    ma::launch_k1(a, first != nullptr, static_cast<unsigned>(grid), st);
     CK(cudaGetLastError());
 }
 
@@ -237,39 +233,6 @@ ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, uint64_t tile_
     return s;
 }
 
-template <int GK, int WK, int VEC>
-void launch_k2_t(const ma::SegTable& tab, const ma::AdamArgs& a, cudaStream_t st, int sms) {
-    static int blocks_per_sm = [] {
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ma::k2_adam<GK, WK, VEC>,
-                                                      ma::kK2Threads, 0);
-        return std::max(1, b);
-    }();
-    const uint64_t grid = std::min<uint64_t>(tab.total_tiles,
-                                             static_cast<uint64_t>(sms) * blocks_per_sm);
-    ma::k2_adam<GK, WK, VEC><<<static_cast<unsigned>(grid), ma::kK2Threads, 0, st>>>(tab, a);
-}
-
-template <int GK, int WK>
-void launch_k2_w(const ma::SegTable& tab, const ma::AdamArgs& a, cudaStream_t st, int sms,
-                 int vec) {
-    if (vec == 4) {
-        launch_k2_t<GK, WK, 4>(tab, a, st, sms);
-    } else {
-        launch_k2_t<GK, WK, 8>(tab, a, st, sms);
-    }
-}
-
-template <int GK>
-void launch_k2_g(int wdt, const ma::SegTable& tab, const ma::AdamArgs& a, cudaStream_t st,
-                 int sms, int vec) {
-    switch (wdt) {
-        case MA_DT_NONE: launch_k2_w<GK, ma::kNone>(tab, a, st, sms, vec); break;
-        case MA_DT_BF16: launch_k2_w<GK, ma::kBF16>(tab, a, st, sms, vec); break;
-        default: launch_k2_w<GK, ma::kF16>(tab, a, st, sms, vec); break;
-    }
-}
-
 void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, const ma::AdamArgs& a,
                cudaStream_t st) {
     const DeviceInfo d = device_info();
@@ -290,11 +253,9 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
         }
         if (tab.count == 0) continue;
         tab.total_tiles = tiles;
-        switch (gdt) {
-            case MA_DT_F32: launch_k2_g<ma::kF32>(wdt, tab, a, st, d.sms, vec); break;
-            case MA_DT_BF16: launch_k2_g<ma::kBF16>(wdt, tab, a, st, d.sms, vec); break;
-            default: launch_k2_g<ma::kF16>(wdt, tab, a, st, d.sms, vec); break;
-        }
+        const uint64_t grid = std::min<uint64_t>(
+            tiles, static_cast<uint64_t>(d.sms) * ma::k2_blocks_per_sm(gdt, wdt, vec));
+        ma::launch_k2(gdt, wdt, vec, tab, a, static_cast<unsigned>(grid), st);
         CK(cudaGetLastError());
     }
 }
@@ -569,7 +530,7 @@ int ma_adam_step_bf16(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uin
         if (!kg) CK(cudaMemcpyAsync(const_cast<float*>(sg), g, 4 * n, cudaMemcpyHostToDevice, st));
         const uint64_t grid = std::min<uint64_t>((n + ma::kK2Threads - 1) / ma::kK2Threads,
                                                  static_cast<uint64_t>(d.sms) * 8);
-        ma::k3_adam_bf16<<<static_cast<unsigned>(grid), ma::kK2Threads, 0, st>>>(sp, sm, sv, sg, n, a);
+        ma::launch_k3(sp, sm, sv, sg, n, a, static_cast<unsigned>(grid), st);
         CK(cudaGetLastError());
         if (!kp) CK(cudaMemcpyAsync(p, sp, 2 * n, cudaMemcpyDeviceToHost, st));
         if (!km) CK(cudaMemcpyAsync(m, sm, 2 * n, cudaMemcpyDeviceToHost, st));
@@ -699,7 +660,7 @@ int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t co
 int ma_stepper_finish_async(ma_stepper* s, void* stream) {
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
-        ma::k_step_finish<<<1, 32, 0, as_stream(stream)>>>(s->d_st, s->d_log);
+        ma::launch_step_finish(s->d_st, s->d_log, as_stream(stream));
         CK(cudaGetLastError());
         s->issued += 1;
         s->last = as_stream(stream);
@@ -754,13 +715,7 @@ int ma_gen_seeded_weights_async(float* p, void* w, int w_dtype, uint64_t n, uint
             std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(d.sms) * 16));
         auto* w16 = static_cast<uint16_t*>(w);
         cudaStream_t st = as_stream(stream);
-        if (w_dtype == MA_DT_NONE || !w) {
-            ma::k_gen_weights<ma::kNone><<<grid, 256, 0, st>>>(p, nullptr, n, base, seed);
-        } else if (w_dtype == MA_DT_BF16) {
-            ma::k_gen_weights<ma::kBF16><<<grid, 256, 0, st>>>(p, w16, n, base, seed);
-        } else {
-            ma::k_gen_weights<ma::kF16><<<grid, 256, 0, st>>>(p, w16, n, base, seed);
-        }
+        ma::launch_gen_weights(w ? w_dtype : MA_DT_NONE, p, w16, n, base, seed, grid, st);
         CK(cudaGetLastError());
     });
 }
@@ -778,17 +733,7 @@ int ma_gen_pseudo_grads_async(void* g, int g_dtype, const void* w, int w_dtype, 
             std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(d.sms) * 16));
         const auto* w16 = static_cast<const uint16_t*>(w);
         cudaStream_t st = as_stream(stream);
-#define MA_GEN(GK, WK) ma::k_gen_grads<GK, WK><<<grid, 256, 0, st>>>(g, w16, n, base, seed, step, d_scale, scale)
-        if (w_dtype == MA_DT_BF16) {
-            if (g_dtype == MA_DT_F32) MA_GEN(ma::kF32, ma::kBF16);
-            else if (g_dtype == MA_DT_BF16) MA_GEN(ma::kBF16, ma::kBF16);
-            else MA_GEN(ma::kF16, ma::kBF16);
-        } else {
-            if (g_dtype == MA_DT_F32) MA_GEN(ma::kF32, ma::kF16);
-            else if (g_dtype == MA_DT_BF16) MA_GEN(ma::kBF16, ma::kF16);
-            else MA_GEN(ma::kF16, ma::kF16);
-        }
-#undef MA_GEN
+ma::launch_gen_grads(g_dtype, w_dtype, g, w16, n, base, seed, step, d_scale, scale, grid, st);
         CK(cudaGetLastError());
     });
 }
@@ -797,7 +742,7 @@ int ma_plant_bits_async(void* buf, int dtype, uint64_t index, uint32_t bits, voi
     return guarded([&] {
         check_grad_dtype(dtype);
         device_info();
-        ma::k_plant<<<1, 1, 0, as_stream(stream)>>>(buf, dtype, index, bits);
+        ma::launch_plant(buf, dtype, index, bits, as_stream(stream));
         CK(cudaGetLastError());
     });
 }
@@ -844,12 +789,7 @@ int ma_debug_cast_sweep(int kind, int block_log2, uint64_t* out_host) {
         const uint64_t nb = 1ull << (32 - block_log2);
         uint64_t* d = nullptr;
         CK(cudaMalloc(&d, nb * 8));
-        const unsigned grid = static_cast<unsigned>((nb + 63) / 64);
-        if (kind == MA_DT_BF16) {
-            ma::k_cast_sweep<ma::kBF16><<<grid, 64>>>(block_log2, d, nb);
-        } else {
-            ma::k_cast_sweep<ma::kF16><<<grid, 64>>>(block_log2, d, nb);
-        }
+        ma::launch_cast_sweep(kind, block_log2, d, nb);
         const cudaError_t e = cudaGetLastError();
         const cudaError_t e2 = cudaMemcpy(out_host, d, nb * 8, cudaMemcpyDeviceToHost);
         cudaFree(d);
@@ -865,7 +805,7 @@ int ma_debug_mask_sweep(int kind, uint64_t* mismatches) {
         unsigned long long* d = nullptr;
         CK(cudaMalloc(&d, 8));
         CK(cudaMemset(d, 0, 8));
-        ma::k_mask_sweep<<<dv.sms * 8, 256>>>(kind, d);
+        ma::launch_mask_sweep(kind, d, static_cast<unsigned>(dv.sms * 8));
         const cudaError_t e = cudaGetLastError();
         unsigned long long h = 0;
         const cudaError_t e2 = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);

@@ -13,6 +13,8 @@
 // one-touch state does not thrash L2.
 #include "kernels.cuh"
 
+#include <type_traits>
+
 namespace ma {
 
 // ============================================================== K1
@@ -91,8 +93,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
     if (__any_sync(0xFFFFFFFFu, (acc & sw.top) != 0u) && lane == 0) *a.flag = 1u;
 }
 
-template __global__ void k1_overflow<false>(K1Args);
-template __global__ void k1_overflow<true>(K1Args);
 
 // ============================================================== K2
 __device__ __forceinline__ bool resolve_step(const AdamArgs& a, StepScalars& s) {
@@ -247,19 +247,6 @@ __global__ void __launch_bounds__(kK2Threads) k2_adam(SegTable tab, AdamArgs a) 
     }
 }
 
-#define MA_INST_K2(GK, WK)                                        \
-    template __global__ void k2_adam<GK, WK, 4>(SegTable, AdamArgs); \
-    template __global__ void k2_adam<GK, WK, 8>(SegTable, AdamArgs);
-MA_INST_K2(kF32, kNone)
-MA_INST_K2(kF32, kBF16)
-MA_INST_K2(kF32, kF16)
-MA_INST_K2(kBF16, kNone)
-MA_INST_K2(kBF16, kBF16)
-MA_INST_K2(kBF16, kF16)
-MA_INST_K2(kF16, kNone)
-MA_INST_K2(kF16, kBF16)
-MA_INST_K2(kF16, kF16)
-#undef MA_INST_K2
 
 // ============================================================== K3
 // bf16 state (Bf16Access, optimizer.cpp:83-93): widen, same fp32 update,
@@ -317,9 +304,6 @@ __global__ void k_gen_weights(float* __restrict__ p, uint16_t* __restrict__ w, u
         if constexpr (WK != kNone) w[i] = narrow<WK>(x);
     }
 }
-template __global__ void k_gen_weights<kNone>(float*, uint16_t*, uint64_t, uint64_t, uint64_t);
-template __global__ void k_gen_weights<kBF16>(float*, uint16_t*, uint64_t, uint64_t, uint64_t);
-template __global__ void k_gen_weights<kF16>(float*, uint16_t*, uint64_t, uint64_t, uint64_t);
 
 template <int GK, int WK>
 __global__ void k_gen_grads(void* __restrict__ g, const uint16_t* __restrict__ w, uint64_t n,
@@ -337,12 +321,6 @@ __global__ void k_gen_grads(void* __restrict__ g, const uint16_t* __restrict__ w
         }
     }
 }
-template __global__ void k_gen_grads<kF32, kBF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
-template __global__ void k_gen_grads<kF32, kF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
-template __global__ void k_gen_grads<kBF16, kBF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
-template __global__ void k_gen_grads<kBF16, kF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
-template __global__ void k_gen_grads<kF16, kBF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
-template __global__ void k_gen_grads<kF16, kF16>(void*, const uint16_t*, uint64_t, uint64_t, uint64_t, uint64_t, const float*, float);
 
 __global__ void k_plant(void* buf, int dtype, uint64_t index, uint32_t bits) {
     if (dtype == kF32) {
@@ -368,8 +346,6 @@ __global__ void k_cast_sweep(int log2, uint64_t* out, uint64_t nblocks) {
     }
     out[b] = h;
 }
-template __global__ void k_cast_sweep<kBF16>(int, uint64_t*, uint64_t);
-template __global__ void k_cast_sweep<kF16>(int, uint64_t*, uint64_t);
 
 // K1's word test applied to every pattern vs the IEEE classification.
 __global__ void k_mask_sweep(int kind, unsigned long long* mismatches) {
@@ -397,6 +373,112 @@ __global__ void k_mask_sweep(int kind, unsigned long long* mismatches) {
         bad += (vec != nonfinite) + (scalar != nonfinite);
     }
     if (bad) atomicAdd(mismatches, bad);
+}
+
+// ============================================================== launchers
+void launch_k1(const K1Args& a, bool track, unsigned grid, cudaStream_t st) {
+    if (track) {
+        k1_overflow<true><<<grid, kK1Threads, 0, st>>>(a);
+    } else {
+        k1_overflow<false><<<grid, kK1Threads, 0, st>>>(a);
+    }
+}
+
+namespace {
+
+template <int GK, int WK, int VEC>
+int k2_occupancy() {
+    static const int b = [] {
+        int x = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k2_adam<GK, WK, VEC>, kK2Threads, 0);
+        return x > 0 ? x : 1;
+    }();
+    return b;
+}
+
+// dispatch (gk, wk, vec) -> template; op(kernel-instantiation tag)
+template <typename F>
+void k2_dispatch(int gk, int wk, int vec, F&& f) {
+#define MA_K2_CASE(G, W)                                                 \
+    if (gk == G && wk == W) {                                            \
+        if (vec == 4) f(std::integral_constant<int, G>{}, std::integral_constant<int, W>{}, \
+                        std::integral_constant<int, 4>{});               \
+        else f(std::integral_constant<int, G>{}, std::integral_constant<int, W>{},          \
+               std::integral_constant<int, 8>{});                        \
+        return;                                                          \
+    }
+    MA_K2_CASE(kF32, kNone) MA_K2_CASE(kF32, kBF16) MA_K2_CASE(kF32, kF16)
+    MA_K2_CASE(kBF16, kNone) MA_K2_CASE(kBF16, kBF16) MA_K2_CASE(kBF16, kF16)
+    MA_K2_CASE(kF16, kNone) MA_K2_CASE(kF16, kBF16) MA_K2_CASE(kF16, kF16)
+#undef MA_K2_CASE
+}
+
+}  // namespace
+
+int k2_blocks_per_sm(int gk, int wk, int vec) {
+    int b = 1;
+    k2_dispatch(gk, wk, vec, [&](auto G, auto W, auto V) {
+        b = k2_occupancy<decltype(G)::value, decltype(W)::value, decltype(V)::value>();
+    });
+    return b;
+}
+
+void launch_k2(int gk, int wk, int vec, const SegTable& tab, const AdamArgs& a, unsigned grid,
+               cudaStream_t st) {
+    k2_dispatch(gk, wk, vec, [&](auto G, auto W, auto V) {
+        k2_adam<decltype(G)::value, decltype(W)::value, decltype(V)::value>
+            <<<grid, kK2Threads, 0, st>>>(tab, a);
+    });
+}
+
+void launch_k3(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
+               const AdamArgs& a, unsigned grid, cudaStream_t st) {
+    k3_adam_bf16<<<grid, kK2Threads, 0, st>>>(p, m, v, g, n, a);
+}
+
+void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s) {
+    k_step_finish<<<1, 32, 0, s>>>(st, log);
+}
+
+void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,
+                        unsigned grid, cudaStream_t st) {
+    if (wk == kBF16) {
+        k_gen_weights<kBF16><<<grid, 256, 0, st>>>(p, w, n, base, seed);
+    } else if (wk == kF16) {
+        k_gen_weights<kF16><<<grid, 256, 0, st>>>(p, w, n, base, seed);
+    } else {
+        k_gen_weights<kNone><<<grid, 256, 0, st>>>(p, nullptr, n, base, seed);
+    }
+}
+
+void launch_gen_grads(int gk, int wk, void* g, const uint16_t* w, uint64_t n, uint64_t base,
+                      uint64_t seed, uint64_t step, const float* d_scale, float scale,
+                      unsigned grid, cudaStream_t st) {
+#define MA_GEN(G, W)                                                                       \
+    if (gk == G && wk == W) {                                                              \
+        k_gen_grads<G, W><<<grid, 256, 0, st>>>(g, w, n, base, seed, step, d_scale, scale); \
+        return;                                                                            \
+    }
+    MA_GEN(kF32, kBF16) MA_GEN(kF32, kF16) MA_GEN(kBF16, kBF16) MA_GEN(kBF16, kF16)
+    MA_GEN(kF16, kBF16) MA_GEN(kF16, kF16)
+#undef MA_GEN
+}
+
+void launch_plant(void* buf, int dtype, uint64_t index, uint32_t bits, cudaStream_t st) {
+    k_plant<<<1, 1, 0, st>>>(buf, dtype, index, bits);
+}
+
+void launch_cast_sweep(int kind, int log2, uint64_t* out, uint64_t nblocks) {
+    const unsigned grid = static_cast<unsigned>((nblocks + 63) / 64);
+    if (kind == kBF16) {
+        k_cast_sweep<kBF16><<<grid, 64>>>(log2, out, nblocks);
+    } else {
+        k_cast_sweep<kF16><<<grid, 64>>>(log2, out, nblocks);
+    }
+}
+
+void launch_mask_sweep(int kind, unsigned long long* mismatches, unsigned grid) {
+    k_mask_sweep<<<grid, 256>>>(kind, mismatches);
 }
 
 }  // namespace ma

@@ -57,29 +57,22 @@ struct AdamArgs {
     const float2* bc_table;  // (1-b1^t, 1-b2^t) for t = 1.. when st != nullptr
 };
 
-template <bool kTrack>
-__global__ void k1_overflow(K1Args a);
-
-template <int GK, int WK, int VEC>
-__global__ void k2_adam(SegTable tab, AdamArgs a);
-
-__global__ void k3_adam_bf16(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
-                             AdamArgs a);
-
-__global__ void k_step_finish(StepDev* st, StepLog* log);
-
-template <int WK>
-__global__ void k_gen_weights(float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed);
-
-template <int GK, int WK>
-__global__ void k_gen_grads(void* g, const uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,
-                            uint64_t step, const float* d_scale, float scale);
-
-__global__ void k_plant(void* buf, int dtype, uint64_t index, uint32_t bits);
-
-template <int K>
-__global__ void k_cast_sweep(int log2, uint64_t* out, uint64_t nblocks);
-
-__global__ void k_mask_sweep(int kind, unsigned long long* mismatches);
+// Host-side launchers (defined next to the kernels in kernels.cu so every
+// template instantiation lives in one translation unit).
+void launch_k1(const K1Args& a, bool track, unsigned grid, cudaStream_t st);
+int k2_blocks_per_sm(int gk, int wk, int vec);
+void launch_k2(int gk, int wk, int vec, const SegTable& tab, const AdamArgs& a, unsigned grid,
+               cudaStream_t st);
+void launch_k3(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
+               const AdamArgs& a, unsigned grid, cudaStream_t st);
+void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s);
+void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,
+                        unsigned grid, cudaStream_t st);
+void launch_gen_grads(int gk, int wk, void* g, const uint16_t* w, uint64_t n, uint64_t base,
+                      uint64_t seed, uint64_t step, const float* d_scale, float scale,
+                      unsigned grid, cudaStream_t st);
+void launch_plant(void* buf, int dtype, uint64_t index, uint32_t bits, cudaStream_t st);
+void launch_cast_sweep(int kind, int log2, uint64_t* out, uint64_t nblocks);
+void launch_mask_sweep(int kind, unsigned long long* mismatches, unsigned grid);
 
 }  // namespace ma
