@@ -384,6 +384,7 @@ int ma_overflow_check(const void* grads, uint64_t n, int g_dtype, int track_firs
         if (!grads) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
         device_info();
         Scratch& sc = scratch();
+        CK(cudaDeviceSynchronize());  // synchronous API: operands see all prior device work
         std::lock_guard<std::mutex> lock(sc.mu);
         const uint64_t es = elem_bytes(g_dtype);
         const void* dev = nullptr;
@@ -440,6 +441,7 @@ int ma_adam_step(float* p, float* m, float* v, const void* g, int g_dtype, uint6
         if (n == 0) return;
         device_info();
         Scratch& sc = scratch();
+        CK(cudaDeviceSynchronize());  // synchronous API: operands see all prior device work
         std::lock_guard<std::mutex> lock(sc.mu);
         cudaStream_t st = sc.strm();
         const uint64_t ges = elem_bytes(g_dtype);
@@ -506,6 +508,7 @@ int ma_adam_step_bf16(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uin
         if (n == 0) return;
         const DeviceInfo d = device_info();
         Scratch& sc = scratch();
+        CK(cudaDeviceSynchronize());  // synchronous API: operands see all prior device work
         std::lock_guard<std::mutex> lock(sc.mu);
         cudaStream_t st = sc.strm();
         const void* dp;

@@ -32,7 +32,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
     const uint32_t per_vec = 16u / a.elem_bytes;  // elements per uint4
     uint32_t acc = 0;
 
-    for (uint64_t base = tid; base < a.nvec; base += stride * kK1Unroll) {
+    // The trip count is warp-uniform (tested on the warp's first lane) so the
+    // early-exit shuffle below is always executed by all 32 lanes.
+    for (uint64_t base = tid; base - lane < a.nvec; base += stride * kK1Unroll) {
         uint4 q[kK1Unroll];
 #pragma unroll
         for (int u = 0; u < kK1Unroll; ++u) {
