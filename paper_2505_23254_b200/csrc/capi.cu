@@ -187,10 +187,12 @@ void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* f
 }
 
 // ------------------------------------------------------------ K2 planning
-int k2_vec() {
+// MA_K2_VARIANT selects an alternative K2 schedule (A/B measurements only;
+// see kernels.cuh).  Unset = the production variant.
+int k2_variant() {
     static const int v = [] {
-        const char* e = std::getenv("MA_K2_VEC");
-        return (e && std::atoi(e) == 4) ? 4 : 8;
+        const char* e = std::getenv("MA_K2_VARIANT");
+        return e ? std::atoi(e) : ma::kK2DefaultVariant;
     }();
     return v;
 }
@@ -199,7 +201,11 @@ bool aligned(const void* p, uint64_t h, uint32_t es, uint32_t need) {
     return p == nullptr || ((reinterpret_cast<uintptr_t>(p) + h * es) % need) == 0;
 }
 
-ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, uint64_t tile_begin) {
+// Co-aligns the five streams of one sub-group: `head` scalar elements, then
+// nvec vectors of `vec` elements whose p/m/v start on 16 B and whose 16-bit
+// (or fp32) grads and working weights start on their vector width.
+ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, int tile_vectors, bool stream,
+                 uint64_t tile_begin) {
     ma::Seg s{};
     s.p = g.p;
     s.m = g.m;
@@ -219,14 +225,16 @@ ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, uint64_t tile_
             break;
         }
     }
-    const uint64_t tile_elems = static_cast<uint64_t>(ma::kK2Threads) * vec;
     uint64_t tiles;
     if (s.vector_ok) {
         s.nvec = (g.n - s.head) / vec;
-        tiles = std::max<uint64_t>(1, (s.nvec + ma::kK2Threads - 1) / ma::kK2Threads);
+        tiles = (s.nvec + tile_vectors - 1) / tile_vectors;
+        if (!stream) tiles = std::max<uint64_t>(1, tiles);  // tile 0 carries head/tail
     } else {
         s.nvec = 0;
-        tiles = (g.n + tile_elems - 1) / tile_elems;
+        // stream variants run unaligned sub-groups in their grid-wide scalar pass
+        tiles = stream ? 0 : (g.n + static_cast<uint64_t>(tile_vectors) * vec - 1) /
+                                 (static_cast<uint64_t>(tile_vectors) * vec);
     }
     s.tile_begin = tile_begin;
     s.tile_end = tile_begin + tiles;
@@ -236,10 +244,15 @@ ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, uint64_t tile_
 void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, const ma::AdamArgs& a,
                cudaStream_t st) {
     const DeviceInfo d = device_info();
-    const int vec = k2_vec();
+    const int variant = ma::k2_effective_variant(gdt, wdt, k2_variant());
+    int vec, tile_vectors;
+    bool stream;
+    ma::k2_variant_shape(variant, &vec, &tile_vectors, &stream);
+    const uint64_t cap = static_cast<uint64_t>(d.sms) * ma::k2_blocks_per_sm(gdt, wdt, variant);
     for (uint32_t first = 0; first < count; first += ma::kMaxSegs) {
         ma::SegTable tab{};
         uint64_t tiles = 0;
+        uint64_t scalar_elems = 0;
         const uint32_t last = std::min<uint32_t>(count, first + ma::kMaxSegs);
         for (uint32_t k = first; k < last; ++k) {
             if (groups[k].n == 0) continue;
@@ -247,15 +260,20 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
                 fail(MA_ERR_INVALID_ARGUMENT, "sub-group with a null state/grad pointer");
             if (wdt != MA_DT_NONE && !groups[k].w)
                 fail(MA_ERR_INVALID_ARGUMENT, "sub-group without a working-weight buffer");
-            tab.seg[tab.count] = plan_seg(groups[k], gdt, wdt, vec, tiles);
-            tiles = tab.seg[tab.count].tile_end;
+            ma::Seg& sg = tab.seg[tab.count];
+            sg = plan_seg(groups[k], gdt, wdt, vec, tile_vectors, stream, tiles);
+            tiles = sg.tile_end;
+            scalar_elems += sg.vector_ok ? 0 : sg.n;
             tab.count += 1;
         }
         if (tab.count == 0) continue;
         tab.total_tiles = tiles;
-        const uint64_t grid = std::min<uint64_t>(
-            tiles, static_cast<uint64_t>(d.sms) * ma::k2_blocks_per_sm(gdt, wdt, vec));
-        ma::launch_k2(gdt, wdt, vec, tab, a, static_cast<unsigned>(grid), st);
+        uint64_t grid = std::min<uint64_t>(tiles, cap);
+        if (stream && scalar_elems > 0) {
+            grid = std::max<uint64_t>(grid, std::min<uint64_t>(cap, (scalar_elems + 255) / 256));
+        }
+        grid = std::max<uint64_t>(grid, 1);
+        ma::launch_k2(gdt, wdt, variant, tab, a, static_cast<unsigned>(grid), st);
         CK(cudaGetLastError());
     }
 }

@@ -249,6 +249,136 @@ __global__ void __launch_bounds__(kK2Threads) k2_adam(SegTable tab, AdamArgs a) 
     }
 }
 
+// -------------------------------------------------------------- K2 streaming
+// Warp-contiguous variant: a "slot" is 4 consecutive elements (one float4 of
+// p, m, v; 8 B of 16-bit grads / working weights); the 32 lanes of a warp
+// take 32 consecutive slots, so every load/store instruction covers 512 B
+// (or 256 B) of contiguous memory in whole 32-B sectors.  A CTA tile is
+// U * 256 slots; with PF the next tile's loads are issued before the current
+// tile is computed, so HBM keeps streaming while the ALUs run the
+// division/sqrt sequences.
+struct Slot4 {
+    float4 p, m, v;
+    uint4 g;  // f32: four floats; 16-bit kinds: halves packed in .x/.y
+};
+
+template <int GK>
+__device__ __forceinline__ void load_slot(const Seg& sg, uint64_t e, Slot4& s) {
+    s.p = __ldcs(reinterpret_cast<const float4*>(sg.p + e));
+    s.m = __ldcs(reinterpret_cast<const float4*>(sg.m + e));
+    s.v = __ldcs(reinterpret_cast<const float4*>(sg.v + e));
+    if constexpr (GK == kF32) {
+        s.g = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(sg.g) + e));
+    } else {
+        const uint2 t = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.g) + e));
+        s.g.x = t.x;
+        s.g.y = t.y;
+    }
+}
+
+template <int GK, int WK>
+__device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
+                                            const AdamConsts& c, const StepScalars& sc) {
+    float g0, g1, g2, g3;
+    if constexpr (GK == kF32) {
+        g0 = __uint_as_float(s.g.x);
+        g1 = __uint_as_float(s.g.y);
+        g2 = __uint_as_float(s.g.z);
+        g3 = __uint_as_float(s.g.w);
+    } else {
+        g0 = widen<GK>(s.g.x & 0xFFFFu);
+        g1 = widen<GK>(s.g.x >> 16);
+        g2 = widen<GK>(s.g.y & 0xFFFFu);
+        g3 = widen<GK>(s.g.y >> 16);
+    }
+    adam_elem(s.p.x, s.m.x, s.v.x, g0, c, sc);
+    adam_elem(s.p.y, s.m.y, s.v.y, g1, c, sc);
+    adam_elem(s.p.z, s.m.z, s.v.z, g2, c, sc);
+    adam_elem(s.p.w, s.m.w, s.v.w, g3, c, sc);
+    __stcs(reinterpret_cast<float4*>(sg.p + e), s.p);
+    __stcs(reinterpret_cast<float4*>(sg.m + e), s.m);
+    __stcs(reinterpret_cast<float4*>(sg.v + e), s.v);
+    if constexpr (WK != kNone) {
+        const uint32_t lo = static_cast<uint32_t>(narrow<WK>(s.p.x)) |
+                            (static_cast<uint32_t>(narrow<WK>(s.p.y)) << 16);
+        const uint32_t hi = static_cast<uint32_t>(narrow<WK>(s.p.z)) |
+                            (static_cast<uint32_t>(narrow<WK>(s.p.w)) << 16);
+        __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.w) + e), make_uint2(lo, hi));
+    }
+}
+
+template <int GK, int U>
+__device__ __forceinline__ void load_tile(const Seg& sg, uint64_t lt, Slot4 (&t)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint64_t j = lt * (U * kK2Threads) + u * kK2Threads + threadIdx.x;
+        if (j < sg.nvec) load_slot<GK>(sg, sg.head + 4 * j, t[u]);
+    }
+}
+
+template <int GK, int WK, int U>
+__device__ __forceinline__ void update_tile(const Seg& sg, uint64_t lt, Slot4 (&t)[U],
+                                            const AdamConsts& c, const StepScalars& sc) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint64_t j = lt * (U * kK2Threads) + u * kK2Threads + threadIdx.x;
+        if (j < sg.nvec) update_slot<GK, WK>(sg, sg.head + 4 * j, t[u], c, sc);
+    }
+}
+
+template <int GK, int WK, int U, bool PF>
+__global__ void __launch_bounds__(kK2Threads) k2_stream(SegTable tab, AdamArgs a) {
+    StepScalars sc;
+    if (!resolve_step(a, sc)) return;  // skipped step: no state touched
+    const AdamConsts c = a.c;
+    uint64_t t = blockIdx.x;
+    if (t < tab.total_tiles) {
+        uint32_t si = 0;
+        while (t >= tab.seg[si].tile_end) ++si;
+        Slot4 cur[U];
+        load_tile<GK, U>(tab.seg[si], t - tab.seg[si].tile_begin, cur);
+        for (;;) {
+            const uint64_t tn = t + gridDim.x;
+            const bool more = tn < tab.total_tiles;
+            uint32_t sn = si;
+            if (more) {
+                while (tn >= tab.seg[sn].tile_end) ++sn;
+            }
+            if constexpr (PF) {
+                Slot4 nxt[U];
+                if (more) load_tile<GK, U>(tab.seg[sn], tn - tab.seg[sn].tile_begin, nxt);
+                update_tile<GK, WK, U>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
+                if (!more) break;
+#pragma unroll
+                for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+            } else {
+                update_tile<GK, WK, U>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
+                if (!more) break;
+                load_tile<GK, U>(tab.seg[sn], tn - tab.seg[sn].tile_begin, cur);
+            }
+            t = tn;
+            si = sn;
+        }
+    }
+    // scalar remainder: unaligned heads/tails, and whole sub-groups whose
+    // pointers cannot be co-aligned (rare; spread over the grid)
+    const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint32_t k = 0; k < tab.count; ++k) {
+        const Seg& sg = tab.seg[k];
+        if (sg.vector_ok) {
+            if (blockIdx.x != k % gridDim.x) continue;
+            const uint64_t tail_begin = sg.head + sg.nvec * 4;
+            const uint64_t extra = sg.head + (sg.n - tail_begin);
+            for (uint64_t q = threadIdx.x; q < extra; q += blockDim.x) {
+                adam_scalar<GK, WK>(sg, q < sg.head ? q : tail_begin + (q - sg.head), c, sc);
+            }
+        } else {
+            for (uint64_t e = gtid; e < sg.n; e += gsize) adam_scalar<GK, WK>(sg, e, c, sc);
+        }
+    }
+}
+
 
 // ============================================================== K3
 // bf16 state (Bf16Access, optimizer.cpp:83-93): widen, same fp32 update,
@@ -388,26 +518,51 @@ void launch_k1(const K1Args& a, bool track, unsigned grid, cudaStream_t st) {
 
 namespace {
 
-template <int GK, int WK, int VEC>
+// K2 variants (see kernels.cuh: k2_variant_shape).  Every dtype pair gets the
+// production variant; the bench pair (bf16 grads, bf16 weights) additionally
+// carries the alternatives used for the A/B measurements in DESIGN.md.
+template <int GK, int WK, int V>
+struct K2Kernel;
+template <int GK, int WK> struct K2Kernel<GK, WK, 0> { static constexpr auto fn = k2_adam<GK, WK, 8>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 1> { static constexpr auto fn = k2_adam<GK, WK, 4>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 2> { static constexpr auto fn = k2_stream<GK, WK, 2, false>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 3> { static constexpr auto fn = k2_stream<GK, WK, 1, true>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 4> { static constexpr auto fn = k2_stream<GK, WK, 2, true>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 5> { static constexpr auto fn = k2_stream<GK, WK, 4, false>; };
+
+template <int GK, int WK, int V>
 int k2_occupancy() {
     static const int b = [] {
         int x = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k2_adam<GK, WK, VEC>, kK2Threads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, K2Kernel<GK, WK, V>::fn, kK2Threads, 0);
         return x > 0 ? x : 1;
     }();
     return b;
 }
 
-// dispatch (gk, wk, vec) -> template; op(kernel-instantiation tag)
+template <int GK, int WK, typename F>
+void k2_variants(int variant, F&& f) {
+    if constexpr (GK == kBF16 && WK == kBF16) {
+        switch (variant) {
+            case 0: f(std::integral_constant<int, 0>{}); return;
+            case 1: f(std::integral_constant<int, 1>{}); return;
+            case 2: f(std::integral_constant<int, 2>{}); return;
+            case 3: f(std::integral_constant<int, 3>{}); return;
+            case 4: f(std::integral_constant<int, 4>{}); return;
+            case 5: f(std::integral_constant<int, 5>{}); return;
+            default: break;
+        }
+    }
+    f(std::integral_constant<int, kK2DefaultVariant>{});
+}
+
 template <typename F>
-void k2_dispatch(int gk, int wk, int vec, F&& f) {
-#define MA_K2_CASE(G, W)                                                 \
-    if (gk == G && wk == W) {                                            \
-        if (vec == 4) f(std::integral_constant<int, G>{}, std::integral_constant<int, W>{}, \
-                        std::integral_constant<int, 4>{});               \
-        else f(std::integral_constant<int, G>{}, std::integral_constant<int, W>{},          \
-               std::integral_constant<int, 8>{});                        \
-        return;                                                          \
+void k2_dispatch(int gk, int wk, int variant, F&& f) {
+#define MA_K2_CASE(G, W)                                                          \
+    if (gk == G && wk == W) {                                                     \
+        k2_variants<G, W>(variant, [&](auto V) { f(std::integral_constant<int, G>{}, \
+                                                   std::integral_constant<int, W>{}, V); }); \
+        return;                                                                   \
     }
     MA_K2_CASE(kF32, kNone) MA_K2_CASE(kF32, kBF16) MA_K2_CASE(kF32, kF16)
     MA_K2_CASE(kBF16, kNone) MA_K2_CASE(kBF16, kBF16) MA_K2_CASE(kBF16, kF16)
@@ -417,18 +572,34 @@ void k2_dispatch(int gk, int wk, int vec, F&& f) {
 
 }  // namespace
 
-int k2_blocks_per_sm(int gk, int wk, int vec) {
+int k2_effective_variant(int gk, int wk, int variant) {
+    int v = kK2DefaultVariant;
+    k2_dispatch(gk, wk, variant, [&](auto, auto, auto V) { v = decltype(V)::value; });
+    return v;
+}
+
+void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
+    static const int kVec[6] = {8, 4, 4, 4, 4, 4};
+    static const int kTile[6] = {kK2Threads, kK2Threads, 2 * kK2Threads, kK2Threads,
+                                 2 * kK2Threads, 4 * kK2Threads};
+    const int v = variant >= 0 && variant < 6 ? variant : kK2DefaultVariant;
+    *vec = kVec[v];
+    *tile_vectors = kTile[v];
+    *stream = v >= 2;
+}
+
+int k2_blocks_per_sm(int gk, int wk, int variant) {
     int b = 1;
-    k2_dispatch(gk, wk, vec, [&](auto G, auto W, auto V) {
+    k2_dispatch(gk, wk, variant, [&](auto G, auto W, auto V) {
         b = k2_occupancy<decltype(G)::value, decltype(W)::value, decltype(V)::value>();
     });
     return b;
 }
 
-void launch_k2(int gk, int wk, int vec, const SegTable& tab, const AdamArgs& a, unsigned grid,
+void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st) {
-    k2_dispatch(gk, wk, vec, [&](auto G, auto W, auto V) {
-        k2_adam<decltype(G)::value, decltype(W)::value, decltype(V)::value>
+    k2_dispatch(gk, wk, variant, [&](auto G, auto W, auto V) {
+        K2Kernel<decltype(G)::value, decltype(W)::value, decltype(V)::value>::fn
             <<<grid, kK2Threads, 0, st>>>(tab, a);
     });
 }

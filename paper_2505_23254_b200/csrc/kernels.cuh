@@ -60,8 +60,14 @@ struct AdamArgs {
 // Host-side launchers (defined next to the kernels in kernels.cu so every
 // template instantiation lives in one translation unit).
 void launch_k1(const K1Args& a, bool track, unsigned grid, cudaStream_t st);
-int k2_blocks_per_sm(int gk, int wk, int vec);
-void launch_k2(int gk, int wk, int vec, const SegTable& tab, const AdamArgs& a, unsigned grid,
+// K2 variants: 0 thread-contiguous VEC=8, 1 thread-contiguous VEC=4,
+// 2 warp-contiguous U=2, 3 warp-contiguous U=1 + prefetch, 4 U=2 + prefetch,
+// 5 U=4.  Dtype pairs other than (bf16, bf16) only carry kK2DefaultVariant.
+constexpr int kK2DefaultVariant = 2;
+int k2_effective_variant(int gk, int wk, int variant);
+void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream);
+int k2_blocks_per_sm(int gk, int wk, int variant);
+void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st);
 void launch_k3(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
                const AdamArgs& a, unsigned grid, cudaStream_t st);

@@ -183,7 +183,7 @@ def test_k2_errors():
 
 def test_k2_random100_golden(golden):
     """test_optimizer.cpp:61-98, bitwise per step, against the reference."""
-    from tests.test_oracle_golden import kat_random100_inputs
+    from kat_inputs import kat_random100_inputs
 
     r = golden("adam_kat.json")["random100"]
     p0, grads = kat_random100_inputs(r)
