@@ -252,20 +252,26 @@ def plant_bits(buf, index, bits, kind=None, stream=None):
 
 
 # ----------------------------------------------------------------- host memory
+def _raw(x):
+    """(pointer, bytes) of any tensor / array, whatever its dtype."""
+    if torch is not None and isinstance(x, torch.Tensor):
+        return x.data_ptr(), x.numel() * x.element_size()
+    return x.ctypes.data, x.nbytes
+
+
 def host_register(array) -> None:
     """PinnedAllocator's "registered" state, made real (pinned.cpp:122-124)."""
-    ptr, n, _ = _info(array)
-    nbytes = array.nbytes if hasattr(array, "nbytes") else array.numel() * array.element_size()
+    ptr, nbytes = _raw(array)
     check(capi.lib().ma_host_register(ptr, nbytes))
 
 
 def host_unregister(array) -> None:
-    ptr, _, _ = _info(array)
+    ptr, _ = _raw(array)
     check(capi.lib().ma_host_unregister(ptr))
 
 
 def pointer_kind(x) -> int:
-    ptr, _, _ = _info(x)
+    ptr, _ = _raw(x)
     k = C.c_int()
     check(capi.lib().ma_pointer_kind(ptr, C.byref(k)))
     return k.value

@@ -179,10 +179,20 @@ void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* f
     a.kind = dt;
     a.elem_bytes = es;
     a.early_exit = early_exit ? 1 : 0;
-    const uint64_t per_cta = static_cast<uint64_t>(ma::kK1Threads) * ma::kK1Unroll;
+    // MA_K1_UNROLL / MA_K1_CTAS_PER_SM: A/B knobs (defaults 4 and 8)
+    static const int unroll = [] {
+        const char* e = std::getenv("MA_K1_UNROLL");
+        return (e && std::atoi(e) == 8) ? 8 : ma::kK1Unroll;
+    }();
+    static const int ctas = [] {
+        const char* e = std::getenv("MA_K1_CTAS_PER_SM");
+        const int v = e ? std::atoi(e) : 8;
+        return v > 0 && v <= 32 ? v : 8;
+    }();
+    const uint64_t per_cta = static_cast<uint64_t>(ma::kK1Threads) * unroll;
     const uint64_t want = std::max<uint64_t>(1, (a.nvec + per_cta - 1) / per_cta);
-    const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(d.sms) * 8);
-    ma::launch_k1(a, first != nullptr, static_cast<unsigned>(grid), st);
+    const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(d.sms) * ctas);
+    ma::launch_k1(a, first != nullptr, unroll, static_cast<unsigned>(grid), st);
     CK(cudaGetLastError());
 }
 

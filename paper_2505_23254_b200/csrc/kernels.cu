@@ -23,7 +23,7 @@ namespace ma {
 // first lane of any warp that saw a non-finite lane (idempotent, no atomics).
 // Early exit (ScanConfig::early_exit, overflow.cpp:88-114): warps poll the
 // flag once per unrolled batch and stop once any CTA has set it.
-template <bool kTrack>
+template <bool kTrack, int kK1Unroll>
 __global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
     const ScanWord sw = scan_word(a.kind);
     const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -508,11 +508,13 @@ __global__ void k_mask_sweep(int kind, unsigned long long* mismatches) {
 }
 
 // ============================================================== launchers
-void launch_k1(const K1Args& a, bool track, unsigned grid, cudaStream_t st) {
+void launch_k1(const K1Args& a, bool track, int unroll, unsigned grid, cudaStream_t st) {
     if (track) {
-        k1_overflow<true><<<grid, kK1Threads, 0, st>>>(a);
+        k1_overflow<true, 4><<<grid, kK1Threads, 0, st>>>(a);
+    } else if (unroll == 8) {
+        k1_overflow<false, 8><<<grid, kK1Threads, 0, st>>>(a);
     } else {
-        k1_overflow<false><<<grid, kK1Threads, 0, st>>>(a);
+        k1_overflow<false, 4><<<grid, kK1Threads, 0, st>>>(a);
     }
 }
 

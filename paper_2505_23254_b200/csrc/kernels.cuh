@@ -10,7 +10,7 @@
 namespace ma {
 
 constexpr int kK1Threads = 256;
-constexpr int kK1Unroll = 4;  // 4 x 16 B in flight per thread per batch
+constexpr int kK1Unroll = 4;  // default: 4 x 16 B in flight per thread per batch (MA_K1_UNROLL=8 for A/B)
 constexpr int kK2Threads = 256;
 constexpr int kMaxSegs = 96;  // sub-groups per K2 launch (8.5 KB of kernel parameters)
 
@@ -59,7 +59,7 @@ struct AdamArgs {
 
 // Host-side launchers (defined next to the kernels in kernels.cu so every
 // template instantiation lives in one translation unit).
-void launch_k1(const K1Args& a, bool track, unsigned grid, cudaStream_t st);
+void launch_k1(const K1Args& a, bool track, int unroll, unsigned grid, cudaStream_t st);
 // K2 variants: 0 thread-contiguous VEC=8, 1 thread-contiguous VEC=4,
 // 2 warp-contiguous U=2, 3 warp-contiguous U=1 + prefetch, 4 U=2 + prefetch,
 // 5 U=4.  Dtype pairs other than (bf16, bf16) only carry kK2DefaultVariant.
