@@ -328,13 +328,18 @@ def ours(args, n, rank, world, local_rank):
     alg_bytes = BYTES_PER_PARAM * n
     k2_gbs = alg_bytes / (k2_ms / 1e3) / 1e9
     launches_per_step = 1 + (len(groups) + 95) // 96 + 1
+    # DRAM bytes per launch of K2 = ncu's dram__bytes_{read,write}.sum per param
+    # (one `ncu --set full` capture, profiles/*_ncu_summary.json) x params/launch
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(workload_config(args, n, world)["workload"])
-        except Exception:
-            traffic = None
+    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True):
+        if name.endswith("_ncu_summary.json"):
+            try:
+                summ = json.load(open(os.path.join(ROOT, "profiles", name)))
+                k2 = next(v for v in summ.values() if "k2_" in v.get("Kernel Name", ""))
+                traffic = k2["dram_bytes_per_param"] * n
+                break
+            except Exception:
+                traffic = None
     line = {
         "metric": METRIC,
         "value": n * world / (ms_per_step / 1e3),

@@ -182,7 +182,7 @@ void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* f
     // MA_K1_UNROLL / MA_K1_CTAS_PER_SM: A/B knobs (defaults 4 and 8)
     static const int unroll = [] {
         const char* e = std::getenv("MA_K1_UNROLL");
-        return (e && std::atoi(e) == 8) ? 8 : ma::kK1Unroll;
+        return e ? (std::atoi(e) == 4 ? 4 : 8) : ma::kK1Unroll;
     }();
     static const int ctas = [] {
         const char* e = std::getenv("MA_K1_CTAS_PER_SM");

@@ -10,7 +10,7 @@
 namespace ma {
 
 constexpr int kK1Threads = 256;
-constexpr int kK1Unroll = 4;  // default: 4 x 16 B in flight per thread per batch (MA_K1_UNROLL=8 for A/B)
+constexpr int kK1Unroll = 8;  // 8 x 16 B in flight per thread per batch (A/B: MA_K1_UNROLL=4)
 constexpr int kK2Threads = 256;
 constexpr int kMaxSegs = 96;  // sub-groups per K2 launch (8.5 KB of kernel parameters)
 
