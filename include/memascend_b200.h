@@ -13,7 +13,7 @@
  *   PinnedAllocator        proj/src/pinned.cpp:98-148 ("registered" becomes cudaHostRegister)
  *   pseudo_gradient etc.   proj/include/memascend/simulator.hpp:23-42 (synthetic workload)
  *
- * The drop-in C++ API (include/memascend/*.hpp, namespace memascend) is a
+ * The drop-in C++ API (headers under include/memascend/, namespace memascend) is a
  * thin layer over these entry points; INTEGRATION.md shows the ctypes / C++
  * bindings a maintainer adds.
  *
