@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "optimizer-step params/sec (overflow check+AdamW) and HBM GB/s vs B200 peak"
 LLAMA3_8B = 8_030_261_248       # proj/src/model.cpp:233
+QWEN25_14B = 14_770_033_664     # proj/src/model.cpp:239 (configs[3], sharded 8 ways)
 CFG1 = 67_108_864               # configs[0]: one 64M-param sub-group
 SUBGROUP = 100_000_000          # optimizer sub-group
 BYTES_PER_PARAM = 28            # 2 g + 12 pmv read + 12 pmv write + 2 w16
@@ -47,7 +48,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["cfg2", "cfg1"], default="cfg2")
+    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg4"], default="cfg2")
+    ap.add_argument("--slots", type=int, default=3, help="cfg4 staging slots")
+    ap.add_argument("--slot-params", type=int, default=1 << 24, help="cfg4 params per slot")
     ap.add_argument("--params", type=int, default=0, help="override params per GPU (debug)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -191,9 +194,12 @@ def reference_arm(args, n_per_gpu, rank, world):
 def workload_config(args, n, world):
     name = ("llama3-8b-optimizer-state-hbm" if args.config == "cfg2" and not args.params
             else "cfg1-64M-subgroup" if args.config == "cfg1" and not args.params
-            else f"custom-{n}")
+            else "qwen2.5-14b-shard-streamed-from-host" if args.config == "cfg4"
+            and not args.params else f"custom-{n}")
+    state = ("fp32 master/m/v in the registered host pool, staged H2D/D2H"
+             if args.config == "cfg4" else "fp32 master/m/v in HBM")
     return {"workload": name, "params_per_gpu": n, "subgroup_params": min(SUBGROUP, n),
-            "grads": "bf16", "working_weights": "bf16", "state": "fp32 master/m/v in HBM",
+            "grads": "bf16", "working_weights": "bf16", "state": state,
             "optimizer": "AdamW lr=1e-3 b1=0.9 b2=0.999 eps=1e-8 wd=0.01, loss scale 65536",
             "parallelism": f"zero-partition x{world} (flag all-reduce only)",
             "l2": "inputs larger than L2 (no flush needed)" if n * 28 > 4 * 126e6
@@ -370,12 +376,116 @@ def ours(args, n, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def ours_streamed(args, n, rank, world, local_rank):
+    """configs[3]: Qwen2.5-14B-shaped state sharded 8 ways (1.85 B params per
+    GPU); fp32 p/m/v live in the registered host pool, grads and working
+    weights in HBM; every 100 M sub-group is staged H2D -> K2 -> D2H through
+    `--slots` device slots.  Bound: the host link, 24 B/param (12 in, 12 out)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_23254_b200 as mab
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    p = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    m = torch.zeros(n, dtype=torch.float32, pin_memory=True)
+    v = torch.zeros(n, dtype=torch.float32, pin_memory=True)
+    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    base = rank * n
+    chunk = 1 << 28
+    tmp = torch.empty(min(n, chunk), dtype=torch.float32, device=dev)
+    for o in range(0, n, chunk):
+        k = min(chunk, n - o)
+        mab.gen_seeded_weights(tmp[:k], w[o:o + k], base=base + o, seed=1)
+        p[o:o + k].copy_(tmp[:k])
+    del tmp
+    mab.gen_pseudo_grads(g, w, step=0, base=base, seed=1, scale=65536.0)
+    st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "bf16", device=dev)
+    sub = min(SUBGROUP, n)
+    groups = mab.Stepper.subgroups(
+        [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub], w[o:o + sub])
+         for o in range(0, n, sub)])
+    slot = args.slot_params
+    staging = torch.empty(3 * args.slots * slot, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step():
+        st.check(g)
+        if world > 1:
+            dist.all_reduce(st.flag, op=dist.ReduceOp.MAX)
+        st.apply_streamed(groups, staging, slot, args.slots)
+        st.finish()
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local_rank) as clk:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+
+    # measured host-link ceiling: concurrent pinned H2D + D2H of 1 GiB each
+    hb = torch.empty(1 << 28, dtype=torch.float32, pin_memory=True)
+    hb2 = torch.empty(1 << 28, dtype=torch.float32, pin_memory=True)
+    db = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+    db2 = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    best = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s1.wait_stream(stream)
+        s2.wait_stream(stream)
+        with torch.cuda.stream(s1):
+            db.copy_(hb, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hb2.copy_(db2, non_blocking=True)
+        stream.wait_stream(s1)
+        stream.wait_stream(s2)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        best = max(best, 2 * (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    if rank != 0:
+        return
+    link = 24 * n / (ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": n * world / (ms / 1e3), "unit": "params/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference generators seeded_weight/pseudo_gradient)",
+        "config": dict(workload_config(args, n, world), slots=args.slots, slot_params=slot),
+        "host_link": {"bound": "host-link", "achieved": link, "unit": "GB/s",
+                      "peak": best, "frac": link / best, "bytes_per_param": 24,
+                      "peak_source": "measured concurrent pinned H2D+D2H, 1 GiB each"},
+        "gpu_launches": (1 + ((n + slot - 1) // slot) + 1) * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    n = args.params or (LLAMA3_8B if args.config == "cfg2" else CFG1)
+    n = args.params or {"cfg2": LLAMA3_8B, "cfg1": CFG1,
+                        "cfg4": (QWEN25_14B + 7) // 8}[args.config]
     if args.impl == "reference":
         reference_arm(args, n, rank, world)
         return
@@ -386,7 +496,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        ours(args, n, rank, world, local_rank)
+        if args.config == "cfg4":
+            ours_streamed(args, n, rank, world, local_rank)
+        else:
+            ours(args, n, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -178,6 +178,20 @@ MA_API uint32_t* ma_stepper_flag(ma_stepper* s);
 MA_API float* ma_stepper_scale(ma_stepper* s);
 MA_API int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
                            void* stream);
+/* Streamed update (configs 4/5: state offloaded to the pinned host pool).
+ * groups[k].p/m/v live in registered host memory, .g/.w on the device.
+ * Sub-group slices are staged through `slots` (2..16) device slots of
+ * slot_elems fp32 x {p, m, v} (d_staging, 3 * slots * slot_elems floats):
+ * H2D on h2d_stream, K2 on stream, D2H on d2h_stream, slot reuse ordered by
+ * events, so the copy-in of slice k+1 and the write-back of k-1 overlap the
+ * update of k (§4.4 double buffering).  Reads this step's flag
+ * first (one 4-byte readback): a skipped step moves no state (*skipped = 1).
+ * Returns with the work enqueued; `stream` is ordered after the last
+ * write-back. */
+MA_API int ma_stepper_apply_streamed(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
+                                     float* d_staging, uint64_t slot_elems, uint32_t slots,
+                                     void* stream, void* h2d_stream, void* d2h_stream,
+                                     int* skipped);
 MA_API int ma_stepper_finish_async(ma_stepper* s, void* stream);
 /* Synchronises the stepper's last stream and reads the scaler state. */
 MA_API int ma_stepper_state(ma_stepper* s, ma_step_state* out);

@@ -201,6 +201,24 @@ class Stepper:
         arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
         check(capi.lib().ma_stepper_apply_async(self._h, arr, len(arr), _stream_ptr(stream)))
 
+    def apply_streamed(self, groups, staging, slot_elems, slots=2, stream=None,
+                       h2d_stream=None, d2h_stream=None) -> bool:
+        """groups' p/m/v in registered host memory, g/w on the device; staging
+        is a device fp32 tensor of 3 * slots * slot_elems.  Returns True when
+        the step was skipped (no state moved)."""
+        arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
+        if h2d_stream is None:
+            self._h2d = getattr(self, "_h2d", None) or torch.cuda.Stream(device=staging.device)
+            h2d_stream = self._h2d
+        if d2h_stream is None:
+            self._d2h = getattr(self, "_d2h", None) or torch.cuda.Stream(device=staging.device)
+            d2h_stream = self._d2h
+        skipped = C.c_int()
+        check(capi.lib().ma_stepper_apply_streamed(
+            self._h, arr, len(arr), staging.data_ptr(), slot_elems, slots, _stream_ptr(stream),
+            _stream_ptr(h2d_stream), _stream_ptr(d2h_stream), C.byref(skipped)))
+        return bool(skipped.value)
+
     def finish(self, stream=None):
         check(capi.lib().ma_stepper_finish_async(self._h, _stream_ptr(stream)))
 

@@ -78,6 +78,8 @@ SIGNATURES = [
     ("ma_stepper_flag", _VP, [_VP]),
     ("ma_stepper_scale", _VP, [_VP]),
     ("ma_stepper_apply_async", _I, [_VP, C.POINTER(Subgroup), _U32, _VP]),
+    ("ma_stepper_apply_streamed", _I, [_VP, C.POINTER(Subgroup), _U32, _VP, _U64, _U32, _VP,
+                                       _VP, _VP, C.POINTER(_I)]),
     ("ma_stepper_finish_async", _I, [_VP, _VP]),
     ("ma_stepper_state", _I, [_VP, C.POINTER(StepState)]),
     ("ma_stepper_history", _I, [_VP, _VP, _VP, _U64, C.POINTER(_U64)]),

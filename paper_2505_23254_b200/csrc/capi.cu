@@ -688,6 +688,75 @@ int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t co
     });
 }
 
+int ma_stepper_apply_streamed(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
+                              float* d_staging, uint64_t slot_elems, uint32_t slots,
+                              void* stream, void* h2d_stream, void* d2h_stream,
+                              int* skipped) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
+        if (!d_staging || slot_elems == 0 || slots < 2 || slots > 16)
+            fail(MA_ERR_INVALID_ARGUMENT, "staging needs 2..16 slots of slot_elems > 0");
+        if (slot_elems % 4) fail(MA_ERR_ALIGNMENT, "slot_elems must be a multiple of 4");
+        cudaStream_t cs = as_stream(stream);
+        cudaStream_t hs = as_stream(h2d_stream);
+        cudaStream_t ds = as_stream(d2h_stream);
+        // The decision decides whether any state moves at all: a skipped step
+        // transfers nothing (test_simulator.cpp:111-125 "skip steps move only
+        // the forward reads").  One 4-byte readback per step.
+        uint32_t flag = 0;
+        CK(cudaMemcpyAsync(&flag, &s->d_st->flag, 4, cudaMemcpyDeviceToHost, cs));
+        CK(cudaStreamSynchronize(cs));
+        if (skipped) *skipped = flag ? 1 : 0;
+        s->last = cs;
+        if (flag) return;
+        stepper_grow_bc(s, s->issued + 1);
+        ma::AdamArgs a{};
+        a.c = s->c;
+        a.skip = &s->d_st->flag;
+        a.st = s->d_st;
+        a.bc_table = s->d_bc;
+        // event ids: [0] entry fence, then per slot {h2d, k2, d2h}
+        cudaEvent_t entry = s->event(0);
+        CK(cudaEventRecord(entry, cs));
+        CK(cudaStreamWaitEvent(hs, entry, 0));
+        auto ev = [&](uint32_t slot, int kind) { return s->event(1 + 3 * slot + kind); };
+        std::vector<bool> used(slots, false);
+        uint64_t chunk_no = 0;
+        for (uint32_t k = 0; k < count; ++k) {
+            const ma_subgroup& gsub = groups[k];
+            for (uint64_t off = 0; off < gsub.n; off += slot_elems, ++chunk_no) {
+                const uint64_t len = std::min(slot_elems, gsub.n - off);
+                const uint32_t slot = static_cast<uint32_t>(chunk_no % slots);
+                float* sp = d_staging + static_cast<uint64_t>(slot) * 3 * slot_elems;
+                float* sm = sp + slot_elems;
+                float* sv = sm + slot_elems;
+                if (used[slot]) CK(cudaStreamWaitEvent(hs, ev(slot, 2), 0));  // slot drained
+                CK(cudaMemcpyAsync(sp, gsub.p + off, len * 4, cudaMemcpyHostToDevice, hs));
+                CK(cudaMemcpyAsync(sm, gsub.m + off, len * 4, cudaMemcpyHostToDevice, hs));
+                CK(cudaMemcpyAsync(sv, gsub.v + off, len * 4, cudaMemcpyHostToDevice, hs));
+                CK(cudaEventRecord(ev(slot, 0), hs));
+                CK(cudaStreamWaitEvent(cs, ev(slot, 0), 0));
+                const uint64_t ges = elem_bytes(s->g_dtype);
+                ma_subgroup part{sp, sm, sv, static_cast<const uint8_t*>(gsub.g) + off * ges,
+                                 gsub.w ? static_cast<uint8_t*>(gsub.w) + off * 2 : nullptr, len};
+                launch_k2(&part, 1, s->g_dtype, s->w_dtype, a, cs);
+                CK(cudaEventRecord(ev(slot, 1), cs));
+                CK(cudaStreamWaitEvent(ds, ev(slot, 1), 0));
+                CK(cudaMemcpyAsync(gsub.p + off, sp, len * 4, cudaMemcpyDeviceToHost, ds));
+                CK(cudaMemcpyAsync(gsub.m + off, sm, len * 4, cudaMemcpyDeviceToHost, ds));
+                CK(cudaMemcpyAsync(gsub.v + off, sv, len * 4, cudaMemcpyDeviceToHost, ds));
+                CK(cudaEventRecord(ev(slot, 2), ds));
+                used[slot] = true;
+            }
+        }
+        // the compute stream (finish, the caller's sync) orders after every write-back
+        for (uint32_t slot = 0; slot < slots; ++slot) {
+            if (used[slot]) CK(cudaStreamWaitEvent(cs, ev(slot, 2), 0));
+        }
+    });
+}
+
 int ma_stepper_finish_async(ma_stepper* s, void* stream) {
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");

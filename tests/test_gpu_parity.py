@@ -383,3 +383,38 @@ def test_full_size_sampled_parity():
     assert (host_f32(m[it]).view(np.uint32) == smp["m"].view(np.uint32)).all()
     assert (host_f32(v[it]).view(np.uint32) == smp["v"].view(np.uint32)).all()
     assert (host_bits16(w[it]) == smp["w"]).all()
+
+
+@pytest.mark.parametrize("slots,slot_elems", [(2, 8192), (3, 30000), (2, 1 << 20)])
+def test_streamed_apply_workload_golden(golden, slots, slot_elems):
+    """Configs 4/5 path: p/m/v in the registered host pool, sub-group slices
+    staged H2D -> K2 -> D2H through device slots; per step vs the reference."""
+    c = next(x for x in golden("workload.json")["cases"] if x["name"] == "cfg_bf16_n100003")
+    n, sub, seed = c["n"], c["subgroup"], c["seed"]
+    hyper = mab.AdamHyper(lr=u2f(c["lr"]), beta1=u2f(c["beta1"]), beta2=u2f(c["beta2"]),
+                          eps=u2f(c["eps"]), weight_decay=u2f(c["wd"]))
+    p = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    m = torch.zeros(n, dtype=torch.float32, pin_memory=True)
+    v = torch.zeros(n, dtype=torch.float32, pin_memory=True)
+    pd = torch.empty(n, dtype=torch.float32, device=DEV)
+    w = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    g = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    mab.gen_seeded_weights(pd, w, seed=seed)
+    p.copy_(pd)
+    assert mab.pointer_kind(p) == 2
+    st = mab.Stepper(hyper, c["init_scale"], c["growth_interval"], "bf16", "bf16")
+    groups = [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub], w[o:o + sub])
+              for o in range(0, n, sub)]
+    staging = torch.empty(3 * slots * slot_elems, dtype=torch.float32, device=DEV)
+    for s, want in enumerate(c["per_step"]):
+        mab.gen_pseudo_grads(g, w, step=s, seed=seed, d_scale=st.scale_t)
+        for f in c["faults"]:
+            if f["step"] == s:
+                mab.plant_bits(g, f["index"] % n, f["bits"])
+        st.check(g)
+        skipped = st.apply_streamed(groups, staging, slot_elems, slots)
+        st.finish()
+        torch.cuda.synchronize()
+        assert skipped == want["overflow"]
+        for k, t in (("p", p), ("m", m), ("v", v), ("w", w)):
+            assert fnv(t) == want[f"{k}_fnv"], (s, k)
