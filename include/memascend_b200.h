@@ -178,6 +178,19 @@ MA_API uint32_t* ma_stepper_flag(ma_stepper* s);
 MA_API float* ma_stepper_scale(ma_stepper* s);
 MA_API int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
                            void* stream);
+/* Pure-bf16 optimizer mode (OptimPrecision::pure_bf16, optimizer.cpp:83-93,
+ * simulator.cpp:470-486): p (the bf16 weights themselves), m and v are bf16
+ * arrays updated in place by K3; g is the stepper's gradient kind. */
+typedef struct ma_subgroup_bf16 {
+    uint16_t* p;
+    uint16_t* m;
+    uint16_t* v;
+    const void* g;
+    uint64_t n;
+} ma_subgroup_bf16;
+MA_API int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups,
+                                       uint32_t count, void* stream);
+
 /* Streamed update (configs 4/5: state offloaded to the pinned host pool).
  * groups[k].p/m/v live in registered host memory, .g/.w on the device.
  * Sub-group slices are staged through `slots` (2..16) device slots of

@@ -201,6 +201,14 @@ class Stepper:
         arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
         check(capi.lib().ma_stepper_apply_async(self._h, arr, len(arr), _stream_ptr(stream)))
 
+    def apply_bf16(self, groups, stream=None):
+        """Pure-bf16 mode: groups of (p_bf16, m_bf16, v_bf16, g) tensors (K3)."""
+        arr = (capi.SubgroupBf16 * len(groups))()
+        for k, (p, m, v, g) in enumerate(groups):
+            arr[k] = capi.SubgroupBf16(p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
+                                       p.numel())
+        check(capi.lib().ma_stepper_apply_bf16_async(self._h, arr, len(arr), _stream_ptr(stream)))
+
     def apply_streamed(self, groups, staging, slot_elems, slots=2, stream=None,
                        h2d_stream=None, d2h_stream=None) -> bool:
         """groups' p/m/v in registered host memory, g/w on the device; staging

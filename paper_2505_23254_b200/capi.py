@@ -52,6 +52,11 @@ class Subgroup(C.Structure):
                 ("w", C.c_void_p), ("n", C.c_uint64)]
 
 
+class SubgroupBf16(C.Structure):
+    _fields_ = [("p", C.c_void_p), ("m", C.c_void_p), ("v", C.c_void_p), ("g", C.c_void_p),
+                ("n", C.c_uint64)]
+
+
 class StepState(C.Structure):
     _fields_ = [("scale", C.c_float), ("clean_steps", C.c_uint32), ("updates", C.c_uint64),
                 ("steps", C.c_uint64), ("last_overflow", C.c_uint32),
@@ -78,6 +83,7 @@ SIGNATURES = [
     ("ma_stepper_flag", _VP, [_VP]),
     ("ma_stepper_scale", _VP, [_VP]),
     ("ma_stepper_apply_async", _I, [_VP, C.POINTER(Subgroup), _U32, _VP]),
+    ("ma_stepper_apply_bf16_async", _I, [_VP, C.POINTER(SubgroupBf16), _U32, _VP]),
     ("ma_stepper_apply_streamed", _I, [_VP, C.POINTER(Subgroup), _U32, _VP, _U64, _U32, _VP,
                                        _VP, _VP, C.POINTER(_I)]),
     ("ma_stepper_finish_async", _I, [_VP, _VP]),

@@ -215,7 +215,7 @@ bool aligned(const void* p, uint64_t h, uint32_t es, uint32_t need) {
 // nvec vectors of `vec` elements whose p/m/v start on 16 B and whose 16-bit
 // (or fp32) grads and working weights start on their vector width.
 ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, int tile_vectors, bool stream,
-                 uint64_t tile_begin) {
+                 uint64_t tile_begin, uint32_t state_es = 4) {
     ma::Seg s{};
     s.p = g.p;
     s.m = g.m;
@@ -226,10 +226,12 @@ ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, int tile_vecto
     const uint32_t ges = static_cast<uint32_t>(elem_bytes(gdt));
     const uint32_t gneed = ges * static_cast<uint32_t>(vec) >= 16 ? 16u : ges * vec;
     const uint32_t wneed = 2u * static_cast<uint32_t>(vec) >= 16 ? 16u : 2u * vec;
+    const uint32_t sneed = state_es * static_cast<uint32_t>(vec) >= 16 ? 16u : state_es * vec;
     s.vector_ok = 0;
     for (uint64_t h = 0; h < static_cast<uint64_t>(vec) && h <= g.n; ++h) {
-        if (aligned(g.p, h, 4, 16) && aligned(g.m, h, 4, 16) && aligned(g.v, h, 4, 16) &&
-            aligned(g.g, h, ges, gneed) && aligned(s.w, h, 2, wneed)) {
+        if (aligned(g.p, h, state_es, sneed) && aligned(g.m, h, state_es, sneed) &&
+            aligned(g.v, h, state_es, sneed) && aligned(g.g, h, ges, gneed) &&
+            aligned(s.w, h, 2, wneed)) {
             s.vector_ok = 1;
             s.head = h;
             break;
@@ -284,6 +286,36 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
         }
         grid = std::max<uint64_t>(grid, 1);
         ma::launch_k2(gdt, wdt, variant, tab, a, static_cast<unsigned>(grid), st);
+        CK(cudaGetLastError());
+    }
+}
+
+// K3: pure-bf16 state; groups' p/m/v point at uint16 (bf16) arrays.
+void launch_k3(const ma_subgroup* groups, uint32_t count, int gdt, const ma::AdamArgs& a,
+               cudaStream_t st) {
+    const DeviceInfo d = device_info();
+    constexpr int kVec = 4, kTile = 2 * ma::kK2Threads;
+    const uint64_t cap = static_cast<uint64_t>(d.sms) * ma::k3_blocks_per_sm(gdt);
+    for (uint32_t first = 0; first < count; first += ma::kMaxSegs) {
+        ma::SegTable tab{};
+        uint64_t tiles = 0, scalar_elems = 0;
+        const uint32_t last = std::min<uint32_t>(count, first + ma::kMaxSegs);
+        for (uint32_t k = first; k < last; ++k) {
+            if (groups[k].n == 0) continue;
+            if (!groups[k].p || !groups[k].m || !groups[k].v || !groups[k].g)
+                fail(MA_ERR_INVALID_ARGUMENT, "sub-group with a null state/grad pointer");
+            ma::Seg& sg = tab.seg[tab.count];
+            sg = plan_seg(groups[k], gdt, MA_DT_NONE, kVec, kTile, true, tiles, 2);
+            tiles = sg.tile_end;
+            scalar_elems += sg.vector_ok ? 0 : sg.n;
+            tab.count += 1;
+        }
+        if (tab.count == 0) continue;
+        tab.total_tiles = tiles;
+        uint64_t grid = std::min<uint64_t>(tiles, cap);
+        if (scalar_elems > 0) grid = std::max<uint64_t>(grid, std::min<uint64_t>(cap, (scalar_elems + 255) / 256));
+        grid = std::max<uint64_t>(grid, 1);
+        ma::launch_k3(gdt, tab, a, static_cast<unsigned>(grid), st);
         CK(cudaGetLastError());
     }
 }
@@ -546,23 +578,24 @@ int ma_adam_step_bf16(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uin
         const int kp = classify(p, &dp), km = classify(m, &dm), kv = classify(v, &dv),
                   kg = classify(g, &dg);
         // K3 is the "next" row: stage everything that is not device-accessible
-        const uint64_t bytes = n * (2 + 2 + 2 + 4);
+        const uint64_t r16 = (2 * n + 255) / 256 * 256;  // 256-B aligned staging regions
+        const uint64_t bytes = 3 * r16 + 4 * n;
         uint8_t* base = static_cast<uint8_t*>(sc.get(bytes));
         uint16_t* sp = kp ? const_cast<uint16_t*>(static_cast<const uint16_t*>(dp))
                           : reinterpret_cast<uint16_t*>(base);
         uint16_t* sm = km ? const_cast<uint16_t*>(static_cast<const uint16_t*>(dm))
-                          : reinterpret_cast<uint16_t*>(base + 2 * n);
+                          : reinterpret_cast<uint16_t*>(base + r16);
         uint16_t* sv = kv ? const_cast<uint16_t*>(static_cast<const uint16_t*>(dv))
-                          : reinterpret_cast<uint16_t*>(base + 4 * n);
-        const float* sg = kg ? static_cast<const float*>(dg) : reinterpret_cast<float*>(base + 6 * n);
+                          : reinterpret_cast<uint16_t*>(base + 2 * r16);
+        const float* sg = kg ? static_cast<const float*>(dg) : reinterpret_cast<float*>(base + 3 * r16);
         if (!kp) CK(cudaMemcpyAsync(sp, p, 2 * n, cudaMemcpyHostToDevice, st));
         if (!km) CK(cudaMemcpyAsync(sm, m, 2 * n, cudaMemcpyHostToDevice, st));
         if (!kv) CK(cudaMemcpyAsync(sv, v, 2 * n, cudaMemcpyHostToDevice, st));
         if (!kg) CK(cudaMemcpyAsync(const_cast<float*>(sg), g, 4 * n, cudaMemcpyHostToDevice, st));
-        const uint64_t grid = std::min<uint64_t>((n + ma::kK2Threads - 1) / ma::kK2Threads,
-                                                 static_cast<uint64_t>(d.sms) * 8);
-        ma::launch_k3(sp, sm, sv, sg, n, a, static_cast<unsigned>(grid), st);
-        CK(cudaGetLastError());
+        (void)d;
+        ma_subgroup grp{reinterpret_cast<float*>(sp), reinterpret_cast<float*>(sm),
+                        reinterpret_cast<float*>(sv), sg, nullptr, n};
+        launch_k3(&grp, 1, MA_DT_F32, a, st);
         if (!kp) CK(cudaMemcpyAsync(p, sp, 2 * n, cudaMemcpyDeviceToHost, st));
         if (!km) CK(cudaMemcpyAsync(m, sm, 2 * n, cudaMemcpyDeviceToHost, st));
         if (!kv) CK(cudaMemcpyAsync(v, sv, 2 * n, cudaMemcpyDeviceToHost, st));
@@ -684,6 +717,29 @@ int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t co
         a.st = s->d_st;
         a.bc_table = s->d_bc;
         launch_k2(groups, count, s->g_dtype, s->w_dtype, a, as_stream(stream));
+        s->last = as_stream(stream);
+    });
+}
+
+int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups, uint32_t count,
+                                void* stream) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
+        stepper_grow_bc(s, s->issued + 1);
+        ma::AdamArgs a{};
+        a.c = s->c;
+        a.skip = &s->d_st->flag;
+        a.st = s->d_st;
+        a.bc_table = s->d_bc;
+        std::vector<ma_subgroup> gs(count);
+        for (uint32_t k = 0; k < count; ++k) {
+            gs[k] = ma_subgroup{reinterpret_cast<float*>(groups[k].p),
+                                reinterpret_cast<float*>(groups[k].m),
+                                reinterpret_cast<float*>(groups[k].v), groups[k].g, nullptr,
+                                groups[k].n};
+        }
+        launch_k3(gs.data(), count, s->g_dtype, a, as_stream(stream));
         s->last = as_stream(stream);
     });
 }

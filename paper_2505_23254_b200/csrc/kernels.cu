@@ -381,23 +381,90 @@ __global__ void __launch_bounds__(kK2Threads) k2_stream(SegTable tab, AdamArgs a
 
 
 // ============================================================== K3
-// bf16 state (Bf16Access, optimizer.cpp:83-93): widen, same fp32 update,
-// round each stored quantity back with the reference's bf16 rounding.
-__global__ void __launch_bounds__(kK2Threads) k3_adam_bf16(uint16_t* __restrict__ p,
-                                                           uint16_t* __restrict__ m,
-                                                           uint16_t* __restrict__ v,
-                                                           const float* __restrict__ g,
-                                                           uint64_t n, AdamArgs a) {
-    StepScalars s;
-    if (!resolve_step(a, s)) return;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += stride) {
-        float pf = widen_bf16(p[i]), mf = widen_bf16(m[i]), vf = widen_bf16(v[i]);
-        adam_elem(pf, mf, vf, g[i], a.c, s);
-        p[i] = bf16_bits(pf);
-        m[i] = bf16_bits(mf);
-        v[i] = bf16_bits(vf);
+// Pure-bf16 mode (Bf16Access, optimizer.cpp:83-93; simulator.cpp:470-486):
+// the weights ARE the bf16 parameters, m and v are bf16; every quantity is
+// widened, updated in fp32 with K2's arithmetic and rounded back with the
+// reference's bf16 rounding.  12 B/param of state traffic (the paper's 58%
+// I/O cut) + the gradient.  Same warp-contiguous 4-element slots as K2; the
+// Seg's p/m/v point at uint16 arrays.
+template <int GK>
+__device__ __forceinline__ void bf16_state_scalar(const Seg& sg, uint64_t e, const AdamConsts& c,
+                                                  const StepScalars& s) {
+    uint16_t* P = reinterpret_cast<uint16_t*>(sg.p);
+    uint16_t* M = reinterpret_cast<uint16_t*>(sg.m);
+    uint16_t* V = reinterpret_cast<uint16_t*>(sg.v);
+    float p = widen_bf16(P[e]), m = widen_bf16(M[e]), v = widen_bf16(V[e]);
+    adam_elem(p, m, v, load_grad1<GK>(sg.g, e), c, s);
+    P[e] = bf16_bits(p);
+    M[e] = bf16_bits(m);
+    V[e] = bf16_bits(v);
+}
+
+__device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d) {
+    return make_uint2(static_cast<uint32_t>(bf16_bits(a)) | (static_cast<uint32_t>(bf16_bits(b)) << 16),
+                      static_cast<uint32_t>(bf16_bits(c)) | (static_cast<uint32_t>(bf16_bits(d)) << 16));
+}
+
+template <int GK>
+__device__ __forceinline__ void bf16_state_slot(const Seg& sg, uint64_t e, const AdamConsts& c,
+                                                const StepScalars& s) {
+    uint2* P = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.p) + e);
+    uint2* M = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.m) + e);
+    uint2* V = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.v) + e);
+    const uint2 pq = __ldcs(P), mq = __ldcs(M), vq = __ldcs(V);
+    float g[4];
+    if constexpr (GK == kF32) {
+        const float4 t = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(sg.g) + e));
+        g[0] = t.x; g[1] = t.y; g[2] = t.z; g[3] = t.w;
+    } else {
+        const uint2 t = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.g) + e));
+        g[0] = widen<GK>(t.x & 0xFFFFu); g[1] = widen<GK>(t.x >> 16);
+        g[2] = widen<GK>(t.y & 0xFFFFu); g[3] = widen<GK>(t.y >> 16);
+    }
+    float p[4] = {widen_bf16(pq.x & 0xFFFFu), widen_bf16(pq.x >> 16), widen_bf16(pq.y & 0xFFFFu),
+                  widen_bf16(pq.y >> 16)};
+    float m[4] = {widen_bf16(mq.x & 0xFFFFu), widen_bf16(mq.x >> 16), widen_bf16(mq.y & 0xFFFFu),
+                  widen_bf16(mq.y >> 16)};
+    float v[4] = {widen_bf16(vq.x & 0xFFFFu), widen_bf16(vq.x >> 16), widen_bf16(vq.y & 0xFFFFu),
+                  widen_bf16(vq.y >> 16)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) adam_elem(p[k], m[k], v[k], g[k], c, s);
+    __stcs(P, pack_bf16x4(p[0], p[1], p[2], p[3]));
+    __stcs(M, pack_bf16x4(m[0], m[1], m[2], m[3]));
+    __stcs(V, pack_bf16x4(v[0], v[1], v[2], v[3]));
+}
+
+template <int GK>
+__global__ void __launch_bounds__(kK2Threads) k3_adam_bf16(SegTable tab, AdamArgs a) {
+    StepScalars sc;
+    if (!resolve_step(a, sc)) return;
+    const AdamConsts c = a.c;
+    constexpr int U = 2;
+    uint32_t si = 0;
+    for (uint64_t t = blockIdx.x; t < tab.total_tiles; t += gridDim.x) {
+        while (t >= tab.seg[si].tile_end) ++si;
+        const Seg& sg = tab.seg[si];
+        const uint64_t lt = t - sg.tile_begin;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = lt * (U * kK2Threads) + u * kK2Threads + threadIdx.x;
+            if (j < sg.nvec) bf16_state_slot<GK>(sg, sg.head + 4 * j, c, sc);
+        }
+    }
+    const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint32_t k = 0; k < tab.count; ++k) {
+        const Seg& sg = tab.seg[k];
+        if (sg.vector_ok) {
+            if (blockIdx.x != k % gridDim.x) continue;
+            const uint64_t tail_begin = sg.head + sg.nvec * 4;
+            const uint64_t extra = sg.head + (sg.n - tail_begin);
+            for (uint64_t q = threadIdx.x; q < extra; q += blockDim.x) {
+                bf16_state_scalar<GK>(sg, q < sg.head ? q : tail_begin + (q - sg.head), c, sc);
+            }
+        } else {
+            for (uint64_t e = gtid; e < sg.n; e += gsize) bf16_state_scalar<GK>(sg, e, c, sc);
+        }
     }
 }
 
@@ -606,9 +673,26 @@ void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs&
     });
 }
 
-void launch_k3(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
-               const AdamArgs& a, unsigned grid, cudaStream_t st) {
-    k3_adam_bf16<<<grid, kK2Threads, 0, st>>>(p, m, v, g, n, a);
+int k3_blocks_per_sm(int gk) {
+    static int b[3] = {0, 0, 0};
+    if (b[gk] == 0) {
+        int x = 0;
+        if (gk == kF32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k3_adam_bf16<kF32>, kK2Threads, 0);
+        else if (gk == kBF16) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k3_adam_bf16<kBF16>, kK2Threads, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k3_adam_bf16<kF16>, kK2Threads, 0);
+        b[gk] = x > 0 ? x : 1;
+    }
+    return b[gk];
+}
+
+void launch_k3(int gk, const SegTable& tab, const AdamArgs& a, unsigned grid, cudaStream_t st) {
+    if (gk == kF32) {
+        k3_adam_bf16<kF32><<<grid, kK2Threads, 0, st>>>(tab, a);
+    } else if (gk == kBF16) {
+        k3_adam_bf16<kBF16><<<grid, kK2Threads, 0, st>>>(tab, a);
+    } else {
+        k3_adam_bf16<kF16><<<grid, kK2Threads, 0, st>>>(tab, a);
+    }
 }
 
 void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s) {

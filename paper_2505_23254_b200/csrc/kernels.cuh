@@ -69,8 +69,9 @@ void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream);
 int k2_blocks_per_sm(int gk, int wk, int variant);
 void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st);
-void launch_k3(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
-               const AdamArgs& a, unsigned grid, cudaStream_t st);
+// K3 (bf16 state): Seg p/m/v point at uint16 arrays; 2 slots of 4 elements.
+int k3_blocks_per_sm(int gk);
+void launch_k3(int gk, const SegTable& tab, const AdamArgs& a, unsigned grid, cudaStream_t st);
 void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s);
 void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,
                         unsigned grid, cudaStream_t st);

@@ -418,3 +418,27 @@ def test_streamed_apply_workload_golden(golden, slots, slot_elems):
         assert skipped == want["overflow"]
         for k, t in (("p", p), ("m", m), ("v", v), ("w", w)):
             assert fnv(t) == want[f"{k}_fnv"], (s, k)
+
+
+@pytest.mark.parametrize("sub", [1 << 30, 10007])
+def test_stepper_pure_bf16_digest(golden, sub):
+    """test_simulator.cpp:44-51: the pure-bf16 run (bf16 weights/m/v, fp32 flat
+    grads) through K3 and the device-resident scaler, vs the reference digest."""
+    t = golden("trainer.json")
+    c = next(x for x in t["cases"] if x["pure_bf16"])
+    n, seed = t["n"], c["seed"]
+    w = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    m = torch.zeros(n, dtype=torch.int16, device=DEV)
+    v = torch.zeros(n, dtype=torch.int16, device=DEV)
+    g = torch.empty(n, dtype=torch.float32, device=DEV)
+    mab.gen_seeded_weights(None, w, n=n, seed=seed)
+    st = mab.Stepper(mab.AdamHyper(), 65536.0, 2000, "f32", "none")
+    groups = [(w[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub]) for o in range(0, n, sub)]
+    for s in range(c["steps"]):
+        mab.gen_pseudo_grads(g, w, step=s, seed=seed, d_scale=st.scale_t)
+        st.check(g)
+        st.apply_bf16(groups)
+        st.finish()
+    torch.cuda.synchronize()
+    assert fnv(w) == c["sim_digest"]
+    assert st.state()["scale"] == c["final_scale"]
