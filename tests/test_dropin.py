@@ -1,5 +1,6 @@
 """Drop-in proof: the reference's OWN test suites for the hot path
-(proj/tests/test_overflow.cpp, test_optimizer.cpp, test_pinned.cpp), compiled
+(proj/tests/test_overflow.cpp, test_optimizer.cpp, test_pinned.cpp, test_pool.cpp,
+test_model.cpp), compiled
 unmodified against our headers (include/memascend/*.hpp) and linked against
 our library (libmemascend.so -> libmemascend_b200.so).  Built by
 `make -C oracle dropin` in the build container (needs /root/reference); the
@@ -28,7 +29,7 @@ def test_dropin_without_gpu_fails_loudly():
     if torch.cuda.is_available():
         pytest.skip("GPU present: see test_dropin_reference_suites_gpu")
     total, passed, failed, p = run()
-    assert total == 26
+    assert total == 44
     # pure host logic (capacity rules, scaler, conversions, ...) passes; every
     # failure is the loud no-device error, never a silent CPU result
     errs = [ln for ln in p.stderr.splitlines() if "threw:" in ln]
@@ -39,4 +40,4 @@ def test_dropin_without_gpu_fails_loudly():
 @pytest.mark.gpu
 def test_dropin_reference_suites_gpu():
     total, passed, failed, p = run()
-    assert (total, failed) == (26, 0), p.stdout + p.stderr
+    assert (total, failed) == (44, 0), p.stdout + p.stderr
