@@ -41,3 +41,19 @@ def test_dropin_without_gpu_fails_loudly():
 def test_dropin_reference_suites_gpu():
     total, passed, failed, p = run()
     assert (total, failed) == (44, 0), p.stdout + p.stderr
+
+
+SIM = os.path.join(ROOT, "oracle", "_ref", "dropin_simulator")
+
+
+@pytest.mark.gpu
+def test_reference_simulator_on_b200_hot_path():
+    """The reference's unmodified offloaded trainer (simulator.cpp +
+    direct_io.cpp) linked to our hot path, run by its own test_simulator.cpp:
+    digests bitwise equal to its in-memory reference trainer, fault skip,
+    I/O accounting, pool fragmentation (13 cases)."""
+    if not os.path.exists(SIM):
+        pytest.skip("oracle/_ref/dropin_simulator not built")
+    p = subprocess.run([SIM], capture_output=True, text=True, cwd="/tmp", timeout=900)
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed", p.stdout)
+    assert m and (int(m.group(1)), int(m.group(3))) == (13, 0), p.stdout + p.stderr
