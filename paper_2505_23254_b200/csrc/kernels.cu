@@ -262,15 +262,38 @@ struct Slot4 {
     uint4 g;  // f32: four floats; 16-bit kinds: halves packed in .x/.y
 };
 
-template <int GK>
+// Load flavours (A/B): 0 = ld.global.cs (evict-first), 1 = default caching,
+// 2 = ld.global.L1::no_allocate.L2::256B (L2 sector prefetch hint).
+template <int LD>
+__device__ __forceinline__ float4 ld4(const float4* p) {
+    if constexpr (LD == 0) return __ldcs(p);
+    if constexpr (LD == 1) return *p;
+    float4 r;
+    asm("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+
+template <int LD>
+__device__ __forceinline__ uint2 ld2(const uint2* p) {
+    if constexpr (LD == 0) return __ldcs(p);
+    if constexpr (LD == 1) return *p;
+    uint2 r;
+    asm("ld.global.L1::no_allocate.L2::256B.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+
+template <int GK, int LD = 0>
 __device__ __forceinline__ void load_slot(const Seg& sg, uint64_t e, Slot4& s) {
-    s.p = __ldcs(reinterpret_cast<const float4*>(sg.p + e));
-    s.m = __ldcs(reinterpret_cast<const float4*>(sg.m + e));
-    s.v = __ldcs(reinterpret_cast<const float4*>(sg.v + e));
+    s.p = ld4<LD>(reinterpret_cast<const float4*>(sg.p + e));
+    s.m = ld4<LD>(reinterpret_cast<const float4*>(sg.m + e));
+    s.v = ld4<LD>(reinterpret_cast<const float4*>(sg.v + e));
     if constexpr (GK == kF32) {
-        s.g = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(sg.g) + e));
+        const float4 t = ld4<LD>(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(sg.g) + e));
+        s.g = make_uint4(__float_as_uint(t.x), __float_as_uint(t.y), __float_as_uint(t.z),
+                         __float_as_uint(t.w));
     } else {
-        const uint2 t = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.g) + e));
+        const uint2 t = ld2<LD>(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.g) + e));
         s.g.x = t.x;
         s.g.y = t.y;
     }
@@ -307,12 +330,12 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
     }
 }
 
-template <int GK, int U>
+template <int GK, int U, int LD = 0>
 __device__ __forceinline__ void load_tile(const Seg& sg, uint64_t lt, Slot4 (&t)[U]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const uint64_t j = lt * (U * kK2Threads) + u * kK2Threads + threadIdx.x;
-        if (j < sg.nvec) load_slot<GK>(sg, sg.head + 4 * j, t[u]);
+        if (j < sg.nvec) load_slot<GK, LD>(sg, sg.head + 4 * j, t[u]);
     }
 }
 
@@ -326,8 +349,8 @@ __device__ __forceinline__ void update_tile(const Seg& sg, uint64_t lt, Slot4 (&
     }
 }
 
-template <int GK, int WK, int U, bool PF>
-__global__ void __launch_bounds__(kK2Threads) k2_stream(SegTable tab, AdamArgs a) {
+template <int GK, int WK, int U, bool PF, int MINB = 1, int LD = 0>
+__global__ void __launch_bounds__(kK2Threads, MINB) k2_stream(SegTable tab, AdamArgs a) {
     StepScalars sc;
     if (!resolve_step(a, sc)) return;  // skipped step: no state touched
     const AdamConsts c = a.c;
@@ -336,7 +359,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_stream(SegTable tab, AdamArgs a
         uint32_t si = 0;
         while (t >= tab.seg[si].tile_end) ++si;
         Slot4 cur[U];
-        load_tile<GK, U>(tab.seg[si], t - tab.seg[si].tile_begin, cur);
+        load_tile<GK, U, LD>(tab.seg[si], t - tab.seg[si].tile_begin, cur);
         for (;;) {
             const uint64_t tn = t + gridDim.x;
             const bool more = tn < tab.total_tiles;
@@ -346,7 +369,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_stream(SegTable tab, AdamArgs a
             }
             if constexpr (PF) {
                 Slot4 nxt[U];
-                if (more) load_tile<GK, U>(tab.seg[sn], tn - tab.seg[sn].tile_begin, nxt);
+                if (more) load_tile<GK, U, LD>(tab.seg[sn], tn - tab.seg[sn].tile_begin, nxt);
                 update_tile<GK, WK, U>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
                 if (!more) break;
 #pragma unroll
@@ -354,7 +377,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_stream(SegTable tab, AdamArgs a
             } else {
                 update_tile<GK, WK, U>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
                 if (!more) break;
-                load_tile<GK, U>(tab.seg[sn], tn - tab.seg[sn].tile_begin, cur);
+                load_tile<GK, U, LD>(tab.seg[sn], tn - tab.seg[sn].tile_begin, cur);
             }
             t = tn;
             si = sn;
@@ -598,6 +621,10 @@ template <int GK, int WK> struct K2Kernel<GK, WK, 2> { static constexpr auto fn 
 template <int GK, int WK> struct K2Kernel<GK, WK, 3> { static constexpr auto fn = k2_stream<GK, WK, 1, true>; };
 template <int GK, int WK> struct K2Kernel<GK, WK, 4> { static constexpr auto fn = k2_stream<GK, WK, 2, true>; };
 template <int GK, int WK> struct K2Kernel<GK, WK, 5> { static constexpr auto fn = k2_stream<GK, WK, 4, false>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 6> { static constexpr auto fn = k2_stream<GK, WK, 2, false, 5, 0>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 7> { static constexpr auto fn = k2_stream<GK, WK, 2, false, 1, 1>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 8> { static constexpr auto fn = k2_stream<GK, WK, 2, false, 1, 2>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 9> { static constexpr auto fn = k2_stream<GK, WK, 2, false, 6, 0>; };
 
 template <int GK, int WK, int V>
 int k2_occupancy() {
@@ -619,6 +646,10 @@ void k2_variants(int variant, F&& f) {
             case 3: f(std::integral_constant<int, 3>{}); return;
             case 4: f(std::integral_constant<int, 4>{}); return;
             case 5: f(std::integral_constant<int, 5>{}); return;
+            case 6: f(std::integral_constant<int, 6>{}); return;
+            case 7: f(std::integral_constant<int, 7>{}); return;
+            case 8: f(std::integral_constant<int, 8>{}); return;
+            case 9: f(std::integral_constant<int, 9>{}); return;
             default: break;
         }
     }
@@ -648,10 +679,11 @@ int k2_effective_variant(int gk, int wk, int variant) {
 }
 
 void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
-    static const int kVec[6] = {8, 4, 4, 4, 4, 4};
-    static const int kTile[6] = {kK2Threads, kK2Threads, 2 * kK2Threads, kK2Threads,
-                                 2 * kK2Threads, 4 * kK2Threads};
-    const int v = variant >= 0 && variant < 6 ? variant : kK2DefaultVariant;
+    static const int kVec[10] = {8, 4, 4, 4, 4, 4, 4, 4, 4, 4};
+    static const int kTile[10] = {kK2Threads, kK2Threads, 2 * kK2Threads, kK2Threads,
+                                  2 * kK2Threads, 4 * kK2Threads, 2 * kK2Threads, 2 * kK2Threads,
+                                  2 * kK2Threads, 2 * kK2Threads};
+    const int v = variant >= 0 && variant < 10 ? variant : kK2DefaultVariant;
     *vec = kVec[v];
     *tile_vectors = kTile[v];
     *stream = v >= 2;
