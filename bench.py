@@ -278,6 +278,9 @@ def ours(args, n, rank, world, local_rank):
         torch.cuda.synchronize()
     clocks = clk.summary()
     elapsed_ms = t0.elapsed_time(t1)
+    if flush is not None:
+        # L2 was flushed before every step: time only the steps themselves
+        elapsed_ms = float(sum(e[0].elapsed_time(e[3]) for e in ev))
     k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
     k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
     state = st.state()
@@ -484,6 +487,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks for the N>1 path on a single GPU (tests/ only): every rank on
+    # MA_BENCH_DEVICE, collectives over MA_BENCH_BACKEND (gloo); default nccl
+    local_rank = int(os.environ.get("MA_BENCH_DEVICE", local_rank))
+    backend = os.environ.get("MA_BENCH_BACKEND", "nccl")
     n = args.params or {"cfg2": LLAMA3_8B, "cfg1": CFG1,
                         "cfg4": (QWEN25_14B + 7) // 8}[args.config]
     if args.impl == "reference":
@@ -494,7 +501,10 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         if args.config == "cfg4":
             ours_streamed(args, n, rank, world, local_rank)
