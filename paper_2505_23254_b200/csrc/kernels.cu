@@ -403,6 +403,148 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_stream(SegTable tab, Adam
 }
 
 
+// -------------------------------------------------------------- K2 TMA
+// Bulk-copy pipeline variant (A/B variant 10): one producer thread streams
+// each 1024-element tile's p, m, v and g into a kStages-deep shared-memory
+// ring with cp.async.bulk (TMA, completion on an mbarrier); four consumer
+// warps wait on the stage's full barrier, update from shared memory and store
+// p/m/v/w straight to global with coalesced 128-bit stores, then release the
+// stage.  Loads are thereby decoupled from the division/sqrt work.
+constexpr int kTmaTile = 1024;        // elements per tile (multiple of 8 => 16-B bulk sizes)
+constexpr int kTmaStages = 6;
+constexpr int kTmaConsumers = 128;    // 4 warps; warp 4 is the producer
+constexpr int kTmaThreads = kTmaConsumers + 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                     "selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// elements of the 1024-element tile starting at e0 that lie in the body
+__device__ __forceinline__ uint32_t tile_count(const Seg& sg, uint64_t e0) {
+    const uint64_t left = sg.head + sg.nvec * 8 - e0;
+    return static_cast<uint32_t>(left < kTmaTile ? left : kTmaTile);
+}
+
+template <int GK>
+constexpr uint32_t tma_stage_bytes() {
+    return kTmaTile * (12u + (GK == kF32 ? 4u : 2u));
+}
+
+template <int GK, int WK, int NC = kTmaConsumers>
+__global__ void __launch_bounds__(NC + 32, 2) k2_tma(SegTable tab, AdamArgs a) {
+    StepScalars sc;
+    if (!resolve_step(a, sc)) return;
+    const AdamConsts c = a.c;
+    constexpr uint32_t kGB = GK == kF32 ? 4u : 2u;
+    constexpr uint32_t kStage = tma_stage_bytes<GK>();
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * kStage);
+    uint64_t* empty = full + kTmaStages;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    if (warp == NC / 32) {
+        // ---------------- producer
+        if ((threadIdx.x & 31) == 0) {
+            uint32_t si = 0, it = 0;
+            for (uint64_t t = blockIdx.x; t < tab.total_tiles; t += gridDim.x, ++it) {
+                while (t >= tab.seg[si].tile_end) ++si;
+                const Seg& sg = tab.seg[si];
+                const uint64_t e0 = sg.head + (t - sg.tile_begin) * kTmaTile;
+                const uint32_t cnt = static_cast<uint32_t>(
+                    tile_count(sg, e0));
+                const uint32_t s = it % kTmaStages;
+                mbar_wait(&empty[s], ((it / kTmaStages) & 1u) ^ 1u);
+                unsigned char* st = smem + s * kStage;
+                mbar_expect_tx(&full[s], cnt * (12u + kGB));
+                bulk_g2s(st, sg.p + e0, cnt * 4u, &full[s]);
+                bulk_g2s(st + kTmaTile * 4, sg.m + e0, cnt * 4u, &full[s]);
+                bulk_g2s(st + kTmaTile * 8, sg.v + e0, cnt * 4u, &full[s]);
+                bulk_g2s(st + kTmaTile * 12, static_cast<const unsigned char*>(sg.g) + e0 * kGB,
+                         cnt * kGB, &full[s]);
+            }
+        }
+    } else {
+        // ---------------- consumers: 8 elements per thread per tile
+        uint32_t si = 0, it = 0;
+        for (uint64_t t = blockIdx.x; t < tab.total_tiles; t += gridDim.x, ++it) {
+            while (t >= tab.seg[si].tile_end) ++si;
+            const Seg& sg = tab.seg[si];
+            const uint64_t e0 = sg.head + (t - sg.tile_begin) * kTmaTile;
+            const uint32_t cnt = static_cast<uint32_t>(
+                tile_count(sg, e0));
+            const uint32_t s = it % kTmaStages;
+            mbar_wait(&full[s], (it / kTmaStages) & 1u);
+            const unsigned char* st = smem + s * kStage;
+#pragma unroll
+            for (int half = 0; half < kTmaTile / (4 * NC); ++half) {
+                const uint32_t q = half * (4 * NC) + 4u * threadIdx.x;  // element in tile
+                if (q < cnt) {
+                    Slot4 sl;
+                    sl.p = *reinterpret_cast<const float4*>(st + 4 * q);
+                    sl.m = *reinterpret_cast<const float4*>(st + kTmaTile * 4 + 4 * q);
+                    sl.v = *reinterpret_cast<const float4*>(st + kTmaTile * 8 + 4 * q);
+                    if constexpr (GK == kF32) {
+                        sl.g = *reinterpret_cast<const uint4*>(st + kTmaTile * 12 + 4 * q);
+                    } else {
+                        const uint2 gg = *reinterpret_cast<const uint2*>(st + kTmaTile * 12 + 2 * q);
+                        sl.g.x = gg.x;
+                        sl.g.y = gg.y;
+                    }
+                    update_slot<GK, WK>(sg, e0 + q, sl, c, sc);
+                }
+            }
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+        }
+    }
+    // scalar remainder (heads, tails < 8 elements, unaligned sub-groups)
+    const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint32_t k = 0; k < tab.count; ++k) {
+        const Seg& sg = tab.seg[k];
+        if (sg.vector_ok) {
+            if (blockIdx.x != k % gridDim.x) continue;
+            const uint64_t tail_begin = sg.head + sg.nvec * 8;
+            const uint64_t extra = sg.head + (sg.n - tail_begin);
+            for (uint64_t q = threadIdx.x; q < extra; q += blockDim.x) {
+                adam_scalar<GK, WK>(sg, q < sg.head ? q : tail_begin + (q - sg.head), c, sc);
+            }
+        } else {
+            for (uint64_t e = gtid; e < sg.n; e += gsize) adam_scalar<GK, WK>(sg, e, c, sc);
+        }
+    }
+}
+
 // ============================================================== K3
 // Pure-bf16 mode (Bf16Access, optimizer.cpp:83-93; simulator.cpp:470-486):
 // the weights ARE the bf16 parameters, m and v are bf16; every quantity is
@@ -672,13 +814,46 @@ void k2_dispatch(int gk, int wk, int variant, F&& f) {
 
 }  // namespace
 
+namespace {
+
+constexpr int kTmaVariant = 10;     // 128 consumer threads per CTA
+constexpr int kTmaVariantWide = 11; // 256 consumer threads per CTA
+
+size_t tma_smem_bytes() {
+    return static_cast<size_t>(kTmaStages) * tma_stage_bytes<kBF16>() + 2 * kTmaStages * 8;
+}
+
+template <int NC>
+int tma_blocks_per_sm() {
+    static const int b = [] {
+        cudaFuncSetAttribute(k2_tma<kBF16, kBF16, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(tma_smem_bytes()));
+        int x = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k2_tma<kBF16, kBF16, NC>, NC + 32,
+                                                      tma_smem_bytes());
+        return x > 0 ? x : 1;
+    }();
+    return b;
+}
+
+bool is_tma(int variant) { return variant == kTmaVariant || variant == kTmaVariantWide; }
+
+}  // namespace
+
 int k2_effective_variant(int gk, int wk, int variant) {
+    if (is_tma(variant) && gk == kBF16 && wk == kBF16) return variant;
     int v = kK2DefaultVariant;
     k2_dispatch(gk, wk, variant, [&](auto, auto, auto V) { v = decltype(V)::value; });
     return v;
 }
 
 void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
+    if (is_tma(variant)) {
+        *vec = 8;
+        *tile_vectors = kTmaTile / 8;
+        *stream = true;
+        return;
+    }
     static const int kVec[10] = {8, 4, 4, 4, 4, 4, 4, 4, 4, 4};
     static const int kTile[10] = {kK2Threads, kK2Threads, 2 * kK2Threads, kK2Threads,
                                   2 * kK2Threads, 4 * kK2Threads, 2 * kK2Threads, 2 * kK2Threads,
@@ -690,6 +865,8 @@ void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
 }
 
 int k2_blocks_per_sm(int gk, int wk, int variant) {
+    if (variant == kTmaVariant) return tma_blocks_per_sm<128>();
+    if (variant == kTmaVariantWide) return tma_blocks_per_sm<256>();
     int b = 1;
     k2_dispatch(gk, wk, variant, [&](auto G, auto W, auto V) {
         b = k2_occupancy<decltype(G)::value, decltype(W)::value, decltype(V)::value>();
@@ -699,6 +876,16 @@ int k2_blocks_per_sm(int gk, int wk, int variant) {
 
 void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st) {
+    if (variant == kTmaVariant) {
+        tma_blocks_per_sm<128>();  // sets the dynamic shared-memory attribute once
+        k2_tma<kBF16, kBF16, 128><<<grid, 160, tma_smem_bytes(), st>>>(tab, a);
+        return;
+    }
+    if (variant == kTmaVariantWide) {
+        tma_blocks_per_sm<256>();
+        k2_tma<kBF16, kBF16, 256><<<grid, 288, tma_smem_bytes(), st>>>(tab, a);
+        return;
+    }
     k2_dispatch(gk, wk, variant, [&](auto G, auto W, auto V) {
         K2Kernel<decltype(G)::value, decltype(W)::value, decltype(V)::value>::fn
             <<<grid, kK2Threads, 0, st>>>(tab, a);
