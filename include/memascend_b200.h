@@ -172,6 +172,14 @@ MA_API int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void
  * (the staged H2D of PAPER.md §4.4 / north-star item (1)). */
 MA_API int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
                                        uint64_t chunk_elems, void* stream, void* copy_stream);
+/* Producer-side fused check: dst[i] = src[i] * scale
+ * stored in the stepper's gradient kind — the scaled copy into the flat
+ * buffer of simulator.cpp:401-405, with the device-resident loss scale — and
+ * the overflow test applied to the stored values in the same pass (sets the
+ * step's flag).  Replaces ma_stepper_check_async for buffers produced this
+ * way: the gradients are read once per step instead of twice. */
+MA_API int ma_stepper_ingest_async(ma_stepper* s, const void* src, int src_dtype, void* dst,
+                                   uint64_t n, void* stream);
 /* Device uint32 holding this step's overflow flag (for the cross-rank OR). */
 MA_API uint32_t* ma_stepper_flag(ma_stepper* s);
 /* Device float holding the current loss scale (gradient producers read it). */

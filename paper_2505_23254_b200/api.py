@@ -178,6 +178,12 @@ class Stepper:
         check(capi.lib().ma_stepper_check_async(self._h, grads.data_ptr(), grads.numel(),
                                                 _stream_ptr(stream)))
 
+    def ingest(self, src, dst, src_kind=None, stream=None):
+        """dst = src * scale in the stepper's gradient kind, checked in the same pass."""
+        sp, n, sdt = _info(src, src_kind)
+        check(capi.lib().ma_stepper_ingest_async(self._h, sp, sdt, dst.data_ptr(), n,
+                                                 _stream_ptr(stream)))
+
     def check_from_host(self, host_g, dev_g, chunk_elems=64 << 20, stream=None,
                         copy_stream=None):
         """H2D of pinned host gradients into dev_g, K1 overlapped per chunk."""

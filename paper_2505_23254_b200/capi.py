@@ -80,6 +80,7 @@ SIGNATURES = [
     ("ma_stepper_destroy", _I, [_VP]),
     ("ma_stepper_check_async", _I, [_VP, _VP, _U64, _VP]),
     ("ma_stepper_check_host_async", _I, [_VP, _VP, _VP, _U64, _U64, _VP, _VP]),
+    ("ma_stepper_ingest_async", _I, [_VP, _VP, _I, _VP, _U64, _VP]),
     ("ma_stepper_flag", _VP, [_VP]),
     ("ma_stepper_scale", _VP, [_VP]),
     ("ma_stepper_apply_async", _I, [_VP, C.POINTER(Subgroup), _U32, _VP]),

@@ -701,6 +701,23 @@ int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, 
     });
 }
 
+int ma_stepper_ingest_async(ma_stepper* s, const void* src, int src_dtype, void* dst, uint64_t n,
+                            void* stream) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        check_grad_dtype(src_dtype);
+        if (n == 0) return;
+        if (!src || !dst) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
+        const DeviceInfo d = device_info();
+        const unsigned grid = static_cast<unsigned>(
+            std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(d.sms) * 8));
+        ma::launch_ingest(src_dtype, s->g_dtype, src, dst, n, &s->d_st->scale, &s->d_st->flag,
+                          grid, as_stream(stream));
+        CK(cudaGetLastError());
+        s->last = as_stream(stream);
+    });
+}
+
 uint32_t* ma_stepper_flag(ma_stepper* s) { return s ? &s->d_st->flag : nullptr; }
 
 float* ma_stepper_scale(ma_stepper* s) { return s ? &s->d_st->scale : nullptr; }

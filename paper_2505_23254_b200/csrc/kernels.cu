@@ -686,6 +686,46 @@ __global__ void k_gen_grads(void* __restrict__ g, const uint16_t* __restrict__ w
     }
 }
 
+// Producer-side fused check: the scaled store into the
+// flat gradient buffer that simulator.cpp:401-405 performs
+// (flat[i] = g * scale), with K1's exponent test applied to the stored value
+// in the same pass — the optimizer step then needs no separate K1 read.
+template <int SK, int DK>
+__global__ void __launch_bounds__(256) k_ingest(const void* __restrict__ src, void* __restrict__ dst,
+                                                uint64_t n, const float* d_scale, uint32_t* flag) {
+    const float sc = *d_scale;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    bool bad = false;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += stride) {
+        const float x = SK == kF32 ? reinterpret_cast<const float*>(src)[i]
+                                   : widen<SK>(reinterpret_cast<const uint16_t*>(src)[i]);
+        const float gs = __fmul_rn(x, sc);
+        if constexpr (DK == kF32) {
+            reinterpret_cast<float*>(dst)[i] = gs;
+            bad |= elem_non_finite(__float_as_uint(gs), kF32);
+        } else {
+            const uint16_t h = narrow<DK>(gs);
+            reinterpret_cast<uint16_t*>(dst)[i] = h;
+            bad |= elem_non_finite(h, DK);
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31u) == 0) *flag = 1u;
+}
+
+void launch_ingest(int sk, int dk, const void* src, void* dst, uint64_t n, const float* d_scale,
+                   uint32_t* flag, unsigned grid, cudaStream_t st) {
+#define MA_ING(S, D)                                                               \
+    if (sk == S && dk == D) {                                                      \
+        k_ingest<S, D><<<grid, 256, 0, st>>>(src, dst, n, d_scale, flag);          \
+        return;                                                                    \
+    }
+    MA_ING(kF32, kF32) MA_ING(kF32, kBF16) MA_ING(kF32, kF16)
+    MA_ING(kBF16, kF32) MA_ING(kBF16, kBF16) MA_ING(kBF16, kF16)
+    MA_ING(kF16, kF32) MA_ING(kF16, kBF16) MA_ING(kF16, kF16)
+#undef MA_ING
+}
+
 __global__ void k_plant(void* buf, int dtype, uint64_t index, uint32_t bits) {
     if (dtype == kF32) {
         reinterpret_cast<uint32_t*>(buf)[index] = bits;

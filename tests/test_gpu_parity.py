@@ -442,3 +442,41 @@ def test_stepper_pure_bf16_digest(golden, sub):
     torch.cuda.synchronize()
     assert fnv(w) == c["sim_digest"]
     assert st.state()["scale"] == c["final_scale"]
+
+
+def test_stepper_ingest_fused_check(golden):
+    """§8(f) row 2: raw (unscaled) gradients scaled into the flat buffer with
+    the overflow test fused into that store; no separate K1.  Decisions and
+    the p/m/v/w trajectory must equal the reference composition."""
+    c = next(x for x in golden("workload.json")["cases"] if x["name"] == "cfg_bf16_n100003")
+    n, sub, seed = c["n"], c["subgroup"], c["seed"]
+    hyper = mab.AdamHyper(lr=u2f(c["lr"]), beta1=u2f(c["beta1"]), beta2=u2f(c["beta2"]),
+                          eps=u2f(c["eps"]), weight_decay=u2f(c["wd"]))
+    p = torch.empty(n, dtype=torch.float32, device=DEV)
+    m = torch.zeros(n, dtype=torch.float32, device=DEV)
+    v = torch.zeros(n, dtype=torch.float32, device=DEV)
+    w = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    g = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    raw = torch.empty(n, dtype=torch.float32, device=DEV)
+    mab.gen_seeded_weights(p, w, seed=seed)
+    st = mab.Stepper(hyper, c["init_scale"], c["growth_interval"], "bf16", "bf16")
+    groups = [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub], w[o:o + sub])
+              for o in range(0, n, sub)]
+    for s, want in enumerate(c["per_step"]):
+        mab.gen_pseudo_grads(raw, w, step=s, seed=seed, scale=1.0)  # the producer's raw grads
+        mine = [f for f in c["faults"] if f["step"] == s]
+        for f in mine:
+            if (f["bits"] & 0x7F80) == 0x7F80:  # inf/NaN: planted in the source, stays non-finite
+                mab.plant_bits(raw, f["index"] % n, f["bits"] << 16)
+        st.ingest(raw, g)
+        for f in mine:
+            if (f["bits"] & 0x7F80) != 0x7F80:  # finite control: lands in the flat buffer as-is
+                mab.plant_bits(g, f["index"] % n, f["bits"])
+        st.apply(groups)
+        st.finish()
+        torch.cuda.synchronize()
+        assert bool(st.state()["last_overflow"]) == want["overflow"], s
+        if not want["overflow"]:
+            assert fnv(g) == want["grads_fnv"], s
+        for k, t in (("p", p), ("m", m), ("v", v), ("w", w)):
+            assert fnv(t) == want[f"{k}_fnv"], (s, k)
