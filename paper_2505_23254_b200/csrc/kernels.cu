@@ -266,7 +266,7 @@ struct Slot4 {
 // 2 = ld.global.L1::no_allocate.L2::256B (L2 sector prefetch hint).
 template <int LD>
 __device__ __forceinline__ float4 ld4(const float4* p) {
-    if constexpr (LD == 0) return __ldcs(p);
+    if constexpr (LD == 0 || LD == 3) return __ldcs(p);
     if constexpr (LD == 1) return *p;
     float4 r;
     asm("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -276,7 +276,7 @@ __device__ __forceinline__ float4 ld4(const float4* p) {
 
 template <int LD>
 __device__ __forceinline__ uint2 ld2(const uint2* p) {
-    if constexpr (LD == 0) return __ldcs(p);
+    if constexpr (LD == 0 || LD == 3) return __ldcs(p);
     if constexpr (LD == 1) return *p;
     uint2 r;
     asm("ld.global.L1::no_allocate.L2::256B.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
@@ -299,7 +299,7 @@ __device__ __forceinline__ void load_slot(const Seg& sg, uint64_t e, Slot4& s) {
     }
 }
 
-template <int GK, int WK>
+template <int GK, int WK, bool PROBE = false>
 __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
                                             const AdamConsts& c, const StepScalars& sc) {
     float g0, g1, g2, g3;
@@ -314,10 +314,17 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
         g2 = widen<GK>(s.g.y & 0xFFFFu);
         g3 = widen<GK>(s.g.y >> 16);
     }
-    adam_elem(s.p.x, s.m.x, s.v.x, g0, c, sc);
-    adam_elem(s.p.y, s.m.y, s.v.y, g1, c, sc);
-    adam_elem(s.p.z, s.m.z, s.v.z, g2, c, sc);
-    adam_elem(s.p.w, s.m.w, s.v.w, g3, c, sc);
+    if constexpr (PROBE) {
+        adam_elem_probe(s.p.x, s.m.x, s.v.x, g0, c, sc);
+        adam_elem_probe(s.p.y, s.m.y, s.v.y, g1, c, sc);
+        adam_elem_probe(s.p.z, s.m.z, s.v.z, g2, c, sc);
+        adam_elem_probe(s.p.w, s.m.w, s.v.w, g3, c, sc);
+    } else {
+        adam_elem(s.p.x, s.m.x, s.v.x, g0, c, sc);
+        adam_elem(s.p.y, s.m.y, s.v.y, g1, c, sc);
+        adam_elem(s.p.z, s.m.z, s.v.z, g2, c, sc);
+        adam_elem(s.p.w, s.m.w, s.v.w, g3, c, sc);
+    }
     __stcs(reinterpret_cast<float4*>(sg.p + e), s.p);
     __stcs(reinterpret_cast<float4*>(sg.m + e), s.m);
     __stcs(reinterpret_cast<float4*>(sg.v + e), s.v);
@@ -339,13 +346,13 @@ __device__ __forceinline__ void load_tile(const Seg& sg, uint64_t lt, Slot4 (&t)
     }
 }
 
-template <int GK, int WK, int U>
+template <int GK, int WK, int U, bool PROBE = false>
 __device__ __forceinline__ void update_tile(const Seg& sg, uint64_t lt, Slot4 (&t)[U],
                                             const AdamConsts& c, const StepScalars& sc) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const uint64_t j = lt * (U * kK2Threads) + u * kK2Threads + threadIdx.x;
-        if (j < sg.nvec) update_slot<GK, WK>(sg, sg.head + 4 * j, t[u], c, sc);
+        if (j < sg.nvec) update_slot<GK, WK, PROBE>(sg, sg.head + 4 * j, t[u], c, sc);
     }
 }
 
@@ -370,12 +377,12 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_stream(SegTable tab, Adam
             if constexpr (PF) {
                 Slot4 nxt[U];
                 if (more) load_tile<GK, U, LD>(tab.seg[sn], tn - tab.seg[sn].tile_begin, nxt);
-                update_tile<GK, WK, U>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
+                update_tile<GK, WK, U, LD == 3>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
                 if (!more) break;
 #pragma unroll
                 for (int u = 0; u < U; ++u) cur[u] = nxt[u];
             } else {
-                update_tile<GK, WK, U>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
+                update_tile<GK, WK, U, LD == 3>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
                 if (!more) break;
                 load_tile<GK, U, LD>(tab.seg[sn], tn - tab.seg[sn].tile_begin, cur);
             }
@@ -807,6 +814,8 @@ template <int GK, int WK> struct K2Kernel<GK, WK, 6> { static constexpr auto fn 
 template <int GK, int WK> struct K2Kernel<GK, WK, 7> { static constexpr auto fn = k2_stream<GK, WK, 2, false, 1, 1>; };
 template <int GK, int WK> struct K2Kernel<GK, WK, 8> { static constexpr auto fn = k2_stream<GK, WK, 2, false, 1, 2>; };
 template <int GK, int WK> struct K2Kernel<GK, WK, 9> { static constexpr auto fn = k2_stream<GK, WK, 2, false, 6, 0>; };
+// 12: PROBE ONLY (approximate div/sqrt, not bit-exact) — bounds the cost of the IEEE sequences
+template <int GK, int WK> struct K2Kernel<GK, WK, 12> { static constexpr auto fn = k2_stream<GK, WK, 2, false, 1, 3>; };
 
 template <int GK, int WK, int V>
 int k2_occupancy() {
@@ -832,6 +841,7 @@ void k2_variants(int variant, F&& f) {
             case 7: f(std::integral_constant<int, 7>{}); return;
             case 8: f(std::integral_constant<int, 8>{}); return;
             case 9: f(std::integral_constant<int, 9>{}); return;
+            case 12: f(std::integral_constant<int, 12>{}); return;
             default: break;
         }
     }
