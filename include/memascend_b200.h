@@ -172,6 +172,25 @@ MA_API int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void
  * (the staged H2D of PAPER.md §4.4 / north-star item (1)). */
 MA_API int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
                                        uint64_t chunk_elems, void* stream, void* copy_stream);
+/* Cross-rank skip decision fused into K1 (replaces the all-reduce(max) of
+ * the flag).  Each rank creates an exchange object, publishes its 64-byte
+ * CUDA IPC handle, and opens everybody's handles (rank order); then, per
+ * step, the LAST check of the step goes through ma_stepper_check_xchg_async:
+ * K1's last CTA writes this rank's flag into every peer's slot over NVLink
+ * (peer memory mapped with CUDA IPC), waits for all peers' slots of this
+ * step, and leaves the OR in the local flag, so the following apply skips or
+ * updates identically on every rank.  All ranks must call it the same number
+ * of times.  A peer missing for ~15 s forces a skip and sets the error
+ * reported by ma_xchg_error instead of hanging the GPU. */
+#define MA_IPC_HANDLE_BYTES 64
+typedef struct ma_xchg ma_xchg;
+MA_API int ma_xchg_create(int world, int rank, ma_xchg** out, void* ipc_handle_out);
+MA_API int ma_xchg_open(ma_xchg* x, const void* all_handles);
+MA_API int ma_xchg_error(ma_xchg* x, int* timed_out);
+MA_API int ma_xchg_destroy(ma_xchg* x);
+MA_API int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n, ma_xchg* x,
+                                       void* stream);
+
 /* Producer-side fused check: dst[i] = src[i] * scale
  * stored in the stepper's gradient kind — the scaled copy into the flat
  * buffer of simulator.cpp:401-405, with the device-resident loss scale — and

@@ -174,7 +174,15 @@ class Stepper:
         except Exception:
             pass
 
-    def check(self, grads, stream=None):
+    def check(self, grads, stream=None, xchg: "FlagExchange | None" = None):
+        """K1 into this step's flag; with `xchg`, K1's last CTA also ORs the
+        flag across all ranks over peer memory (use it for the step's last
+        gradient buffer only)."""
+        if xchg is not None:
+            check(capi.lib().ma_stepper_check_xchg_async(
+                self._h, grads.data_ptr() if grads is not None else None,
+                grads.numel() if grads is not None else 0, xchg._h, _stream_ptr(stream)))
+            return
         check(capi.lib().ma_stepper_check_async(self._h, grads.data_ptr(), grads.numel(),
                                                 _stream_ptr(stream)))
 
@@ -259,6 +267,52 @@ class Stepper:
         check(capi.lib().ma_stepper_history(self._h, of.ctypes.data, sc.ctypes.data, cap,
                                             C.byref(cnt)))
         return of[:cnt.value].astype(bool), sc[:cnt.value]
+
+
+class FlagExchange:
+    """Cross-rank skip decision over peer memory, fused into K1 (ma_xchg_*).
+
+    `all_gather(handle: bytes) -> list[bytes]` must return every rank's
+    64-byte CUDA IPC handle in rank order (e.g. torch.distributed
+    all_gather_object); it is the only host-side exchange, done once."""
+
+    def __init__(self, world: int, rank: int, all_gather):
+        h = C.c_void_p()
+        buf = (C.c_ubyte * capi.IPC_HANDLE_BYTES)()
+        check(capi.lib().ma_xchg_create(world, rank, C.byref(h), buf))
+        self._h = h
+        handles = all_gather(bytes(buf))
+        assert len(handles) == world and all(len(x) == capi.IPC_HANDLE_BYTES for x in handles)
+        joined = (C.c_ubyte * (capi.IPC_HANDLE_BYTES * world)).from_buffer_copy(b"".join(handles))
+        check(capi.lib().ma_xchg_open(self._h, joined))
+
+    def timed_out(self) -> bool:
+        e = C.c_int()
+        check(capi.lib().ma_xchg_error(self._h, C.byref(e)))
+        return bool(e.value)
+
+    def close(self):
+        if self._h:
+            capi.lib().ma_xchg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def torch_all_gather_bytes(group=None):
+    """all_gather callable for FlagExchange over torch.distributed."""
+    import torch.distributed as dist
+
+    def gather(b: bytes):
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, b, group=group)
+        return out
+
+    return gather
 
 
 # ----------------------------------------------------------------- workload

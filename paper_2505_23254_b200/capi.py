@@ -25,6 +25,7 @@ ERROR_NAMES = {
 
 DT_F32, DT_BF16, DT_F16, DT_NONE = 0, 1, 2, 3
 STEPPER_STATE_BYTES = 64
+IPC_HANDLE_BYTES = 64
 DTYPES = {"f32": DT_F32, "bf16": DT_BF16, "f16": DT_F16, "none": DT_NONE}
 
 
@@ -80,6 +81,11 @@ SIGNATURES = [
     ("ma_stepper_destroy", _I, [_VP]),
     ("ma_stepper_check_async", _I, [_VP, _VP, _U64, _VP]),
     ("ma_stepper_check_host_async", _I, [_VP, _VP, _VP, _U64, _U64, _VP, _VP]),
+    ("ma_xchg_create", _I, [_I, _I, C.POINTER(_VP), _VP]),
+    ("ma_xchg_open", _I, [_VP, _VP]),
+    ("ma_xchg_error", _I, [_VP, C.POINTER(_I)]),
+    ("ma_xchg_destroy", _I, [_VP]),
+    ("ma_stepper_check_xchg_async", _I, [_VP, _VP, _U64, _VP, _VP]),
     ("ma_stepper_ingest_async", _I, [_VP, _VP, _I, _VP, _U64, _VP]),
     ("ma_stepper_flag", _VP, [_VP]),
     ("ma_stepper_scale", _VP, [_VP]),

@@ -161,13 +161,16 @@ Scratch& scratch() {
 
 // ------------------------------------------------------------ K1 launch
 void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* first,
-               uint64_t index_base, bool early_exit, cudaStream_t st) {
-    if (n == 0) return;
+               uint64_t index_base, bool early_exit, cudaStream_t st,
+               const ma::XchgDev* xchg = nullptr, unsigned long long epoch = 0) {
+    if (n == 0 && !xchg) return;  // an empty rank still takes part in the exchange
     const DeviceInfo d = device_info();
     const uint32_t es = static_cast<uint32_t>(elem_bytes(dt));
     const uintptr_t addr = reinterpret_cast<uintptr_t>(data);
     if (addr % es) fail(MA_ERR_ALIGNMENT, "gradient buffer is not element-aligned");
     ma::K1Args a{};
+    a.xchg = xchg;
+    a.epoch = epoch;
     a.raw = data;
     a.n = n;
     a.head = std::min<uint64_t>(((16 - (addr & 15)) & 15) / es, n);
@@ -698,6 +701,117 @@ int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, 
                       nullptr, 0, true, st);
         }
         s->last = st;
+    });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ peer exchange
+struct ma_xchg {
+    int world = 1;
+    int rank = 0;
+    unsigned long long* slots = nullptr;  // [2][world], shared with peers via CUDA IPC
+    unsigned int* local = nullptr;        // [0] CTA counter, [1] error
+    ma::XchgDev* d_desc = nullptr;
+    std::vector<void*> opened;
+    unsigned long long epoch = 0;
+    bool ready = false;
+};
+
+extern "C" {
+
+int ma_xchg_create(int world, int rank, ma_xchg** out, void* ipc_handle_out) {
+    return guarded([&] {
+        if (!out || !ipc_handle_out) fail(MA_ERR_INVALID_ARGUMENT, "null output");
+        if (world < 1 || world > ma::kMaxRanks || rank < 0 || rank >= world)
+            fail(MA_ERR_INVALID_ARGUMENT, "bad world/rank for the peer exchange");
+        static_assert(sizeof(cudaIpcMemHandle_t) <= MA_IPC_HANDLE_BYTES, "ipc handle size");
+        device_info();
+        auto* x = new ma_xchg();
+        try {
+            x->world = world;
+            x->rank = rank;
+            CK(cudaMalloc(&x->slots, 2 * static_cast<size_t>(world) * sizeof(unsigned long long)));
+            CK(cudaMemset(x->slots, 0, 2 * static_cast<size_t>(world) * sizeof(unsigned long long)));
+            CK(cudaMalloc(&x->local, 2 * sizeof(unsigned int)));
+            CK(cudaMemset(x->local, 0, 2 * sizeof(unsigned int)));
+            CK(cudaMalloc(&x->d_desc, sizeof(ma::XchgDev)));
+            cudaIpcMemHandle_t h;
+            CK(cudaIpcGetMemHandle(&h, x->slots));
+            std::memset(ipc_handle_out, 0, MA_IPC_HANDLE_BYTES);
+            std::memcpy(ipc_handle_out, &h, sizeof h);
+            CK(cudaDeviceSynchronize());  // zeroed slots before any peer can write them
+        } catch (...) {
+            if (x->slots) cudaFree(x->slots);
+            if (x->local) cudaFree(x->local);
+            if (x->d_desc) cudaFree(x->d_desc);
+            delete x;
+            throw;
+        }
+        *out = x;
+    });
+}
+
+int ma_xchg_open(ma_xchg* x, const void* all_handles) {
+    return guarded([&] {
+        if (!x || !all_handles) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
+        if (x->ready) fail(MA_ERR_LIFECYCLE, "peer exchange already opened");
+        ma::XchgDev desc{};
+        desc.world = static_cast<uint32_t>(x->world);
+        desc.rank = static_cast<uint32_t>(x->rank);
+        desc.my_slots = x->slots;
+        desc.counter = x->local;
+        desc.error = x->local + 1;
+        for (int r = 0; r < x->world; ++r) {
+            if (r == x->rank) {
+                desc.peer_slots[r] = x->slots;
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const unsigned char*>(all_handles) + r * MA_IPC_HANDLE_BYTES,
+                        sizeof h);
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            x->opened.push_back(p);
+            desc.peer_slots[r] = static_cast<unsigned long long*>(p);
+        }
+        CK(cudaMemcpy(x->d_desc, &desc, sizeof desc, cudaMemcpyHostToDevice));
+        x->ready = true;
+    });
+}
+
+int ma_xchg_error(ma_xchg* x, int* timed_out) {
+    return guarded([&] {
+        if (!x || !timed_out) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
+        unsigned int e = 0;
+        CK(cudaMemcpy(&e, x->local + 1, sizeof e, cudaMemcpyDeviceToHost));
+        *timed_out = e ? 1 : 0;
+    });
+}
+
+int ma_xchg_destroy(ma_xchg* x) {
+    return guarded([&] {
+        if (!x) return;
+        cudaDeviceSynchronize();
+        for (void* p : x->opened) cudaIpcCloseMemHandle(p);
+        cudaFree(x->slots);
+        cudaFree(x->local);
+        cudaFree(x->d_desc);
+        delete x;
+    });
+}
+
+int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n, ma_xchg* x,
+                                void* stream) {
+    return guarded([&] {
+        if (!s || !x) fail(MA_ERR_INVALID_ARGUMENT, "null stepper / exchange");
+        if (!x->ready) fail(MA_ERR_LIFECYCLE, "peer exchange not opened (ma_xchg_open)");
+        if (n && !g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
+        x->epoch += 1;
+        alignas(16) static const uint32_t dummy[4] = {0, 0, 0, 0};  // never read (n == 0)
+        launch_k1(n ? g : &dummy, n, s->g_dtype, &s->d_st->flag, nullptr, 0, true,
+                  as_stream(stream), x->d_desc, x->epoch);
+        s->last = as_stream(stream);
     });
 }
 

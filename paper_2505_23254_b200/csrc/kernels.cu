@@ -23,6 +23,63 @@ namespace ma {
 // first lane of any warp that saw a non-finite lane (idempotent, no atomics).
 // Early exit (ScanConfig::early_exit, overflow.cpp:88-114): warps poll the
 // flag once per unrolled batch and stop once any CTA has set it.
+// ---- fused cross-rank exchange (last CTA of K1, warp 0) -------------------
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Every rank's K1 ends here: the last CTA to finish publishes this rank's
+// flag into slot [epoch & 1][rank] of every peer (remote stores over
+// NVLink), then waits for all peers' entries of this epoch in its own slots
+// and replaces the local flag by the OR — the all-reduce(max) of the skip
+// decision without a separate collective launch.  A peer that never arrives
+// within ~2^35 cycles raises `error` and forces a skip instead of hanging.
+__device__ void k1_exchange_epilogue(const K1Args& a, unsigned lane) {
+    __shared__ uint32_t is_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(a.xchg->counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last || threadIdx.x >= 32) return;
+    const XchgDev& x = *a.xchg;
+    __threadfence();
+    const uint32_t local = *reinterpret_cast<volatile uint32_t*>(a.flag) != 0u;
+    const unsigned long long bank = a.epoch & 1ull;
+    const unsigned long long val = (a.epoch << 1) | local;
+    for (uint32_t r = lane; r < x.world; r += 32) {
+        st_release_sys(x.peer_slots[r] + bank * x.world + x.rank, val);
+    }
+    uint32_t any = 0, timed_out = 0;
+    const long long start = clock64();
+    for (uint32_t r = lane; r < x.world; r += 32) {
+        unsigned long long v;
+        for (;;) {
+            v = ld_acquire_sys(x.my_slots + bank * x.world + r);
+            if ((v >> 1) == a.epoch) break;
+            if (clock64() - start > (1ll << 35)) {
+                timed_out = 1;
+                break;
+            }
+        }
+        any |= static_cast<uint32_t>(v & 1ull);
+    }
+    any = __any_sync(0xFFFFFFFFu, any != 0u);
+    timed_out = __any_sync(0xFFFFFFFFu, timed_out != 0u);
+    if (lane == 0) {
+        if (timed_out) atomicExch(x.error, 1u);
+        *a.flag = (any || timed_out) ? 1u : 0u;
+        *x.counter = 0u;  // re-arm for the next launch (all CTAs have arrived)
+        __threadfence();
+    }
+}
+
 template <bool kTrack, int kK1Unroll>
 __global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
     const ScanWord sw = scan_word(a.kind);
@@ -92,7 +149,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
             }
         }
     }
-    if (__any_sync(0xFFFFFFFFu, (acc & sw.top) != 0u) && lane == 0) *a.flag = 1u;
+    if (__any_sync(0xFFFFFFFFu, (acc & sw.top) != 0u) && lane == 0) {
+        *a.flag = 1u;
+        if (a.xchg) __threadfence();
+    }
+    if (a.xchg) k1_exchange_epilogue(a, lane);
 }
 
 

@@ -14,6 +14,22 @@ constexpr int kK1Unroll = 8;  // 8 x 16 B in flight per thread per batch (A/B: M
 constexpr int kK2Threads = 256;
 constexpr int kMaxSegs = 96;  // sub-groups per K2 launch (8.5 KB of kernel parameters)
 
+// Cross-rank flag exchange over peer memory (NVLink P2P through CUDA IPC
+// mappings), fused into K1's last CTA.  slots[bank][r] on every rank holds
+// rank r's (epoch << 1 | flag) for epochs of parity `bank`; two banks make it
+// impossible for a rank that runs one step ahead to overwrite a value a slower
+// rank has not read yet.
+constexpr int kMaxRanks = 64;
+
+struct XchgDev {
+    unsigned long long* peer_slots[kMaxRanks];  // rank r's slot array, mapped here
+    unsigned long long* my_slots;               // this rank's slot array [2][world]
+    unsigned int* counter;                      // K1 CTAs finished (last CTA exchanges)
+    unsigned int* error;                        // set on a peer timeout
+    uint32_t world;
+    uint32_t rank;
+};
+
 struct K1Args {
     const uint4* body;      // 16-byte aligned vector body
     const void* raw;        // element 0 (for the unaligned head/tail)
@@ -26,6 +42,8 @@ struct K1Args {
     int kind;
     uint32_t elem_bytes;
     int early_exit;
+    const XchgDev* xchg;    // non-null: exchange the flag with all ranks at the end
+    unsigned long long epoch;
 };
 
 struct Seg {

@@ -161,8 +161,12 @@ class DeviceShard:
 
         plant_bits(self.g, local_index, bits)
 
+    xchg = None  # FlagExchange: fuse the cross-rank OR into K1 (no all-reduce)
+
     def check(self) -> None:
-        if self.n:
+        if self.xchg is not None:
+            self.st.check(self.g if self.n else None, xchg=self.xchg)
+        elif self.n:
             self.st.check(self.g)
 
     def apply(self) -> None:

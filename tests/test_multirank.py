@@ -72,7 +72,7 @@ class OracleShard:
         self.flag[0] = 0
 
 
-def _worker(rank, port, out_dir, device_backend):
+def _worker(rank, port, out_dir, device_backend, p2p=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
@@ -84,9 +84,13 @@ def _worker(rank, port, out_dir, device_backend):
 
             torch.cuda.set_device(0)
             be = DeviceShard(n, base, SUBGROUP, seed=SEED, hyper=mab.AdamHyper(**HYP))
-
-            def allreduce(flag):
-                dist.all_reduce(flag, op=dist.ReduceOp.MAX)  # gloo on a CUDA tensor
+            if p2p:
+                # the OR rides on K1 over peer memory (CUDA IPC mappings)
+                be.xchg = mab.api.FlagExchange(WORLD, rank, mab.api.torch_all_gather_bytes())
+                allreduce = None
+            else:
+                def allreduce(flag):
+                    dist.all_reduce(flag, op=dist.ReduceOp.MAX)  # gloo on a CUDA tensor
         else:
             be = OracleShard(n, base)
 
@@ -98,6 +102,8 @@ def _worker(rank, port, out_dir, device_backend):
             drv.step(s)
         if device_backend:
             torch.cuda.synchronize()
+            if p2p:
+                assert not be.xchg.timed_out()
             of, sc = be.st.history()
             res = dict(p=be.p.cpu().numpy(), m=be.m.cpu().numpy(), v=be.v.cpu().numpy(),
                        w=be.w.view(torch.int16).cpu().numpy().view(np.uint16),
@@ -167,4 +173,15 @@ def test_two_ranks_on_b200_matches_single_process():
         pytest.skip("needs a B200")
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(free_port(), d, True), nprocs=WORLD, join=True)
+        _check_against_single_process(d)
+
+
+@pytest.mark.gpu
+def test_two_ranks_on_b200_peer_exchange_fused_in_k1():
+    """Same run with the skip decision exchanged by K1's last CTA through
+    peer memory (ma_stepper_check_xchg_async) instead of an all-reduce."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(free_port(), d, True, True), nprocs=WORLD, join=True)
         _check_against_single_process(d)
