@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--slot-params", type=int, default=1 << 24, help="cfg4 params per slot")
     ap.add_argument("--params", type=int, default=0, help="override params per GPU (debug)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--flag-exchange", choices=["nccl", "p2p"], default="nccl",
+                    help="N>1: all-reduce the skip flag with NCCL, or fuse the exchange into "
+                         "K1 over peer memory")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=CFG1,
                     help="params in the CPU baseline's bounded sample")
@@ -237,8 +240,14 @@ def ours(args, n, rank, world, local_rank):
     if n * BYTES_PER_PARAM < 4 * 126e6:  # small configs: flush L2 between steps
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    # cross-rank OR of the skip flag: NCCL all-reduce(max) (default), or fused
+    # into K1's last CTA over peer memory (--flag-exchange p2p)
+    xchg = None
+    if world > 1 and args.flag_exchange == "p2p":
+        xchg = mab.api.FlagExchange(world, rank, mab.api.torch_all_gather_bytes())
+
     def allreduce(flag):
-        if world > 1:
+        if world > 1 and xchg is None:
             dist.all_reduce(flag, op=dist.ReduceOp.MAX)
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
@@ -248,7 +257,7 @@ def ours(args, n, rank, world, local_rank):
             flush.zero_()
         if rec:
             rec[0].record(stream)
-        st.check(g)
+        st.check(g, xchg=xchg)
         if rec:
             rec[1].record(stream)
         allreduce(st.flag)
@@ -302,6 +311,8 @@ def ours(args, n, rank, world, local_rank):
 
         def e2e_step():
             st.check_from_host(g_host, g)
+            if xchg is not None:
+                st.check(None, xchg=xchg)  # exchange-only K1 launch (no elements)
             allreduce(st.flag)
             st.apply(groups)
             st.finish()

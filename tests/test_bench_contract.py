@@ -63,3 +63,11 @@ def test_our_arm_two_ranks_one_gpu_gloo():
     j = run(["--params", "100000000", "--steps", "3", "--warmup", "3", "--e2e-steps", "1"],
             nproc=2, env={"MA_BENCH_BACKEND": "gloo", "MA_BENCH_DEVICE": "0"})
     assert j["n_gpus"] == 2 and j["scaling"] == "weak" and j["value"] > 0
+
+
+@pytest.mark.gpu
+def test_our_arm_two_ranks_one_gpu_p2p_exchange():
+    j = run(["--params", "100000000", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
+             "--flag-exchange", "p2p"],
+            nproc=2, env={"MA_BENCH_BACKEND": "gloo", "MA_BENCH_DEVICE": "0"})
+    assert j["n_gpus"] == 2 and j["value"] > 0
