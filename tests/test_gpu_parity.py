@@ -480,3 +480,32 @@ def test_stepper_ingest_fused_check(golden):
             assert fnv(g) == want["grads_fnv"], s
         for k, t in (("p", p), ("m", m), ("v", v), ("w", w)):
             assert fnv(t) == want[f"{k}_fnv"], (s, k)
+
+
+def test_cfg2_full_size_sampled_parity():
+    """BASELINE configs[1] at its full size: 8,030,261,248 params on one B200
+    (81 sub-groups of 100M), 3 steps with a NaN planted past 2^32 at step 1.
+    Decisions exact; 100k random elements plus the 2^32 boundary bit-exact
+    against the oracle's elementwise replay."""
+    torch.cuda.empty_cache()
+    n, steps, seed = 8_030_261_248, 3, 1
+    if torch.cuda.mem_get_info()[0] < n * 16 + (2 << 30):
+        pytest.skip("needs 130 GB of free HBM")
+    faults = [(1, (1 << 32) + 12345, 0x7FC0)]
+    st, p, m, v, w = run_workload_on_gpu(n, steps, seed, "bf16", "bf16", 100_000_000,
+                                         mab.AdamHyper(weight_decay=0.01), 65536.0, 2000, faults)
+    of, _ = st.history()
+    assert of.tolist() == [False, True, False]
+    rs = np.random.default_rng(1)
+    edge = [0, (1 << 31) - 1, 1 << 31, (1 << 32) - 1, 1 << 32, (1 << 32) + 1, n - 1,
+            99_999_999, 100_000_000]
+    idx = np.unique(np.concatenate([rs.integers(0, n, 100_000), edge]).astype(np.uint64))
+    smp = ora.train_sample(idx, of.astype(np.uint8), steps, seed, g_kind="bf16", w_kind="bf16",
+                           hyp=ora.hyper(weight_decay=0.01))
+    it = torch.from_numpy(idx.astype(np.int64)).to(DEV)
+    assert (host_f32(p[it]).view(np.uint32) == smp["p"].view(np.uint32)).all()
+    assert (host_f32(m[it]).view(np.uint32) == smp["m"].view(np.uint32)).all()
+    assert (host_f32(v[it]).view(np.uint32) == smp["v"].view(np.uint32)).all()
+    assert (host_bits16(w[it]) == smp["w"]).all()
+    del p, m, v, w, st
+    torch.cuda.empty_cache()
