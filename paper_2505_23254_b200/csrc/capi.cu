@@ -283,11 +283,27 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
         }
         if (tab.count == 0) continue;
         tab.total_tiles = tiles;
-        uint64_t grid = std::min<uint64_t>(tiles, cap);
-        if (stream && scalar_elems > 0) {
-            grid = std::max<uint64_t>(grid, std::min<uint64_t>(cap, (scalar_elems + 255) / 256));
+        uint64_t grid;
+        if (ma::k2_variant_oneshot(variant)) {
+            // one CTA per tile, then trailing CTAs for heads/tails and
+            // unaligned sub-groups (at least one whenever any remainder exists)
+            bool remainder = scalar_elems > 0;
+            for (uint32_t k = 0; k < tab.count && !remainder; ++k) {
+                const ma::Seg& sg = tab.seg[k];
+                remainder = sg.head + sg.nvec * vec != sg.n;
+            }
+            const uint64_t trailing =
+                remainder ? std::max<uint64_t>(1, std::min<uint64_t>(cap, (scalar_elems + 255) / 256))
+                          : 0;
+            grid = std::max<uint64_t>(1, tiles + trailing);
+            if (grid > 0x7FFFFFFFull) fail(MA_ERR_INVALID_ARGUMENT, "sub-group table too large for one launch");
+        } else {
+            grid = std::min<uint64_t>(tiles, cap);
+            if (stream && scalar_elems > 0) {
+                grid = std::max<uint64_t>(grid, std::min<uint64_t>(cap, (scalar_elems + 255) / 256));
+            }
+            grid = std::max<uint64_t>(grid, 1);
         }
-        grid = std::max<uint64_t>(grid, 1);
         ma::launch_k2(gdt, wdt, variant, tab, a, static_cast<unsigned>(grid), st);
         CK(cudaGetLastError());
     }

@@ -84,6 +84,8 @@ void launch_k1(const K1Args& a, bool track, int unroll, unsigned grid, cudaStrea
 constexpr int kK2DefaultVariant = 2;
 int k2_effective_variant(int gk, int wk, int variant);
 void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream);
+// one tile per CTA: grid = total_tiles + trailing CTAs for the scalar remainder
+bool k2_variant_oneshot(int variant);
 int k2_blocks_per_sm(int gk, int wk, int variant);
 void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st);
