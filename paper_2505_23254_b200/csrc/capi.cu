@@ -290,7 +290,7 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
             bool remainder = scalar_elems > 0;
             for (uint32_t k = 0; k < tab.count && !remainder; ++k) {
                 const ma::Seg& sg = tab.seg[k];
-                remainder = sg.head + sg.nvec * vec != sg.n;
+                remainder = sg.head > 0 || sg.head + sg.nvec * vec != sg.n;
             }
             const uint64_t trailing =
                 remainder ? std::max<uint64_t>(1, std::min<uint64_t>(cap, (scalar_elems + 255) / 256))
