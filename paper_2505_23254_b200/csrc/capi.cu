@@ -192,10 +192,18 @@ void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* f
         const int v = e ? std::atoi(e) : 8;
         return v > 0 && v <= 32 ? v : 8;
     }();
-    const uint64_t per_cta = static_cast<uint64_t>(ma::kK1Threads) * unroll;
+    // MA_K1_GRIDSTRIDE=1 selects the persistent grid-stride form (A/B only)
+    static const bool gridstride = [] {
+        const char* e = std::getenv("MA_K1_GRIDSTRIDE");
+        return e && std::atoi(e) == 1;
+    }();
+    const uint64_t per_cta =
+        static_cast<uint64_t>(ma::kK1Threads) * (gridstride ? unroll : ma::kK1Unroll);
     const uint64_t want = std::max<uint64_t>(1, (a.nvec + per_cta - 1) / per_cta);
-    const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(d.sms) * ctas);
-    ma::launch_k1(a, first != nullptr, unroll, static_cast<unsigned>(grid), st);
+    if (!gridstride && want > 0x7FFFFFFFull) fail(MA_ERR_INVALID_ARGUMENT, "gradient buffer too large");
+    const uint64_t grid =
+        gridstride ? std::min<uint64_t>(want, static_cast<uint64_t>(d.sms) * ctas) : want;
+    ma::launch_k1(a, first != nullptr, unroll, !gridstride, static_cast<unsigned>(grid), st);
     CK(cudaGetLastError());
 }
 

@@ -80,6 +80,75 @@ __device__ void k1_exchange_epilogue(const K1Args& a, unsigned lane) {
     }
 }
 
+// One-shot K1 (production): CTA b scans the U * 256 consecutive 16-byte
+// vectors [b * U * 256, (b + 1) * U * 256) — all U loads in flight before
+// the OR — and exits, so the block scheduler sweeps the buffer front to back
+// (6.9 vs 6.2 TB/s for the grid-stride form, tools/layout_probe.cu).  A CTA
+// that starts after the flag is already set skips its loads (the reference's
+// cooperative early exit); with an exchange it still takes part in it.
+template <bool kTrack, int U>
+__global__ void __launch_bounds__(kK1Threads) k1_oneshot(K1Args a) {
+    const ScanWord sw = scan_word(a.kind);
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t per_vec = 16u / a.elem_bytes;
+    const uint64_t first = static_cast<uint64_t>(blockIdx.x) * U * blockDim.x + threadIdx.x;
+    uint32_t acc = 0;
+    const bool skip = !kTrack && a.early_exit && *reinterpret_cast<volatile uint32_t*>(a.flag) != 0u;
+    if (!skip) {
+        uint4 q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = first + static_cast<uint64_t>(u) * blockDim.x;
+            q[u] = i < a.nvec ? __ldcs(a.body + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            acc |= ((q[u].x & sw.mask) + sw.inc) | ((q[u].y & sw.mask) + sw.inc) |
+                   ((q[u].z & sw.mask) + sw.inc) | ((q[u].w & sw.mask) + sw.inc);
+        }
+        if (kTrack && (acc & sw.top)) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = first + static_cast<uint64_t>(u) * blockDim.x;
+                if (i >= a.nvec) continue;
+                const uint32_t w4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+                for (uint32_t e = 0; e < per_vec; ++e) {
+                    const uint32_t word = w4[(e * a.elem_bytes) >> 2];
+                    const uint32_t bits =
+                        a.elem_bytes == 4 ? word : (word >> (16 * (e & 1u))) & 0xFFFFu;
+                    if (elem_non_finite(bits, a.kind)) {
+                        atomicMin(reinterpret_cast<unsigned long long*>(a.first),
+                                  static_cast<unsigned long long>(a.index_base + a.head +
+                                                                  i * per_vec + e));
+                        break;
+                    }
+                }
+            }
+        }
+    }
+    if (blockIdx.x == 0) {  // unaligned head / tail elements
+        const uint64_t tail_begin = a.head + a.nvec * per_vec;
+        const uint64_t extra = a.head + (a.n - tail_begin);
+        for (uint64_t k = threadIdx.x; k < extra; k += blockDim.x) {
+            const uint64_t e = k < a.head ? k : tail_begin + (k - a.head);
+            const uint32_t bits = a.elem_bytes == 4 ? reinterpret_cast<const uint32_t*>(a.raw)[e]
+                                                    : reinterpret_cast<const uint16_t*>(a.raw)[e];
+            if (elem_non_finite(bits, a.kind)) {
+                acc |= sw.top;
+                if (kTrack) {
+                    atomicMin(reinterpret_cast<unsigned long long*>(a.first),
+                              static_cast<unsigned long long>(a.index_base + e));
+                }
+            }
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, (acc & sw.top) != 0u) && lane == 0) {
+        *a.flag = 1u;
+        if (a.xchg) __threadfence();
+    }
+    if (a.xchg) k1_exchange_epilogue(a, lane);
+}
+
 template <bool kTrack, int kK1Unroll>
 __global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
     const ScanWord sw = scan_word(a.kind);
@@ -899,7 +968,16 @@ __global__ void k_mask_sweep(int kind, unsigned long long* mismatches) {
 }
 
 // ============================================================== launchers
-void launch_k1(const K1Args& a, bool track, int unroll, unsigned grid, cudaStream_t st) {
+void launch_k1(const K1Args& a, bool track, int unroll, bool oneshot, unsigned grid,
+               cudaStream_t st) {
+    if (oneshot) {
+        if (track) {
+            k1_oneshot<true, kK1Unroll><<<grid, kK1Threads, 0, st>>>(a);
+        } else {
+            k1_oneshot<false, kK1Unroll><<<grid, kK1Threads, 0, st>>>(a);
+        }
+        return;
+    }
     if (track) {
         k1_overflow<true, 4><<<grid, kK1Threads, 0, st>>>(a);
     } else if (unroll == 8) {

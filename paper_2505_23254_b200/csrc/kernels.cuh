@@ -77,11 +77,17 @@ struct AdamArgs {
 
 // Host-side launchers (defined next to the kernels in kernels.cu so every
 // template instantiation lives in one translation unit).
-void launch_k1(const K1Args& a, bool track, int unroll, unsigned grid, cudaStream_t st);
-// K2 variants: 0 thread-contiguous VEC=8, 1 thread-contiguous VEC=4,
-// 2 warp-contiguous U=2, 3 warp-contiguous U=1 + prefetch, 4 U=2 + prefetch,
-// 5 U=4.  Dtype pairs other than (bf16, bf16) only carry kK2DefaultVariant.
-constexpr int kK2DefaultVariant = 2;
+// oneshot: grid = ceil(nvec / (kK1Threads * kK1Unroll)) CTAs, one block of
+// vectors each (production); otherwise the persistent grid-stride form (A/B)
+void launch_k1(const K1Args& a, bool track, int unroll, bool oneshot, unsigned grid,
+               cudaStream_t st);
+// K2 variants (MA_K2_VARIANT, A/B record in DESIGN.md): persistent grid-stride
+// 0 thread-contiguous VEC=8, 1 thread-contiguous VEC=4, 2 warp-contiguous
+// U=2, 3 U=1 + prefetch, 4 U=2 + prefetch, 5 U=4, 6/9 forced occupancy,
+// 7/8 load cache hints, 10/11 TMA bulk-copy ring, 12 approximate-math probe;
+// one tile per CTA: 13 U=2, **14 U=4 (production)**, 15 U=1.  Dtype pairs other
+// than (bf16, bf16) only carry kK2DefaultVariant.
+constexpr int kK2DefaultVariant = 14;
 int k2_effective_variant(int gk, int wk, int variant);
 void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream);
 // one tile per CTA: grid = total_tiles + trailing CTAs for the scalar remainder
