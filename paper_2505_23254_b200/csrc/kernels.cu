@@ -558,7 +558,7 @@ __device__ __forceinline__ uint32_t seg_of_tile(const SegTable& tab, uint64_t t)
     return lo;
 }
 
-template <int GK, int WK, int U>
+template <int GK, int WK, int U, bool PROBE = false>
 __global__ void __launch_bounds__(kK2Threads) k2_oneshot(SegTable tab, AdamArgs a) {
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_oneshot(SegTable tab, AdamArgs 
         const Seg& sg = tab.seg[seg_of_tile(tab, t)];
         Slot4 cur[U];
         load_tile<GK, U>(sg, t - sg.tile_begin, cur);
-        update_tile<GK, WK, U>(sg, t - sg.tile_begin, cur, c, sc);
+        update_tile<GK, WK, U, PROBE>(sg, t - sg.tile_begin, cur, c, sc);
         return;
     }
     // trailing CTAs: unaligned heads/tails and non-co-alignable sub-groups
@@ -1010,6 +1010,8 @@ template <int GK, int WK> struct K2Kernel<GK, WK, 12> { static constexpr auto fn
 template <int GK, int WK> struct K2Kernel<GK, WK, 13> { static constexpr auto fn = k2_oneshot<GK, WK, 2>; };
 template <int GK, int WK> struct K2Kernel<GK, WK, 14> { static constexpr auto fn = k2_oneshot<GK, WK, 4>; };
 template <int GK, int WK> struct K2Kernel<GK, WK, 15> { static constexpr auto fn = k2_oneshot<GK, WK, 1>; };
+// 16: PROBE ONLY — variant 14 with approximate div/sqrt (power/instruction headroom)
+template <int GK, int WK> struct K2Kernel<GK, WK, 16> { static constexpr auto fn = k2_oneshot<GK, WK, 4, true>; };
 
 template <int GK, int WK, int V>
 int k2_occupancy() {
@@ -1039,6 +1041,7 @@ void k2_variants(int variant, F&& f) {
             case 13: f(std::integral_constant<int, 13>{}); return;
             case 14: f(std::integral_constant<int, 14>{}); return;
             case 15: f(std::integral_constant<int, 15>{}); return;
+            case 16: f(std::integral_constant<int, 16>{}); return;
             default: break;
         }
     }
@@ -1101,9 +1104,9 @@ void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
         *stream = true;
         return;
     }
-    if (variant >= 13 && variant <= 15) {
+    if (variant >= 13 && variant <= 16) {
         *vec = 4;
-        *tile_vectors = (variant == 13 ? 2 : variant == 14 ? 4 : 1) * kK2Threads;
+        *tile_vectors = (variant == 13 ? 2 : variant == 15 ? 1 : 4) * kK2Threads;
         *stream = true;
         return;
     }
@@ -1117,7 +1120,7 @@ void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
     *stream = v >= 2;
 }
 
-bool k2_variant_oneshot(int variant) { return variant >= 13 && variant <= 15; }
+bool k2_variant_oneshot(int variant) { return variant >= 13 && variant <= 16; }
 
 int k2_blocks_per_sm(int gk, int wk, int variant) {
     if (variant == kTmaVariant) return tma_blocks_per_sm<128>();
