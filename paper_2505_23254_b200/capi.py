@@ -13,6 +13,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libmemascend_b200.so")
+if os.environ.get("MA_LIB_PATH"):  # A/B builds of the same C ABI (tools/, never by default)
+    LIB_PATH = os.environ["MA_LIB_PATH"]
 
 # status codes: 1 + memascend::ErrorCode (proj/include/memascend/error.hpp:9-27)
 ERROR_NAMES = {
