@@ -122,6 +122,8 @@ def lib():
                 "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
         L = C.CDLL(LIB_PATH)
         for name, res, args in SIGNATURES:
+            if os.environ.get("MA_LIB_PATH") and not hasattr(L, name):
+                continue  # an older A/B build may predate a symbol
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
