@@ -270,12 +270,6 @@ MA_API int ma_debug_cast_sweep(int kind, int block_log2, uint64_t* out_host);
 /* Number of 32-bit (kind F32) or 16-bit patterns where K1's predicate
  * disagrees with !isfinite(); exhaustive. */
 MA_API int ma_debug_mask_sweep(int kind, uint64_t* mismatches);
-/* Dividends where K2's hoisted-reciprocal division by a per-step constant
- * differs from IEEE __fdiv_rn, summed over `count` divisors; full = 1 sweeps
- * all 2^32 dividends, full = 0 all signs/mantissas at the fast path's edge
- * exponents and at 1.0. */
-MA_API int ma_debug_div_sweep(const float* divisors, uint32_t count, int full,
-                              uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -379,10 +379,3 @@ def debug_mask_sweep(kind: str) -> int:
     mm = C.c_uint64()
     check(capi.lib().ma_debug_mask_sweep(capi.DTYPES[kind], C.byref(mm)))
     return mm.value
-
-
-def debug_div_sweep(divisors, full: bool = False) -> int:
-    d = np.ascontiguousarray(divisors, dtype=np.float32)
-    mm = C.c_uint64()
-    check(capi.lib().ma_debug_div_sweep(d.ctypes.data, d.size, int(full), C.byref(mm)))
-    return mm.value

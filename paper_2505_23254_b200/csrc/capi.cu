@@ -1109,29 +1109,6 @@ int ma_debug_cast_sweep(int kind, int block_log2, uint64_t* out_host) {
     });
 }
 
-int ma_debug_div_sweep(const float* divisors, uint32_t count, int full, uint64_t* mismatches) {
-    return guarded([&] {
-        if (!divisors || !mismatches || count == 0) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
-        const DeviceInfo dv = device_info();
-        float* dd = nullptr;
-        unsigned long long* dm = nullptr;
-        CK(cudaMalloc(&dd, count * sizeof(float)));
-        cudaError_t e = cudaMalloc(&dm, 8);
-        if (e == cudaSuccess) e = cudaMemcpy(dd, divisors, count * sizeof(float), cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemset(dm, 0, 8);
-        if (e == cudaSuccess) {
-            ma::launch_div_sweep(dd, count, full, dm, static_cast<unsigned>(dv.sms * 8));
-            e = cudaGetLastError();
-        }
-        unsigned long long h = 0;
-        if (e == cudaSuccess) e = cudaMemcpy(&h, dm, 8, cudaMemcpyDeviceToHost);
-        cudaFree(dd);
-        cudaFree(dm);
-        CK(e);
-        *mismatches = h;
-    });
-}
-
 int ma_debug_mask_sweep(int kind, uint64_t* mismatches) {
     return guarded([&] {
         check_grad_dtype(kind);

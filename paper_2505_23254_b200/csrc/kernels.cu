@@ -242,11 +242,6 @@ __device__ __forceinline__ bool resolve_step(const AdamArgs& a, StepScalars& s) 
         s.bc2 = a.bc2;
     }
     s.scale_pow2 = exact_reciprocal(s.scale, &s.inv_scale);
-    // the hoisted-reciprocal division is used only for divisors in
-    // [2^-20, 1] (bias corrections of betas in [0, 0.99999]); otherwise
-    // r = 0 routes every element through __fdiv_rn
-    s.rbc1 = (s.bc1 >= 0x1p-20f && s.bc1 <= 1.0f) ? refined_reciprocal(s.bc1) : 0.0f;
-    s.rbc2 = (s.bc2 >= 0x1p-20f && s.bc2 <= 1.0f) ? refined_reciprocal(s.bc2) : 0.0f;
     return true;
 }
 
@@ -942,41 +937,6 @@ __global__ void k_cast_sweep(int log2, uint64_t* out, uint64_t nblocks) {
         h = (h ^ (r >> 8)) * 1099511628211ull;
     }
     out[b] = h;
-}
-
-// div_uniform (hoisted reciprocal) vs __fdiv_rn, bit for bit.  full = 1:
-// all 2^32 dividends; full = 0: every sign/mantissa at the guard's edge
-// exponents and at 1.0 (the fast path is scale-invariant inside its range).
-__global__ void k_div_sweep(const float* divs, uint32_t ndiv, int full,
-                            unsigned long long* mismatches) {
-    const uint64_t total = full ? (1ull << 32) : 3ull * (1ull << 24);
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    unsigned long long bad = 0;
-    for (uint32_t d = 0; d < ndiv; ++d) {
-        const float b = divs[d];
-        const float r = refined_reciprocal(b);
-        for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-             i += stride) {
-            uint32_t bits;
-            if (full) {
-                bits = static_cast<uint32_t>(i);
-            } else {
-                const uint32_t exps[3] = {27u, 127u, 227u};
-                const uint32_t sm = static_cast<uint32_t>(i & 0xFFFFFFu);  // sign + mantissa
-                bits = ((sm >> 23) << 31) | (exps[i >> 24] << 23) | (sm & 0x7FFFFFu);
-            }
-            const float a = __uint_as_float(bits);
-            const uint32_t x = __float_as_uint(div_uniform(a, b, r));
-            const uint32_t y = __float_as_uint(__fdiv_rn(a, b));
-            bad += (x != y);
-        }
-    }
-    if (bad) atomicAdd(mismatches, bad);
-}
-
-void launch_div_sweep(const float* divs, uint32_t ndiv, int full, unsigned long long* mismatches,
-                      unsigned grid) {
-    k_div_sweep<<<grid, 256>>>(divs, ndiv, full, mismatches);
 }
 
 // K1's word test applied to every pattern vs the IEEE classification.

@@ -509,24 +509,3 @@ def test_cfg2_full_size_sampled_parity():
     assert (host_bits16(w[it]) == smp["w"]).all()
     del p, m, v, w, st
     torch.cuda.empty_cache()
-
-
-def _bias_divisors(ts):
-    out = []
-    for t in ts:
-        b1, b2 = ora.step_scalars(t)
-        out += [b1, b2]
-    return np.array(out, np.float32)
-
-
-def test_hoisted_division_exhaustive_for_two_steps():
-    """K2 divides by the per-step constants bc1/bc2 with a hoisted reciprocal
-    (div_uniform): identical to IEEE division for all 2^32 dividends."""
-    assert mab.api.debug_div_sweep(_bias_divisors([1, 100]), full=True) == 0
-
-
-def test_hoisted_division_all_mantissas_many_steps():
-    """...and for every sign/mantissa at the fast path's edge exponents for
-    the bias corrections of t = 1..256 and t = 2^k up to 2^20."""
-    ts = list(range(1, 257)) + [1 << k for k in range(9, 21)] + [4095, 4097, 99999]
-    assert mab.api.debug_div_sweep(_bias_divisors(ts), full=False) == 0
