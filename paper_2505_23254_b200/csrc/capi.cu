@@ -264,6 +264,21 @@ ma::Seg plan_seg(const ma_subgroup& g, int gdt, int wdt, int vec, int tile_vecto
     return s;
 }
 
+// One CTA per tile, then trailing CTAs for heads/tails and unaligned
+// sub-groups (at least one whenever any remainder exists).
+uint64_t oneshot_grid(const ma::SegTable& tab, int vec, uint64_t scalar_elems, uint64_t cap) {
+    bool remainder = scalar_elems > 0;
+    for (uint32_t k = 0; k < tab.count && !remainder; ++k) {
+        const ma::Seg& sg = tab.seg[k];
+        remainder = sg.head > 0 || sg.head + sg.nvec * vec != sg.n;
+    }
+    const uint64_t trailing =
+        remainder ? std::max<uint64_t>(1, std::min<uint64_t>(cap, (scalar_elems + 255) / 256)) : 0;
+    const uint64_t grid = std::max<uint64_t>(1, tab.total_tiles + trailing);
+    if (grid > 0x7FFFFFFFull) fail(MA_ERR_INVALID_ARGUMENT, "sub-group table too large for one launch");
+    return grid;
+}
+
 void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, const ma::AdamArgs& a,
                cudaStream_t st) {
     const DeviceInfo d = device_info();
@@ -293,18 +308,7 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
         tab.total_tiles = tiles;
         uint64_t grid;
         if (ma::k2_variant_oneshot(variant)) {
-            // one CTA per tile, then trailing CTAs for heads/tails and
-            // unaligned sub-groups (at least one whenever any remainder exists)
-            bool remainder = scalar_elems > 0;
-            for (uint32_t k = 0; k < tab.count && !remainder; ++k) {
-                const ma::Seg& sg = tab.seg[k];
-                remainder = sg.head > 0 || sg.head + sg.nvec * vec != sg.n;
-            }
-            const uint64_t trailing =
-                remainder ? std::max<uint64_t>(1, std::min<uint64_t>(cap, (scalar_elems + 255) / 256))
-                          : 0;
-            grid = std::max<uint64_t>(1, tiles + trailing);
-            if (grid > 0x7FFFFFFFull) fail(MA_ERR_INVALID_ARGUMENT, "sub-group table too large for one launch");
+            grid = oneshot_grid(tab, vec, scalar_elems, cap);
         } else {
             grid = std::min<uint64_t>(tiles, cap);
             if (stream && scalar_elems > 0) {
@@ -321,7 +325,7 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
 void launch_k3(const ma_subgroup* groups, uint32_t count, int gdt, const ma::AdamArgs& a,
                cudaStream_t st) {
     const DeviceInfo d = device_info();
-    constexpr int kVec = 4, kTile = 2 * ma::kK2Threads;
+    constexpr int kVec = 4, kTile = ma::kK3Slots * ma::kK2Threads;
     const uint64_t cap = static_cast<uint64_t>(d.sms) * ma::k3_blocks_per_sm(gdt);
     for (uint32_t first = 0; first < count; first += ma::kMaxSegs) {
         ma::SegTable tab{};
@@ -339,9 +343,7 @@ void launch_k3(const ma_subgroup* groups, uint32_t count, int gdt, const ma::Ada
         }
         if (tab.count == 0) continue;
         tab.total_tiles = tiles;
-        uint64_t grid = std::min<uint64_t>(tiles, cap);
-        if (scalar_elems > 0) grid = std::max<uint64_t>(grid, std::min<uint64_t>(cap, (scalar_elems + 255) / 256));
-        grid = std::max<uint64_t>(grid, 1);
+        const uint64_t grid = oneshot_grid(tab, kVec, scalar_elems, cap);
         ma::launch_k3(gdt, tab, a, static_cast<unsigned>(grid), st);
         CK(cudaGetLastError());
     }

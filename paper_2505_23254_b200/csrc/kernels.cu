@@ -792,31 +792,34 @@ __global__ void __launch_bounds__(kK2Threads) k3_adam_bf16(SegTable tab, AdamArg
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
     const AdamConsts c = a.c;
-    constexpr int U = 2;
-    uint32_t si = 0;
-    for (uint64_t t = blockIdx.x; t < tab.total_tiles; t += gridDim.x) {
-        while (t >= tab.seg[si].tile_end) ++si;
-        const Seg& sg = tab.seg[si];
+    constexpr int U = kK3Slots;
+    // one tile per CTA (same one-shot grid as K2), then trailing CTAs
+    const uint64_t t = blockIdx.x;
+    if (t < tab.total_tiles) {
+        const Seg& sg = tab.seg[seg_of_tile(tab, t)];
         const uint64_t lt = t - sg.tile_begin;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t j = lt * (U * kK2Threads) + u * kK2Threads + threadIdx.x;
             if (j < sg.nvec) bf16_state_slot<GK>(sg, sg.head + 4 * j, c, sc);
         }
+        return;
     }
-    const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    const uint64_t gsize = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t q0 = t - tab.total_tiles;
+    const uint64_t nq = gridDim.x - tab.total_tiles;
     for (uint32_t k = 0; k < tab.count; ++k) {
         const Seg& sg = tab.seg[k];
         if (sg.vector_ok) {
-            if (blockIdx.x != k % gridDim.x) continue;
+            if (q0 != k % nq) continue;
             const uint64_t tail_begin = sg.head + sg.nvec * 4;
             const uint64_t extra = sg.head + (sg.n - tail_begin);
             for (uint64_t q = threadIdx.x; q < extra; q += blockDim.x) {
                 bf16_state_scalar<GK>(sg, q < sg.head ? q : tail_begin + (q - sg.head), c, sc);
             }
         } else {
-            for (uint64_t e = gtid; e < sg.n; e += gsize) bf16_state_scalar<GK>(sg, e, c, sc);
+            for (uint64_t e = q0 * blockDim.x + threadIdx.x; e < sg.n; e += nq * blockDim.x) {
+                bf16_state_scalar<GK>(sg, e, c, sc);
+            }
         }
     }
 }

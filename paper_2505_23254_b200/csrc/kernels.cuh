@@ -95,7 +95,9 @@ bool k2_variant_oneshot(int variant);
 int k2_blocks_per_sm(int gk, int wk, int variant);
 void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st);
-// K3 (bf16 state): Seg p/m/v point at uint16 arrays; 2 slots of 4 elements.
+// K3 (bf16 state): Seg p/m/v point at uint16 arrays; one tile of
+// kK3Slots x 256 slots of 4 elements per CTA, trailing CTAs for remainders.
+constexpr int kK3Slots = 2;
 int k3_blocks_per_sm(int gk);
 void launch_k3(int gk, const SegTable& tab, const AdamArgs& a, unsigned grid, cudaStream_t st);
 void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s);
