@@ -199,6 +199,36 @@ MA_API int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n,
  * way: the gradients are read once per step instead of twice. */
 MA_API int ma_stepper_ingest_async(ma_stepper* s, const void* src, int src_dtype, void* dst,
                                    uint64_t n, void* stream);
+/* Reduce-scatter epilogue form of the producer-side check (SURVEY §8(f)
+ * row 2, "the NCCL reduce-scatter epilogue"; K4): dst[i] = post_scale *
+ * (srcs[0][i] + srcs[1][i] + ... ) summed in fp32 in source order, NaN stored
+ * as the canonical quiet NaN, written in the stepper's gradient kind, with
+ * the overflow test of overflow.hpp:46-51 applied to the stored values (sets
+ * the step's flag).  srcs are any device-loadable pointers (local buffers or
+ * peer memory); the caller orders their production before this call. */
+MA_API int ma_stepper_reduce_check_async(ma_stepper* s, const void* const* srcs, int nsrc,
+                                         int src_dtype, uint64_t n, float post_scale, void* dst,
+                                         void* stream);
+/* Multi-process form over NVLink peer memory.  Every rank shares its
+ * full-length gradient buffer (n_total elements of dtype) once: ma_rs_create
+ * returns a MA_RS_HANDLE_BYTES record, the records of all ranks are gathered
+ * in rank order (any host channel) and passed to ma_rs_open.  Per step,
+ * ma_stepper_reduce_scatter_async reduces elements [base, base+n) of all
+ * ranks' buffers into dst: a one-warp entry barrier (all ranks' gradients are
+ * complete), then K4 reading every peer over NVLink, whose last CTA is the
+ * exit barrier (nobody overwrites gradients still being read) and the OR of
+ * all ranks' flags — the stepper's flag is the global skip decision when the
+ * call completes, with no separate collective.  A peer missing for ~2^35
+ * cycles forces a skip and sets the error reported by ma_rs_error. */
+typedef struct ma_rs ma_rs;
+#define MA_RS_HANDLE_BYTES 192
+MA_API int ma_rs_create(int world, int rank, const void* grads, uint64_t n_total, int dtype,
+                        ma_rs** out, void* handle_out);
+MA_API int ma_rs_open(ma_rs* r, const void* all_handles);
+MA_API int ma_rs_error(ma_rs* r, int* timed_out);
+MA_API int ma_rs_destroy(ma_rs* r);
+MA_API int ma_stepper_reduce_scatter_async(ma_stepper* s, ma_rs* r, uint64_t base, uint64_t n,
+                                           float post_scale, void* dst, void* stream);
 /* Device uint32 holding this step's overflow flag (for the cross-rank OR). */
 MA_API uint32_t* ma_stepper_flag(ma_stepper* s);
 /* Device float holding the current loss scale (gradient producers read it). */

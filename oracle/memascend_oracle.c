@@ -573,3 +573,33 @@ void ora_fill_grads(void* g, float* g32, const uint16_t* w, uint64_t n, uint64_t
     j.scale = scale; j.g_kind = g_kind; j.w_kind = w_kind;
     run_fill(j, n, threads);
 }
+
+/* ------------------------------------------------------------------ */
+/* Gradient reduce-scatter with the overflow check in its epilogue (SURVEY
+ * §8(f) row 2).  No reference counterpart exists for the sum (the reference
+ * is single-process); its output feeds the reference's flat gradient buffer
+ * (simulator.cpp:401-405) and the check is overflow.hpp:46-51 applied to the
+ * STORED values.  Defined order: acc = src[0][i], acc += src[r][i] for
+ * r = 1.. in rank order (fp32, one rounding each), then acc *= post_scale
+ * when post_scale != 1; a NaN result is stored as the canonical quiet NaN
+ * (0x7FC00000 before narrowing) so the bits do not depend on which NaN the
+ * hardware propagates. */
+int ora_reduce_check(const void* const* srcs, int nsrc, int src_kind, uint64_t n,
+                     float post_scale, int dst_kind, void* dst) {
+    int any = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        float acc = load_grad(srcs[0], src_kind, i);
+        for (int r = 1; r < nsrc; ++r) acc = acc + load_grad(srcs[r], src_kind, i);
+        if (post_scale != 1.0f) acc = acc * post_scale;
+        if (acc != acc) acc = u2f(0x7FC00000u);
+        if (dst_kind == ORA_F32) {
+            ((float*)dst)[i] = acc;
+            any |= ora_bits_non_finite_f32(f2u(acc));
+        } else {
+            const uint16_t h = narrow(acc, dst_kind);
+            ((uint16_t*)dst)[i] = h;
+            any |= dst_kind == ORA_BF16 ? ora_bits_non_finite_bf16(h) : ora_bits_non_finite_f16(h);
+        }
+    }
+    return any;
+}

@@ -56,6 +56,12 @@ int ora_bits_non_finite_f16(uint16_t bits);
  * UINT64_MAX), matching track_first_index with early_exit=false. */
 int ora_overflow_check(const void* data, uint64_t n, int kind, uint64_t* first_index);
 
+/* Reduce-scatter epilogue form of the check: dst[i] =
+ * post_scale * (src[0][i] + src[1][i] + ...) in fp32, rank order, NaN stored
+ * canonical; returns 1 when any stored value is non-finite. */
+int ora_reduce_check(const void* const* srcs, int nsrc, int src_kind, uint64_t n,
+                     float post_scale, int dst_kind, void* dst);
+
 /* ---- Adam (proj/include/memascend/optimizer.hpp, proj/src/optimizer.cpp) */
 typedef struct {
     float lr, beta1, beta2, eps, weight_decay; /* AdamHyper, optimizer.hpp:9-15 */

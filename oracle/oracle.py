@@ -117,6 +117,9 @@ def lib():
         L.ora_mt64_next.restype = C.c_uint64
         L.ora_mt64_next.argtypes = [C.POINTER(MT64)]
         L.ora_adversarial_buffer.argtypes = [C.POINTER(MT64), C.c_void_p, C.c_uint64, C.c_int]
+        L.ora_reduce_check.restype = C.c_int
+        L.ora_reduce_check.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_float,
+                                       C.c_int, C.c_void_p]
         _lib = L
     return _lib
 
@@ -182,6 +185,20 @@ def adam_step_bf16(p16, m16, v16, g, t, h: Hyper, loss_scale):
                                  C.byref(h), loss_scale)
     if r:
         raise ValueError("invalid_argument: adam step count t must be >= 1")
+
+
+def reduce_check(srcs, src_kind: str, post_scale: float = 1.0, dst_kind: str = "bf16"):
+    """ora_reduce_check: rank-ordered fp32 sum of `srcs` (bit arrays: uint16
+    for bf16/f16, float32 for f32) times post_scale, stored as dst_kind.
+    Returns (dst, overflow)."""
+    srcs = [np.ascontiguousarray(s) for s in srcs]
+    n = srcs[0].size
+    assert all(s.size == n for s in srcs)
+    ptrs = (C.c_void_p * len(srcs))(*[s.ctypes.data for s in srcs])
+    dst = np.empty(n, dtype=np.float32 if dst_kind == "f32" else np.uint16)
+    flag = lib().ora_reduce_check(ptrs, len(srcs), KIND[src_kind], n, post_scale,
+                                  KIND[dst_kind], dst.ctypes.data)
+    return dst, bool(flag)
 
 
 def pseudo_gradient(seed, step, index, weight):

@@ -192,6 +192,28 @@ class Stepper:
         check(capi.lib().ma_stepper_ingest_async(self._h, sp, sdt, dst.data_ptr(), n,
                                                  _stream_ptr(stream)))
 
+    def reduce_check(self, srcs, dst, post_scale=1.0, src_kind=None, stream=None):
+        """K4: dst = post_scale * (srcs[0] + srcs[1] + ...) (fp32, list order) in
+        the stepper's gradient kind, overflow-checked in the same pass."""
+        infos = [_info(x, src_kind) for x in srcs]
+        n, sdt = infos[0][1], infos[0][2]
+        if any(i[1] != n or i[2] != sdt for i in infos) or dst.numel() != n:
+            raise MemAscendError(1, "sources and destination must agree in length and kind")
+        ptrs = (C.c_void_p * len(infos))(*[i[0] for i in infos])
+        check(capi.lib().ma_stepper_reduce_check_async(self._h, ptrs, len(infos), sdt, n,
+                                                       post_scale, dst.data_ptr(),
+                                                       _stream_ptr(stream)))
+
+    def reduce_scatter(self, rs: "GradReduceScatter", base, n, dst, post_scale=1.0, stream=None):
+        """K4 over NVLink peer memory: elements [base, base+n) of every rank's
+        shared gradient buffer, summed in rank order into dst; on completion
+        the stepper's flag is the OR over all ranks (no all-reduce needed)."""
+        if n and dst.numel() < n:
+            raise MemAscendError(1, "destination shorter than the partition")
+        check(capi.lib().ma_stepper_reduce_scatter_async(
+            self._h, rs._h, base, n, post_scale, dst.data_ptr() if n else None,
+            _stream_ptr(stream)))
+
     def check_from_host(self, host_g, dev_g, chunk_elems=64 << 20, stream=None,
                         copy_stream=None):
         """H2D of pinned host gradients into dev_g, K1 overlapped per chunk."""
@@ -294,6 +316,40 @@ class FlagExchange:
     def close(self):
         if self._h:
             capi.lib().ma_xchg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GradReduceScatter:
+    """Shares this rank's full-length gradient buffer with every peer (ma_rs_*)
+    for Stepper.reduce_scatter.  `all_gather(record: bytes) -> list[bytes]`
+    returns every rank's record in rank order; it runs once."""
+
+    def __init__(self, world: int, rank: int, grads, all_gather, kind=None):
+        gp, n, dt = _info(grads, kind)
+        h = C.c_void_p()
+        buf = (C.c_ubyte * capi.RS_HANDLE_BYTES)()
+        check(capi.lib().ma_rs_create(world, rank, gp, n, dt, C.byref(h), buf))
+        self._h = h
+        self.grads = grads
+        recs = all_gather(bytes(buf))
+        assert len(recs) == world and all(len(x) == capi.RS_HANDLE_BYTES for x in recs)
+        joined = (C.c_ubyte * (capi.RS_HANDLE_BYTES * world)).from_buffer_copy(b"".join(recs))
+        check(capi.lib().ma_rs_open(self._h, joined))
+
+    def timed_out(self) -> bool:
+        e = C.c_int()
+        check(capi.lib().ma_rs_error(self._h, C.byref(e)))
+        return bool(e.value)
+
+    def close(self):
+        if self._h:
+            capi.lib().ma_rs_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -28,6 +28,7 @@ ERROR_NAMES = {
 DT_F32, DT_BF16, DT_F16, DT_NONE = 0, 1, 2, 3
 STEPPER_STATE_BYTES = 64
 IPC_HANDLE_BYTES = 64
+RS_HANDLE_BYTES = 192
 DTYPES = {"f32": DT_F32, "bf16": DT_BF16, "f16": DT_F16, "none": DT_NONE}
 
 
@@ -89,6 +90,12 @@ SIGNATURES = [
     ("ma_xchg_destroy", _I, [_VP]),
     ("ma_stepper_check_xchg_async", _I, [_VP, _VP, _U64, _VP, _VP]),
     ("ma_stepper_ingest_async", _I, [_VP, _VP, _I, _VP, _U64, _VP]),
+    ("ma_stepper_reduce_check_async", _I, [_VP, _VP, _I, _I, _U64, _F, _VP, _VP]),
+    ("ma_rs_create", _I, [_I, _I, _VP, _U64, _I, C.POINTER(_VP), _VP]),
+    ("ma_rs_open", _I, [_VP, _VP]),
+    ("ma_rs_error", _I, [_VP, C.POINTER(_I)]),
+    ("ma_rs_destroy", _I, [_VP]),
+    ("ma_stepper_reduce_scatter_async", _I, [_VP, _VP, _U64, _U64, _F, _VP, _VP]),
     ("ma_stepper_flag", _VP, [_VP]),
     ("ma_stepper_scale", _VP, [_VP]),
     ("ma_stepper_apply_async", _I, [_VP, C.POINTER(Subgroup), _U32, _VP]),

@@ -4,6 +4,7 @@
 // pageable host), the staging path for pageable spans, and the device-
 // resident step driver.  Every entry point converts failures to a status
 // code plus a thread-local message; nothing here falls back to the CPU.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -744,87 +745,105 @@ struct ma_xchg {
     bool ready = false;
 };
 
+namespace {
+
+ma_xchg* xchg_new(int world, int rank, void* ipc_handle_out) {
+    if (world < 1 || world > ma::kMaxRanks || rank < 0 || rank >= world)
+        fail(MA_ERR_INVALID_ARGUMENT, "bad world/rank for the peer exchange");
+    static_assert(sizeof(cudaIpcMemHandle_t) <= MA_IPC_HANDLE_BYTES, "ipc handle size");
+    device_info();
+    auto* x = new ma_xchg();
+    try {
+        x->world = world;
+        x->rank = rank;
+        CK(cudaMalloc(&x->slots, 2 * static_cast<size_t>(world) * sizeof(unsigned long long)));
+        CK(cudaMemset(x->slots, 0, 2 * static_cast<size_t>(world) * sizeof(unsigned long long)));
+        CK(cudaMalloc(&x->local, 2 * sizeof(unsigned int)));
+        CK(cudaMemset(x->local, 0, 2 * sizeof(unsigned int)));
+        CK(cudaMalloc(&x->d_desc, sizeof(ma::XchgDev)));
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, x->slots));
+        std::memset(ipc_handle_out, 0, MA_IPC_HANDLE_BYTES);
+        std::memcpy(ipc_handle_out, &h, sizeof h);
+        CK(cudaDeviceSynchronize());  // zeroed slots before any peer can write them
+    } catch (...) {
+        if (x->slots) cudaFree(x->slots);
+        if (x->local) cudaFree(x->local);
+        if (x->d_desc) cudaFree(x->d_desc);
+        delete x;
+        throw;
+    }
+    return x;
+}
+
+// all_handles: world records of `stride` bytes, the slot handle first in each
+void xchg_open_impl(ma_xchg* x, const void* all_handles, size_t stride) {
+    if (x->ready) fail(MA_ERR_LIFECYCLE, "peer exchange already opened");
+    ma::XchgDev desc{};
+    desc.world = static_cast<uint32_t>(x->world);
+    desc.rank = static_cast<uint32_t>(x->rank);
+    desc.my_slots = x->slots;
+    desc.counter = x->local;
+    desc.error = x->local + 1;
+    for (int r = 0; r < x->world; ++r) {
+        if (r == x->rank) {
+            desc.peer_slots[r] = x->slots;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const unsigned char*>(all_handles) + r * stride, sizeof h);
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        x->opened.push_back(p);
+        desc.peer_slots[r] = static_cast<unsigned long long*>(p);
+    }
+    CK(cudaMemcpy(x->d_desc, &desc, sizeof desc, cudaMemcpyHostToDevice));
+    x->ready = true;
+}
+
+void xchg_free(ma_xchg* x) {
+    if (!x) return;
+    cudaDeviceSynchronize();
+    for (void* p : x->opened) cudaIpcCloseMemHandle(p);
+    cudaFree(x->slots);
+    cudaFree(x->local);
+    cudaFree(x->d_desc);
+    delete x;
+}
+
+bool xchg_timed_out(const ma_xchg* x) {
+    unsigned int e = 0;
+    CK(cudaMemcpy(&e, x->local + 1, sizeof e, cudaMemcpyDeviceToHost));
+    return e != 0;
+}
+
+}  // namespace
+
 extern "C" {
 
 int ma_xchg_create(int world, int rank, ma_xchg** out, void* ipc_handle_out) {
     return guarded([&] {
         if (!out || !ipc_handle_out) fail(MA_ERR_INVALID_ARGUMENT, "null output");
-        if (world < 1 || world > ma::kMaxRanks || rank < 0 || rank >= world)
-            fail(MA_ERR_INVALID_ARGUMENT, "bad world/rank for the peer exchange");
-        static_assert(sizeof(cudaIpcMemHandle_t) <= MA_IPC_HANDLE_BYTES, "ipc handle size");
-        device_info();
-        auto* x = new ma_xchg();
-        try {
-            x->world = world;
-            x->rank = rank;
-            CK(cudaMalloc(&x->slots, 2 * static_cast<size_t>(world) * sizeof(unsigned long long)));
-            CK(cudaMemset(x->slots, 0, 2 * static_cast<size_t>(world) * sizeof(unsigned long long)));
-            CK(cudaMalloc(&x->local, 2 * sizeof(unsigned int)));
-            CK(cudaMemset(x->local, 0, 2 * sizeof(unsigned int)));
-            CK(cudaMalloc(&x->d_desc, sizeof(ma::XchgDev)));
-            cudaIpcMemHandle_t h;
-            CK(cudaIpcGetMemHandle(&h, x->slots));
-            std::memset(ipc_handle_out, 0, MA_IPC_HANDLE_BYTES);
-            std::memcpy(ipc_handle_out, &h, sizeof h);
-            CK(cudaDeviceSynchronize());  // zeroed slots before any peer can write them
-        } catch (...) {
-            if (x->slots) cudaFree(x->slots);
-            if (x->local) cudaFree(x->local);
-            if (x->d_desc) cudaFree(x->d_desc);
-            delete x;
-            throw;
-        }
-        *out = x;
+        *out = xchg_new(world, rank, ipc_handle_out);
     });
 }
 
 int ma_xchg_open(ma_xchg* x, const void* all_handles) {
     return guarded([&] {
         if (!x || !all_handles) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
-        if (x->ready) fail(MA_ERR_LIFECYCLE, "peer exchange already opened");
-        ma::XchgDev desc{};
-        desc.world = static_cast<uint32_t>(x->world);
-        desc.rank = static_cast<uint32_t>(x->rank);
-        desc.my_slots = x->slots;
-        desc.counter = x->local;
-        desc.error = x->local + 1;
-        for (int r = 0; r < x->world; ++r) {
-            if (r == x->rank) {
-                desc.peer_slots[r] = x->slots;
-                continue;
-            }
-            cudaIpcMemHandle_t h;
-            std::memcpy(&h, static_cast<const unsigned char*>(all_handles) + r * MA_IPC_HANDLE_BYTES,
-                        sizeof h);
-            void* p = nullptr;
-            CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-            x->opened.push_back(p);
-            desc.peer_slots[r] = static_cast<unsigned long long*>(p);
-        }
-        CK(cudaMemcpy(x->d_desc, &desc, sizeof desc, cudaMemcpyHostToDevice));
-        x->ready = true;
+        xchg_open_impl(x, all_handles, MA_IPC_HANDLE_BYTES);
     });
 }
 
 int ma_xchg_error(ma_xchg* x, int* timed_out) {
     return guarded([&] {
         if (!x || !timed_out) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
-        unsigned int e = 0;
-        CK(cudaMemcpy(&e, x->local + 1, sizeof e, cudaMemcpyDeviceToHost));
-        *timed_out = e ? 1 : 0;
+        *timed_out = xchg_timed_out(x) ? 1 : 0;
     });
 }
 
 int ma_xchg_destroy(ma_xchg* x) {
-    return guarded([&] {
-        if (!x) return;
-        cudaDeviceSynchronize();
-        for (void* p : x->opened) cudaIpcCloseMemHandle(p);
-        cudaFree(x->slots);
-        cudaFree(x->local);
-        cudaFree(x->d_desc);
-        delete x;
-    });
+    return guarded([&] { xchg_free(x); });
 }
 
 int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n, ma_xchg* x,
@@ -1126,6 +1145,224 @@ int ma_debug_mask_sweep(int kind, uint64_t* mismatches) {
         CK(e);
         CK(e2);
         *mismatches = h;
+    });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ reduce-scatter
+// K4 host side: the gradient reduce-scatter with the overflow check in its
+// epilogue.  ma_rs shares this rank's full gradient
+// buffer with every peer through CUDA IPC (the allocation handle plus the
+// offset of the buffer inside it) and owns an exchange slot set for the two
+// barriers of a step.
+struct ma_rs {
+    ma_xchg* x = nullptr;
+    int dtype = MA_DT_BF16;
+    uint64_t n_total = 0;
+    std::vector<const void*> grads;  // [world]: this rank's buffer, peers' mappings
+    std::vector<void*> opened;
+    bool ready = false;
+};
+
+namespace {
+
+constexpr uint32_t kRsMagic = 0x4D415253u;  // "MARS"
+
+struct RsHandle {
+    unsigned char slots[MA_IPC_HANDLE_BYTES];
+    unsigned char grads[MA_IPC_HANDLE_BYTES];
+    uint64_t offset;
+    uint64_t n_total;
+    int32_t dtype, rank, world;
+    uint32_t magic;
+};
+static_assert(sizeof(RsHandle) <= MA_RS_HANDLE_BYTES, "reduce-scatter handle size");
+
+// Base of the device allocation holding p (IPC handles name allocations).
+const void* allocation_base(const void* p) {
+    using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static Fn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q{};
+        void* f = nullptr;
+        CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !f) fail(MA_ERR_CUDA, "cuMemGetAddressRange unavailable");
+        fn = reinterpret_cast<Fn>(f);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+        fail(MA_ERR_INVALID_ARGUMENT, "gradient buffer is not device memory");
+    return reinterpret_cast<const void*>(base);
+}
+
+uint32_t dtype_bytes(int dt) { return dt == MA_DT_F32 ? 4u : 2u; }
+
+void launch_reduce(ma_stepper* s, const void* const* srcs, int nsrc, int sdt, uint64_t n,
+                   float post_scale, void* dst, const ma::XchgDev* xd, unsigned long long epoch,
+                   cudaStream_t st) {
+    if (n == 0 && !xd) return;
+    const DeviceInfo d = device_info();
+    ma::RsArgs a{};
+    const uint32_t es = dtype_bytes(sdt), ed = dtype_bytes(s->g_dtype);
+    for (int r = 0; r < nsrc; ++r) a.src[r] = srcs[r];
+    a.nsrc = static_cast<uint32_t>(nsrc);
+    a.dst = dst;
+    a.n = n;
+    a.post_scale = post_scale;
+    a.flag = &s->d_st->flag;
+    a.xchg = xd;
+    a.epoch = epoch;
+    // co-align every source and dst on 16 bytes at the same element
+    for (uint64_t h = 0; n >= 8 && h < 8; ++h) {
+        bool ok = (reinterpret_cast<uintptr_t>(dst) + h * ed) % 16 == 0;
+        for (int r = 0; r < nsrc && ok; ++r)
+            ok = (reinterpret_cast<uintptr_t>(srcs[r]) + h * es) % 16 == 0;
+        if (ok) {
+            a.head = h;
+            a.nvec = (n - h) / 8;
+            break;
+        }
+    }
+    const uint64_t tile = static_cast<uint64_t>(ma::kRsUnits) * 256;
+    a.tiles = (a.nvec + tile - 1) / tile;
+    const uint64_t rem = n - a.nvec * 8;
+    const uint64_t cap = static_cast<uint64_t>(d.sms) * 8;
+    const uint64_t trailing = rem ? std::max<uint64_t>(1, std::min<uint64_t>(cap, (rem + 255) / 256)) : 0;
+    const uint64_t grid = std::max<uint64_t>(1, a.tiles + trailing);
+    if (grid > 0x7FFFFFFFull) fail(MA_ERR_INVALID_ARGUMENT, "partition too large for one launch");
+    ma::launch_reduce_check(sdt, s->g_dtype, a, static_cast<unsigned>(grid), st);
+    CK(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+int ma_stepper_reduce_check_async(ma_stepper* s, const void* const* srcs, int nsrc, int src_dtype,
+                                  uint64_t n, float post_scale, void* dst, void* stream) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        check_grad_dtype(src_dtype);
+        if (nsrc < 1 || nsrc > ma::kMaxRanks) fail(MA_ERR_INVALID_ARGUMENT, "nsrc out of range");
+        if (n == 0) return;
+        if (!srcs || !dst) fail(MA_ERR_INVALID_ARGUMENT, "null source list / destination");
+        for (int r = 0; r < nsrc; ++r)
+            if (!srcs[r]) fail(MA_ERR_INVALID_ARGUMENT, "null source pointer");
+        launch_reduce(s, srcs, nsrc, src_dtype, n, post_scale, dst, nullptr, 0, as_stream(stream));
+        s->last = as_stream(stream);
+    });
+}
+
+int ma_rs_create(int world, int rank, const void* grads, uint64_t n_total, int dtype, ma_rs** out,
+                 void* handle_out) {
+    return guarded([&] {
+        if (!out || !handle_out) fail(MA_ERR_INVALID_ARGUMENT, "null output");
+        check_grad_dtype(dtype);
+        if (!grads || n_total == 0) fail(MA_ERR_INVALID_ARGUMENT, "empty gradient buffer");
+        RsHandle h{};
+        ma_xchg* x = xchg_new(world, rank, h.slots);
+        auto* r = new ma_rs();
+        try {
+            r->x = x;
+            r->dtype = dtype;
+            r->n_total = n_total;
+            const void* base = allocation_base(grads);
+            cudaIpcMemHandle_t gh;
+            CK(cudaIpcGetMemHandle(&gh, const_cast<void*>(base)));
+            std::memcpy(h.grads, &gh, sizeof gh);
+            h.offset = static_cast<uint64_t>(static_cast<const uint8_t*>(grads) -
+                                             static_cast<const uint8_t*>(base));
+            h.n_total = n_total;
+            h.dtype = dtype;
+            h.rank = rank;
+            h.world = world;
+            h.magic = kRsMagic;
+            r->grads.assign(world, nullptr);
+            r->grads[rank] = grads;
+        } catch (...) {
+            xchg_free(x);
+            delete r;
+            throw;
+        }
+        std::memset(handle_out, 0, MA_RS_HANDLE_BYTES);
+        std::memcpy(handle_out, &h, sizeof h);
+        *out = r;
+    });
+}
+
+int ma_rs_open(ma_rs* r, const void* all_handles) {
+    return guarded([&] {
+        if (!r || !all_handles) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
+        if (r->ready) fail(MA_ERR_LIFECYCLE, "reduce-scatter already opened");
+        const int world = r->x->world;
+        const auto* blob = static_cast<const unsigned char*>(all_handles);
+        for (int k = 0; k < world; ++k) {
+            RsHandle h;
+            std::memcpy(&h, blob + static_cast<size_t>(k) * MA_RS_HANDLE_BYTES, sizeof h);
+            if (h.magic != kRsMagic || h.rank != k || h.world != world)
+                fail(MA_ERR_INVALID_ARGUMENT, "handle list is not in rank order / not ma_rs handles");
+            if (h.n_total != r->n_total || h.dtype != r->dtype)
+                fail(MA_ERR_INVALID_ARGUMENT, "ranks disagree on the gradient length or dtype");
+        }
+        for (int k = 0; k < world; ++k) {
+            if (k == r->x->rank) continue;
+            RsHandle h;
+            std::memcpy(&h, blob + static_cast<size_t>(k) * MA_RS_HANDLE_BYTES, sizeof h);
+            cudaIpcMemHandle_t gh;
+            std::memcpy(&gh, h.grads, sizeof gh);
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, gh, cudaIpcMemLazyEnablePeerAccess));
+            r->opened.push_back(p);
+            r->grads[k] = static_cast<const uint8_t*>(p) + h.offset;
+        }
+        xchg_open_impl(r->x, all_handles, MA_RS_HANDLE_BYTES);
+        r->ready = true;
+    });
+}
+
+int ma_rs_error(ma_rs* r, int* timed_out) {
+    return guarded([&] {
+        if (!r || !timed_out) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
+        *timed_out = xchg_timed_out(r->x) ? 1 : 0;
+    });
+}
+
+int ma_rs_destroy(ma_rs* r) {
+    return guarded([&] {
+        if (!r) return;
+        cudaDeviceSynchronize();
+        for (void* p : r->opened) cudaIpcCloseMemHandle(p);
+        xchg_free(r->x);
+        delete r;
+    });
+}
+
+int ma_stepper_reduce_scatter_async(ma_stepper* s, ma_rs* r, uint64_t base, uint64_t n,
+                                    float post_scale, void* dst, void* stream) {
+    return guarded([&] {
+        if (!s || !r) fail(MA_ERR_INVALID_ARGUMENT, "null stepper / reduce-scatter");
+        if (!r->ready) fail(MA_ERR_LIFECYCLE, "reduce-scatter not opened (ma_rs_open)");
+        if (base > r->n_total || n > r->n_total - base)
+            fail(MA_ERR_INVALID_ARGUMENT, "partition outside the gradient buffer");
+        if (n && !dst) fail(MA_ERR_INVALID_ARGUMENT, "null destination");
+        const cudaStream_t st = as_stream(stream);
+        const int world = r->x->world;
+        const uint32_t es = dtype_bytes(r->dtype);
+        std::vector<const void*> srcs(world);
+        for (int k = 0; k < world; ++k) srcs[k] = static_cast<const uint8_t*>(r->grads[k]) + base * es;
+        // entry: every rank's gradients are complete before anyone reads them
+        r->x->epoch += 1;
+        ma::launch_peer_barrier(r->x->d_desc, r->x->epoch, &s->d_st->flag, st);
+        CK(cudaGetLastError());
+        // K4, whose last CTA is the exit barrier (no rank overwrites its
+        // gradients while a peer still reads them) and the flag OR
+        r->x->epoch += 1;
+        alignas(16) static const uint32_t dummy[4] = {0, 0, 0, 0};  // never written (n == 0)
+        launch_reduce(s, srcs.data(), world, r->dtype, n, post_scale, n ? dst : const_cast<uint32_t*>(dummy),
+                      r->x->d_desc, r->x->epoch, st);
+        s->last = st;
     });
 }
 

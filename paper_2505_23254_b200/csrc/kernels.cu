@@ -39,20 +39,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 // and replaces the local flag by the OR — the all-reduce(max) of the skip
 // decision without a separate collective launch.  A peer that never arrives
 // within ~2^35 cycles raises `error` and forces a skip instead of hanging.
-__device__ void k1_exchange_epilogue(const K1Args& a, unsigned lane) {
-    __shared__ uint32_t is_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        is_last = atomicAdd(a.xchg->counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!is_last || threadIdx.x >= 32) return;
-    const XchgDev& x = *a.xchg;
-    __threadfence();
-    const uint32_t local = *reinterpret_cast<volatile uint32_t*>(a.flag) != 0u;
-    const unsigned long long bank = a.epoch & 1ull;
-    const unsigned long long val = (a.epoch << 1) | local;
+// One warp: publish (epoch << 1 | local) to every rank, wait for every
+// rank's value of this epoch; returns the OR of the flags (timed_out set if a
+// peer never arrived).
+__device__ uint32_t xchg_post_wait(const XchgDev& x, unsigned long long epoch, uint32_t local,
+                                   unsigned lane, uint32_t* timed_out_out) {
+    const unsigned long long bank = epoch & 1ull;
+    const unsigned long long val = (epoch << 1) | local;
+    __threadfence_system();  // everything this rank wrote before is visible to the peers
     for (uint32_t r = lane; r < x.world; r += 32) {
         st_release_sys(x.peer_slots[r] + bank * x.world + x.rank, val);
     }
@@ -62,7 +56,7 @@ __device__ void k1_exchange_epilogue(const K1Args& a, unsigned lane) {
         unsigned long long v;
         for (;;) {
             v = ld_acquire_sys(x.my_slots + bank * x.world + r);
-            if ((v >> 1) == a.epoch) break;
+            if ((v >> 1) == epoch) break;
             if (clock64() - start > (1ll << 35)) {
                 timed_out = 1;
                 break;
@@ -70,13 +64,45 @@ __device__ void k1_exchange_epilogue(const K1Args& a, unsigned lane) {
         }
         any |= static_cast<uint32_t>(v & 1ull);
     }
-    any = __any_sync(0xFFFFFFFFu, any != 0u);
-    timed_out = __any_sync(0xFFFFFFFFu, timed_out != 0u);
+    *timed_out_out = __any_sync(0xFFFFFFFFu, timed_out != 0u);
+    return __any_sync(0xFFFFFFFFu, any != 0u);
+}
+
+__device__ void exchange_epilogue(const XchgDev* xp, unsigned long long epoch, uint32_t* flag,
+                                  unsigned lane) {
+    __shared__ uint32_t is_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(xp->counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last || threadIdx.x >= 32) return;
+    const XchgDev& x = *xp;
+    __threadfence();
+    const uint32_t local = *reinterpret_cast<volatile uint32_t*>(flag) != 0u;
+    uint32_t timed_out = 0;
+    const uint32_t any = xchg_post_wait(x, epoch, local, lane, &timed_out);
     if (lane == 0) {
         if (timed_out) atomicExch(x.error, 1u);
-        *a.flag = (any || timed_out) ? 1u : 0u;
+        *flag = (any || timed_out) ? 1u : 0u;
         *x.counter = 0u;  // re-arm for the next launch (all CTAs have arrived)
         __threadfence();
+    }
+}
+
+__device__ __forceinline__ void k1_exchange_epilogue(const K1Args& a, unsigned lane) {
+    exchange_epilogue(a.xchg, a.epoch, a.flag, lane);
+}
+
+// A peer missing at the barrier forces this step's skip (flag) and raises
+// the error word, like a timeout in the fused exchange.
+__global__ void k_peer_barrier(const XchgDev* xp, unsigned long long epoch, uint32_t* flag) {
+    uint32_t timed_out = 0;
+    xchg_post_wait(*xp, epoch, 0u, threadIdx.x & 31u, &timed_out);
+    if (threadIdx.x == 0 && timed_out) {
+        atomicExch(xp->error, 1u);
+        if (flag) *flag = 1u;
     }
 }
 
@@ -915,6 +941,157 @@ void launch_ingest(int sk, int dk, const void* src, void* dst, uint64_t n, const
     MA_ING(kBF16, kF32) MA_ING(kBF16, kBF16) MA_ING(kBF16, kF16)
     MA_ING(kF16, kF32) MA_ING(kF16, kBF16) MA_ING(kF16, kF16)
 #undef MA_ING
+}
+
+// ============================================================== K4
+// Reduce-scatter epilogue check (the order and NaN rule
+// are those of oracle ora_reduce_check).  Sources are this rank's partition
+// on every rank, read over NVLink through CUDA IPC mappings (or any pointers
+// the device can load); each element is read once from each rank, summed in
+// rank order in fp32, scaled, stored once and tested once — the K1 pass over
+// the flat buffer disappears.  Streaming 128-bit loads; peers are read in
+// rank order with all kRsUnits units of a rank in flight together.
+template <int K>
+__device__ __forceinline__ void rs_load8(const void* base, uint64_t j, float (&x)[8]) {
+    if constexpr (K == kF32) {
+        const float4* s = reinterpret_cast<const float4*>(base) + 2 * j;
+        const float4 a = __ldcs(s), b = __ldcs(s + 1);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+        x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(base) + j);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            x[2 * k] = widen<K>(w[k] & 0xFFFFu);
+            x[2 * k + 1] = widen<K>(w[k] >> 16);
+        }
+    }
+}
+
+template <int K>
+__device__ __forceinline__ float rs_load1(const void* base, uint64_t e) {
+    return K == kF32 ? reinterpret_cast<const float*>(base)[e]
+                     : widen<K>(reinterpret_cast<const uint16_t*>(base)[e]);
+}
+
+__device__ __forceinline__ float rs_finish(float acc, float post_scale) {
+    if (post_scale != 1.0f) acc = __fmul_rn(acc, post_scale);
+    return isnan(acc) ? __uint_as_float(0x7FC00000u) : acc;
+}
+
+// store 8 results; returns the OR of (word & MASK) + INC over the stored words
+template <int K>
+__device__ __forceinline__ uint32_t rs_store8(void* base, uint64_t j, const float (&x)[8]) {
+    const ScanWord sw = scan_word(K);
+    if constexpr (K == kF32) {
+        float4* d = reinterpret_cast<float4*>(base) + 2 * j;
+        __stcs(d, make_float4(x[0], x[1], x[2], x[3]));
+        __stcs(d + 1, make_float4(x[4], x[5], x[6], x[7]));
+        uint32_t acc = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc |= (__float_as_uint(x[k]) & sw.mask) + sw.inc;
+        return acc;
+    } else {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            w[k] = static_cast<uint32_t>(narrow<K>(x[2 * k])) |
+                   (static_cast<uint32_t>(narrow<K>(x[2 * k + 1])) << 16);
+        }
+        __stcs(reinterpret_cast<uint4*>(base) + j, make_uint4(w[0], w[1], w[2], w[3]));
+        return ((w[0] & sw.mask) + sw.inc) | ((w[1] & sw.mask) + sw.inc) |
+               ((w[2] & sw.mask) + sw.inc) | ((w[3] & sw.mask) + sw.inc);
+    }
+}
+
+template <int SK, int DK>
+__device__ __forceinline__ bool rs_scalar(const RsArgs& a, uint64_t e) {
+    float acc = rs_load1<SK>(a.src[0], e);
+    for (uint32_t r = 1; r < a.nsrc; ++r) acc = __fadd_rn(acc, rs_load1<SK>(a.src[r], e));
+    acc = rs_finish(acc, a.post_scale);
+    if constexpr (DK == kF32) {
+        reinterpret_cast<float*>(a.dst)[e] = acc;
+        return elem_non_finite(__float_as_uint(acc), kF32);
+    } else {
+        const uint16_t h = narrow<DK>(acc);
+        reinterpret_cast<uint16_t*>(a.dst)[e] = h;
+        return elem_non_finite(h, DK);
+    }
+}
+
+template <int SK, int DK>
+__global__ void __launch_bounds__(256) k4_reduce_check(RsArgs a) {
+    constexpr int U = kRsUnits;
+    constexpr uint32_t kSrcBytes = SK == kF32 ? 4 : 2, kDstBytes = DK == kF32 ? 4 : 2;
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t top = scan_word(DK).top;
+    uint32_t acc_bits = 0;
+    bool bad = false;
+    if (blockIdx.x < a.tiles) {
+        const uint64_t j0 = static_cast<uint64_t>(blockIdx.x) * U * blockDim.x + threadIdx.x;
+        float acc[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
+            if (j < a.nvec) {
+                rs_load8<SK>(static_cast<const uint8_t*>(a.src[0]) + a.head * kSrcBytes, j, acc[u]);
+            }
+        }
+        for (uint32_t r = 1; r < a.nsrc; ++r) {
+            const uint8_t* body = static_cast<const uint8_t*>(a.src[r]) + a.head * kSrcBytes;
+            float x[U][8];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
+                if (j < a.nvec) rs_load8<SK>(body, j, x[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[u][k] = __fadd_rn(acc[u][k], x[u][k]);
+            }
+        }
+        uint8_t* dbody = static_cast<uint8_t*>(a.dst) + a.head * kDstBytes;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
+            if (j >= a.nvec) continue;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[u][k] = rs_finish(acc[u][k], a.post_scale);
+            acc_bits |= rs_store8<DK>(dbody, j, acc[u]);
+        }
+    } else {
+        // trailing CTAs: the scalar head and tail (everything when nvec == 0)
+        const uint64_t q0 = blockIdx.x - a.tiles, nq = gridDim.x - a.tiles;
+        const uint64_t tail_begin = a.head + a.nvec * 8;
+        const uint64_t extra = a.head + (a.n - tail_begin);
+        for (uint64_t k = q0 * blockDim.x + threadIdx.x; k < extra; k += nq * blockDim.x) {
+            bad |= rs_scalar<SK, DK>(a, k < a.head ? k : tail_begin + (k - a.head));
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, bad || (acc_bits & top) != 0u) && lane == 0) {
+        *a.flag = 1u;
+        if (a.xchg) __threadfence();
+    }
+    if (a.xchg) exchange_epilogue(a.xchg, a.epoch, a.flag, lane);
+}
+
+void launch_reduce_check(int sk, int dk, const RsArgs& a, unsigned grid, cudaStream_t st) {
+#define MA_RS(S, D)                                                 \
+    if (sk == S && dk == D) {                                       \
+        k4_reduce_check<S, D><<<grid, 256, 0, st>>>(a);             \
+        return;                                                     \
+    }
+    MA_RS(kF32, kF32) MA_RS(kF32, kBF16) MA_RS(kF32, kF16)
+    MA_RS(kBF16, kF32) MA_RS(kBF16, kBF16) MA_RS(kBF16, kF16)
+    MA_RS(kF16, kF32) MA_RS(kF16, kBF16) MA_RS(kF16, kF16)
+#undef MA_RS
+}
+
+void launch_peer_barrier(const XchgDev* x, unsigned long long epoch, uint32_t* flag,
+                         cudaStream_t st) {
+    k_peer_barrier<<<1, 32, 0, st>>>(x, epoch, flag);
 }
 
 __global__ void k_plant(void* buf, int dtype, uint64_t index, uint32_t bits) {

@@ -100,6 +100,31 @@ void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs&
 constexpr int kK3Slots = 2;
 int k3_blocks_per_sm(int gk);
 void launch_k3(int gk, const SegTable& tab, const AdamArgs& a, unsigned grid, cudaStream_t st);
+// K4: gradient reduce-scatter with the overflow check in its epilogue
+// (SURVEY §8(f) row 2).  dst[i] = post_scale * sum_r src[r][i] (fp32, rank
+// order), stored in the stepper's gradient kind, non-finite test on the
+// stored value.  8-element units; one tile of kRsUnits x 256 units per CTA,
+// trailing CTAs for the scalar head/tail (or the whole range when the
+// sources and dst cannot be co-aligned).
+constexpr int kRsUnits = 2;
+struct RsArgs {
+    const void* src[kMaxRanks];  // each source at the element `head` is measured from
+    void* dst;
+    uint64_t n;
+    uint64_t head;   // scalar elements before the 16-byte-aligned body
+    uint64_t nvec;   // 8-element units in the body
+    uint64_t tiles;  // CTAs of the vector body
+    uint32_t nsrc;
+    float post_scale;
+    uint32_t* flag;
+    const XchgDev* xchg;  // non-null: exit barrier + flag OR fused into the last CTA
+    unsigned long long epoch;
+};
+void launch_reduce_check(int sk, int dk, const RsArgs& a, unsigned grid, cudaStream_t st);
+// all ranks meet at `epoch` (one warp; peers' slots over NVLink); a timeout
+// sets *flag (when non-null) so the step is skipped
+void launch_peer_barrier(const XchgDev* x, unsigned long long epoch, uint32_t* flag,
+                         cudaStream_t st);
 void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s);
 void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,
                         unsigned grid, cudaStream_t st);

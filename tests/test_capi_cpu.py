@@ -82,3 +82,7 @@ def test_no_device_fails_loudly(so_path):
     assert lib.ma_adam_step(buf, buf, buf, buf, 0, 4, 1, C.byref(h), 1.0, None, 3) == 101
     # argument validation still reports the reference's invalid_argument first
     assert lib.ma_adam_step(buf, buf, buf, buf, 0, 4, 0, C.byref(h), 1.0, None, 3) == 1
+    # the reduce-scatter entry points need a device too
+    rs = C.c_void_p()
+    rec = (C.c_ubyte * capi.RS_HANDLE_BYTES)()
+    assert lib.ma_rs_create(2, 0, buf, 4, 1, C.byref(rs), rec) == 101
