@@ -485,10 +485,8 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
     __stcs(reinterpret_cast<float4*>(sg.m + e), s.m);
     __stcs(reinterpret_cast<float4*>(sg.v + e), s.v);
     if constexpr (WK != kNone) {
-        const uint32_t lo = static_cast<uint32_t>(narrow<WK>(s.p.x)) |
-                            (static_cast<uint32_t>(narrow<WK>(s.p.y)) << 16);
-        const uint32_t hi = static_cast<uint32_t>(narrow<WK>(s.p.z)) |
-                            (static_cast<uint32_t>(narrow<WK>(s.p.w)) << 16);
+        const uint32_t lo = narrow2<WK>(s.p.x, s.p.y);
+        const uint32_t hi = narrow2<WK>(s.p.z, s.p.w);
         __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.w) + e), make_uint2(lo, hi));
     }
 }
@@ -774,14 +772,13 @@ __device__ __forceinline__ void bf16_state_scalar(const Seg& sg, uint64_t e, con
     uint16_t* V = reinterpret_cast<uint16_t*>(sg.v);
     float p = widen_bf16(P[e]), m = widen_bf16(M[e]), v = widen_bf16(V[e]);
     adam_elem(p, m, v, load_grad1<GK>(sg.g, e), c, s);
-    P[e] = bf16_bits(p);
-    M[e] = bf16_bits(m);
-    V[e] = bf16_bits(v);
+    P[e] = narrow<kBF16>(p);
+    M[e] = narrow<kBF16>(m);
+    V[e] = narrow<kBF16>(v);
 }
 
 __device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d) {
-    return make_uint2(static_cast<uint32_t>(bf16_bits(a)) | (static_cast<uint32_t>(bf16_bits(b)) << 16),
-                      static_cast<uint32_t>(bf16_bits(c)) | (static_cast<uint32_t>(bf16_bits(d)) << 16));
+    return make_uint2(narrow2<kBF16>(a, b), narrow2<kBF16>(c, d));
 }
 
 template <int GK>
@@ -996,8 +993,7 @@ __device__ __forceinline__ uint32_t rs_store8(void* base, uint64_t j, const floa
         uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            w[k] = static_cast<uint32_t>(narrow<K>(x[2 * k])) |
-                   (static_cast<uint32_t>(narrow<K>(x[2 * k + 1])) << 16);
+            w[k] = narrow2<K>(x[2 * k], x[2 * k + 1]);
         }
         __stcs(reinterpret_cast<uint4*>(base) + j, make_uint4(w[0], w[1], w[2], w[3]));
         return ((w[0] & sw.mask) + sw.inc) | ((w[1] & sw.mask) + sw.inc) |
@@ -1111,12 +1107,22 @@ __global__ void k_cast_sweep(int log2, uint64_t* out, uint64_t nblocks) {
     if (b >= nblocks) return;
     uint64_t h = 1469598103934665603ull;
     const uint64_t len = 1ull << log2;
-    for (uint64_t k = 0; k < len; ++k) {
-        const uint16_t r = narrow<K>(__uint_as_float(static_cast<uint32_t>((b << log2) + k)));
-        h = (h ^ (r & 0xFFu)) * 1099511628211ull;
-        h = (h ^ (r >> 8)) * 1099511628211ull;
+    bool lanes_agree = true;
+    for (uint64_t k = 0; k < len; k += 2) {
+        // consecutive patterns through the pair conversion, and again with the
+        // lanes swapped, so every input is checked in both lanes
+        const float x0 = __uint_as_float(static_cast<uint32_t>((b << log2) + k));
+        const float x1 = __uint_as_float(static_cast<uint32_t>((b << log2) + k + 1));
+        const uint32_t w = narrow2<K>(x0, x1);
+        const uint32_t sw = narrow2<K>(x1, x0);
+        lanes_agree &= sw == ((w >> 16) | (w << 16));
+        for (int e = 0; e < 2; ++e) {
+            const uint32_t r = (w >> (16 * e)) & 0xFFFFu;
+            h = (h ^ (r & 0xFFu)) * 1099511628211ull;
+            h = (h ^ (r >> 8)) * 1099511628211ull;
+        }
     }
-    out[b] = h;
+    out[b] = lanes_agree ? h : ~h;
 }
 
 // K1's word test applied to every pattern vs the IEEE classification.
