@@ -300,6 +300,13 @@ MA_API int ma_debug_cast_sweep(int kind, int block_log2, uint64_t* out_host);
 /* Number of 32-bit (kind F32) or 16-bit patterns where K1's predicate
  * disagrees with !isfinite(); exhaustive. */
 MA_API int ma_debug_mask_sweep(int kind, uint64_t* mismatches);
+/* Verification of the hoisted-guard Adam fast path against the IEEE
+ * intrinsics (see ma_device.cuh): mode 0 square root over every admitted
+ * input, mode 1 division by each of `divisors` (bias corrections) over all
+ * significands at eight exponents, mode 2 `samples` random (m_hat, den)
+ * divisions.  Returns the number of bitwise mismatches and of inputs checked. */
+MA_API int ma_debug_fast_sweep(int mode, const float* divisors, uint32_t ndiv, uint64_t samples,
+                               uint64_t seed, uint64_t* mismatches, uint64_t* checked);
 
 #ifdef __cplusplus
 }

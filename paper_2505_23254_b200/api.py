@@ -431,6 +431,15 @@ def debug_cast_sweep(kind: str, block_log2: int = 20) -> np.ndarray:
     return out
 
 
+def debug_fast_sweep(mode: int, divisors=None, samples: int = 0, seed: int = 1):
+    """(mismatches, checked) of the Adam fast path vs the IEEE intrinsics."""
+    mm, n = C.c_uint64(), C.c_uint64()
+    arr = np.ascontiguousarray(divisors if divisors is not None else [], dtype=np.float32)
+    check(capi.lib().ma_debug_fast_sweep(mode, arr.ctypes.data if arr.size else None, arr.size,
+                                         samples, seed, C.byref(mm), C.byref(n)))
+    return mm.value, n.value
+
+
 def debug_mask_sweep(kind: str) -> int:
     mm = C.c_uint64()
     check(capi.lib().ma_debug_mask_sweep(capi.DTYPES[kind], C.byref(mm)))

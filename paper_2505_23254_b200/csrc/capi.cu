@@ -1130,6 +1130,37 @@ int ma_debug_cast_sweep(int kind, int block_log2, uint64_t* out_host) {
     });
 }
 
+int ma_debug_fast_sweep(int mode, const float* divisors, uint32_t ndiv, uint64_t samples,
+                        uint64_t seed, uint64_t* mismatches, uint64_t* checked) {
+    return guarded([&] {
+        if (!mismatches || !checked) fail(MA_ERR_INVALID_ARGUMENT, "null output");
+        if (mode < 0 || mode > 2) fail(MA_ERR_INVALID_ARGUMENT, "mode must be 0, 1 or 2");
+        if (mode == 1 && (!divisors || ndiv == 0)) fail(MA_ERR_INVALID_ARGUMENT, "no divisors");
+        const DeviceInfo dv = device_info();
+        const uint64_t count = mode == 0 ? 0x60000001ull
+                               : mode == 1 ? static_cast<uint64_t>(ndiv) << 27
+                                           : samples;
+        unsigned long long* d = nullptr;
+        float* dd = nullptr;
+        CK(cudaMalloc(&d, 8));
+        CK(cudaMemset(d, 0, 8));
+        if (mode == 1) {
+            CK(cudaMalloc(&dd, ndiv * sizeof(float)));
+            CK(cudaMemcpy(dd, divisors, ndiv * sizeof(float), cudaMemcpyHostToDevice));
+        }
+        ma::launch_fast_sweep(mode, dd, count, seed, d, static_cast<unsigned>(dv.sms * 16));
+        const cudaError_t e = cudaGetLastError();
+        unsigned long long h = 0;
+        const cudaError_t e2 = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        if (dd) cudaFree(dd);
+        CK(e);
+        CK(e2);
+        *mismatches = h;
+        *checked = count;
+    });
+}
+
 int ma_debug_mask_sweep(int kind, uint64_t* mismatches) {
     return guarded([&] {
         check_grad_dtype(kind);

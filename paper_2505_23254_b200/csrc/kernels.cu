@@ -268,6 +268,9 @@ __device__ __forceinline__ bool resolve_step(const AdamArgs& a, StepScalars& s) 
         s.bc2 = a.bc2;
     }
     s.scale_pow2 = exact_reciprocal(s.scale, &s.inv_scale);
+    s.fast = s.scale_pow2 && fast_step_ok(s.bc1, s.bc2, a.c.eps);
+    s.y1 = s.fast ? rcp_refined(s.bc1) : 0.0f;
+    s.y2 = s.fast ? rcp_refined(s.bc2) : 0.0f;
     return true;
 }
 
@@ -455,7 +458,9 @@ __device__ __forceinline__ void load_slot(const Seg& sg, uint64_t e, Slot4& s) {
     }
 }
 
-template <int GK, int WK, bool PROBE = false>
+// MATH: 0 = production (hoisted-guard fast path, exact fallback), 1 = probe
+// (approximate div/sqrt, never production), 2 = exact intrinsics only (A/B)
+template <int GK, int WK, int MATH = 0>
 __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
                                             const AdamConsts& c, const StepScalars& sc) {
     float g0, g1, g2, g3;
@@ -470,16 +475,25 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
         g2 = widen<GK>(s.g.y & 0xFFFFu);
         g3 = widen<GK>(s.g.y >> 16);
     }
-    if constexpr (PROBE) {
+    if constexpr (MATH == 1) {
         adam_elem_probe(s.p.x, s.m.x, s.v.x, g0, c, sc);
         adam_elem_probe(s.p.y, s.m.y, s.v.y, g1, c, sc);
         adam_elem_probe(s.p.z, s.m.z, s.v.z, g2, c, sc);
         adam_elem_probe(s.p.w, s.m.w, s.v.w, g3, c, sc);
-    } else {
+    } else if constexpr (MATH == 2) {
         adam_elem(s.p.x, s.m.x, s.v.x, g0, c, sc);
         adam_elem(s.p.y, s.m.y, s.v.y, g1, c, sc);
         adam_elem(s.p.z, s.m.z, s.v.z, g2, c, sc);
         adam_elem(s.p.w, s.m.w, s.v.w, g3, c, sc);
+    } else {
+        float p[4] = {s.p.x, s.p.y, s.p.z, s.p.w};
+        float m[4] = {s.m.x, s.m.y, s.m.z, s.m.w};
+        float v[4] = {s.v.x, s.v.y, s.v.z, s.v.w};
+        const float g[4] = {g0, g1, g2, g3};
+        adam_n<4>(p, m, v, g, c, sc);
+        s.p = make_float4(p[0], p[1], p[2], p[3]);
+        s.m = make_float4(m[0], m[1], m[2], m[3]);
+        s.v = make_float4(v[0], v[1], v[2], v[3]);
     }
     __stcs(reinterpret_cast<float4*>(sg.p + e), s.p);
     __stcs(reinterpret_cast<float4*>(sg.m + e), s.m);
@@ -500,13 +514,13 @@ __device__ __forceinline__ void load_tile(const Seg& sg, uint64_t lt, Slot4 (&t)
     }
 }
 
-template <int GK, int WK, int U, bool PROBE = false>
+template <int GK, int WK, int U, int MATH = 0>
 __device__ __forceinline__ void update_tile(const Seg& sg, uint64_t lt, Slot4 (&t)[U],
                                             const AdamConsts& c, const StepScalars& sc) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const uint64_t j = lt * (U * kK2Threads) + u * kK2Threads + threadIdx.x;
-        if (j < sg.nvec) update_slot<GK, WK, PROBE>(sg, sg.head + 4 * j, t[u], c, sc);
+        if (j < sg.nvec) update_slot<GK, WK, MATH>(sg, sg.head + 4 * j, t[u], c, sc);
     }
 }
 
@@ -531,12 +545,12 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_stream(SegTable tab, Adam
             if constexpr (PF) {
                 Slot4 nxt[U];
                 if (more) load_tile<GK, U, LD>(tab.seg[sn], tn - tab.seg[sn].tile_begin, nxt);
-                update_tile<GK, WK, U, LD == 3>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
+                update_tile<GK, WK, U, LD == 3 ? 1 : 0>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
                 if (!more) break;
 #pragma unroll
                 for (int u = 0; u < U; ++u) cur[u] = nxt[u];
             } else {
-                update_tile<GK, WK, U, LD == 3>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
+                update_tile<GK, WK, U, LD == 3 ? 1 : 0>(tab.seg[si], t - tab.seg[si].tile_begin, cur, c, sc);
                 if (!more) break;
                 load_tile<GK, U, LD>(tab.seg[sn], tn - tab.seg[sn].tile_begin, cur);
             }
@@ -582,8 +596,8 @@ __device__ __forceinline__ uint32_t seg_of_tile(const SegTable& tab, uint64_t t)
     return lo;
 }
 
-template <int GK, int WK, int U, bool PROBE = false>
-__global__ void __launch_bounds__(kK2Threads) k2_oneshot(SegTable tab, AdamArgs a) {
+template <int GK, int WK, int U, int MATH = 0, int MINB = 1>
+__global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, AdamArgs a) {
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
     const AdamConsts c = a.c;
@@ -592,7 +606,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_oneshot(SegTable tab, AdamArgs 
         const Seg& sg = tab.seg[seg_of_tile(tab, t)];
         Slot4 cur[U];
         load_tile<GK, U>(sg, t - sg.tile_begin, cur);
-        update_tile<GK, WK, U, PROBE>(sg, t - sg.tile_begin, cur, c, sc);
+        update_tile<GK, WK, U, MATH>(sg, t - sg.tile_begin, cur, c, sc);
         return;
     }
     // trailing CTAs: unaligned heads/tails and non-co-alignable sub-groups
@@ -803,8 +817,7 @@ __device__ __forceinline__ void bf16_state_slot(const Seg& sg, uint64_t e, const
                   widen_bf16(mq.y >> 16)};
     float v[4] = {widen_bf16(vq.x & 0xFFFFu), widen_bf16(vq.x >> 16), widen_bf16(vq.y & 0xFFFFu),
                   widen_bf16(vq.y >> 16)};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) adam_elem(p[k], m[k], v[k], g[k], c, s);
+    adam_n<4>(p, m, v, g, c, s);
     __stcs(P, pack_bf16x4(p[0], p[1], p[2], p[3]));
     __stcs(M, pack_bf16x4(m[0], m[1], m[2], m[3]));
     __stcs(V, pack_bf16x4(v[0], v[1], v[2], v[3]));
@@ -1125,6 +1138,48 @@ __global__ void k_cast_sweep(int log2, uint64_t* out, uint64_t nblocks) {
     out[b] = lanes_agree ? h : ~h;
 }
 
+// Equality of the hoisted-guard fast path (ma_device.cuh) with the IEEE
+// intrinsics over the ranges adam_fast admits:
+//  mode 0: sqrt_fast(x) == __fsqrt_rn(x) for EVERY x in [2^-96, 2^96];
+//  mode 1: div_by(a, d, rcp_refined(d)) == __fdiv_rn(a, d) for every divisor
+//          in `divs` and all 2^24 signed significands of a at eight exponents
+//          spanning the admitted range (a power-of-two factor is exact in both);
+//  mode 2: `count` seeded random pairs, |a| in [2^-50, 2^66], d in
+//          [2^-40, 2^49] (the mh / den division).
+__global__ void k_fast_sweep(int mode, const float* divs, uint64_t count, uint64_t seed,
+                             unsigned long long* bad) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    unsigned long long nbad = 0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += stride) {
+        if (mode == 0) {
+            const float x = __uint_as_float(0x0F800000u + static_cast<uint32_t>(i));
+            nbad += __float_as_uint(sqrt_fast(x)) != __float_as_uint(__fsqrt_rn(x));
+        } else if (mode == 1) {
+            constexpr uint32_t kExp[8] = {31, 32, 77, 126, 127, 176, 177, 205};
+            const float d = divs[i >> 27];
+            const uint32_t r = static_cast<uint32_t>(i & ((1ull << 27) - 1));
+            const uint32_t bits = ((r & (1u << 23)) << 8) | (kExp[r >> 24] << 23) | (r & 0x7FFFFFu);
+            const float a = __uint_as_float(bits);
+            nbad += __float_as_uint(div_by(a, d, rcp_refined(d))) != __float_as_uint(__fdiv_rn(a, d));
+        } else {
+            const uint64_t h1 = splitmix64(seed ^ (2 * i)), h2 = splitmix64(seed ^ (2 * i + 1));
+            const uint32_t ea = 77 + static_cast<uint32_t>((h1 >> 32) % 117);  // 2^-50 .. 2^66
+            const uint32_t ed = 87 + static_cast<uint32_t>((h2 >> 32) % 90);   // 2^-40 .. 2^49
+            const float a = __uint_as_float((static_cast<uint32_t>(h1 >> 31) & 0x80000000u) |
+                                            (ea << 23) | (static_cast<uint32_t>(h1) & 0x7FFFFFu));
+            const float d = __uint_as_float((ed << 23) | (static_cast<uint32_t>(h2) & 0x7FFFFFu));
+            nbad += __float_as_uint(div_by(a, d, rcp_refined(d))) != __float_as_uint(__fdiv_rn(a, d));
+        }
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+
+void launch_fast_sweep(int mode, const float* divs, uint64_t count, uint64_t seed,
+                       unsigned long long* bad, unsigned grid) {
+    k_fast_sweep<<<grid, 256>>>(mode, divs, count, seed, bad);
+}
+
 // K1's word test applied to every pattern vs the IEEE classification.
 __global__ void k_mask_sweep(int kind, unsigned long long* mismatches) {
     const ScanWord sw = scan_word(kind);
@@ -1197,7 +1252,11 @@ template <int GK, int WK> struct K2Kernel<GK, WK, 13> { static constexpr auto fn
 template <int GK, int WK> struct K2Kernel<GK, WK, 14> { static constexpr auto fn = k2_oneshot<GK, WK, 4>; };
 template <int GK, int WK> struct K2Kernel<GK, WK, 15> { static constexpr auto fn = k2_oneshot<GK, WK, 1>; };
 // 16: PROBE ONLY — variant 14 with approximate div/sqrt (power/instruction headroom)
-template <int GK, int WK> struct K2Kernel<GK, WK, 16> { static constexpr auto fn = k2_oneshot<GK, WK, 4, true>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 16> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 1>; };
+// 17: variant 14 held to 3 CTAs/SM (<= 80 registers); 18: variant 14 with the
+// exact intrinsics only (no hoisted-guard fast path) — the previous production
+template <int GK, int WK> struct K2Kernel<GK, WK, 17> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 0, 3>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 18> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 2>; };
 
 template <int GK, int WK, int V>
 int k2_occupancy() {
@@ -1228,6 +1287,8 @@ void k2_variants(int variant, F&& f) {
             case 14: f(std::integral_constant<int, 14>{}); return;
             case 15: f(std::integral_constant<int, 15>{}); return;
             case 16: f(std::integral_constant<int, 16>{}); return;
+            case 17: f(std::integral_constant<int, 17>{}); return;
+            case 18: f(std::integral_constant<int, 18>{}); return;
             default: break;
         }
     }
@@ -1283,6 +1344,8 @@ int k2_effective_variant(int gk, int wk, int variant) {
     return v;
 }
 
+bool k2_variant_oneshot(int variant) { return variant >= 13 && variant <= 18; }
+
 void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
     if (is_tma(variant)) {
         *vec = 8;
@@ -1290,7 +1353,7 @@ void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
         *stream = true;
         return;
     }
-    if (variant >= 13 && variant <= 16) {
+    if (k2_variant_oneshot(variant)) {
         *vec = 4;
         *tile_vectors = (variant == 13 ? 2 : variant == 15 ? 1 : 4) * kK2Threads;
         *stream = true;
@@ -1300,13 +1363,11 @@ void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
     static const int kTile[10] = {kK2Threads, kK2Threads, 2 * kK2Threads, kK2Threads,
                                   2 * kK2Threads, 4 * kK2Threads, 2 * kK2Threads, 2 * kK2Threads,
                                   2 * kK2Threads, 2 * kK2Threads};
-    const int v = variant >= 0 && variant < 10 ? variant : kK2DefaultVariant;
+    const int v = variant >= 0 && variant < 10 ? variant : 2;  // 12 = variant 2's shape
     *vec = kVec[v];
     *tile_vectors = kTile[v];
     *stream = v >= 2;
 }
-
-bool k2_variant_oneshot(int variant) { return variant >= 13 && variant <= 16; }
 
 int k2_blocks_per_sm(int gk, int wk, int variant) {
     if (variant == kTmaVariant) return tma_blocks_per_sm<128>();

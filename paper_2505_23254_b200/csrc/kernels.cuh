@@ -136,5 +136,7 @@ void launch_ingest(int sk, int dk, const void* src, void* dst, uint64_t n, const
                    uint32_t* flag, unsigned grid, cudaStream_t st);
 void launch_cast_sweep(int kind, int log2, uint64_t* out, uint64_t nblocks);
 void launch_mask_sweep(int kind, unsigned long long* mismatches, unsigned grid);
+void launch_fast_sweep(int mode, const float* divs, uint64_t count, uint64_t seed,
+                       unsigned long long* bad, unsigned grid);
 
 }  // namespace ma

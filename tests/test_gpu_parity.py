@@ -154,6 +154,67 @@ def test_cast_exhaustive_vs_reference(golden, kind, key):
     assert (got == want).all(), np.nonzero(got != want)[0][:5]
 
 
+# ------------------------------------------------------- Adam fast path
+def test_fast_path_sqrt_exhaustive():
+    """sqrt_fast == __fsqrt_rn for every input the guarded fast path admits."""
+    bad, n = mab.api.debug_fast_sweep(0)
+    assert n == 0x60000001 and bad == 0
+
+
+def test_fast_path_division_by_bias_corrections():
+    """m/bc1 and v/bc2 through the per-CTA reciprocal == __fdiv_rn, for the
+    bias corrections (glibc powf, as the table holds them) of t = 1..2000 at
+    the default betas, t = 1..200 at two other beta pairs and large t, over
+    all 2^24 signed significands at eight exponents of the admitted range."""
+    ds = set()
+    for (b1, b2), ts in (((0.9, 0.999), list(range(1, 2001)) + [10**4, 10**5, 10**6, 10**7]),
+                         ((0.95, 0.999), range(1, 201)), ((0.99, 0.9999), range(1, 201))):
+        for t in ts:
+            ds.update(ora.step_scalars(t, b1, b2))
+    divs = np.array(sorted(d for d in ds if 2.0 ** -16 <= d <= 1.0), np.float32)
+    assert divs.size > 2500
+    bad, n = mab.api.debug_fast_sweep(1, divs)
+    assert n == divs.size << 27 and bad == 0
+
+
+def test_fast_path_general_division_random():
+    """mh / den through the refined reciprocal == __fdiv_rn on 2^36 random
+    pairs over the admitted ranges."""
+    bad, n = mab.api.debug_fast_sweep(2, samples=1 << 36, seed=12345)
+    assert n == 1 << 36 and bad == 0
+
+
+def test_k2_fast_path_fallback_slots_bit_exact():
+    """Slots whose new m/v leave the guarded ranges (zeros, tiny and huge
+    moments, subnormal gradients) recompute exactly: K2 equals the oracle
+    element for element (NaN-producing inputs are excluded: x86 and the GPU
+    propagate different NaN payloads)."""
+    n = 1 << 16
+    rs = np.random.default_rng(5)
+    g = (rs.standard_normal(n) * 1024).astype(f32)
+    m = (rs.standard_normal(n) * 1e-3).astype(f32)
+    v = np.abs(rs.standard_normal(n) * 1e-6).astype(f32)
+    p = rs.standard_normal(n).astype(f32)
+    sel = rs.integers(0, n, 4000)
+    g[sel[:500]] = 0.0
+    m[sel[:500]] = 0.0
+    v[sel[:500]] = 0.0                                        # m = v = 0 exactly
+    m[sel[500:1000]] = 1e-30                                  # |m| below 2^-50
+    v[sel[1000:1500]] = 1e-35                                 # v below 2^-96
+    m[sel[1500:2000]] = 3e17                                  # |m| above 2^50
+    v[sel[2000:2500]] = 3e30                                  # v above 2^80
+    g[sel[2500:2600]] = 1e-45                                 # subnormal gradients
+    p[sel[2600:2700]] = 0.0
+    h = ora.hyper(lr=1e-3, weight_decay=0.01)
+    for t in (1, 7, 1000):
+        want = [x.copy() for x in (p, m, v)]
+        ora.adam_step(*want, g, t, h, 1024.0, g_kind="f32", w_kind="none")
+        dp, dm, dv, dg = _dev(p, m, v, g)
+        mab.adam_step_fp32(dp, dm, dv, dg, t, mab.AdamHyper(lr=1e-3, weight_decay=0.01), 1024.0)
+        for a, b in zip((dp, dm, dv), want):
+            assert (a.cpu().numpy().view(np.uint32) == b.view(np.uint32)).all(), t
+
+
 # ------------------------------------------------------------------ K2
 def _dev(*arrs):
     return [torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in arrs]
