@@ -490,7 +490,19 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
         float m[4] = {s.m.x, s.m.y, s.m.z, s.m.w};
         float v[4] = {s.v.x, s.v.y, s.v.z, s.v.w};
         const float g[4] = {g0, g1, g2, g3};
-        adam_n<4>(p, m, v, g, c, sc);
+        if (sc.fast && adam_fast<4>(p, m, v, g, c, sc)) {
+            // no output of a fast slot is NaN: plain pair conversions
+            __stcs(reinterpret_cast<float4*>(sg.p + e), make_float4(p[0], p[1], p[2], p[3]));
+            __stcs(reinterpret_cast<float4*>(sg.m + e), make_float4(m[0], m[1], m[2], m[3]));
+            __stcs(reinterpret_cast<float4*>(sg.v + e), make_float4(v[0], v[1], v[2], v[3]));
+            if constexpr (WK != kNone) {
+                __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.w) + e),
+                       make_uint2(narrow2_num<WK>(p[0], p[1]), narrow2_num<WK>(p[2], p[3])));
+            }
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) adam_elem(p[k], m[k], v[k], g[k], c, sc);
         s.p = make_float4(p[0], p[1], p[2], p[3]);
         s.m = make_float4(m[0], m[1], m[2], m[3]);
         s.v = make_float4(v[0], v[1], v[2], v[3]);
@@ -604,9 +616,30 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, Ada
     const uint64_t t = blockIdx.x;
     if (t < tab.total_tiles) {
         const Seg& sg = tab.seg[seg_of_tile(tab, t)];
+        const uint64_t lt = t - sg.tile_begin;
+        // this thread's slot-0 element; slot u is u * 1024 elements further,
+        // so every access below is base register + compile-time offset
+        const uint64_t j0 = lt * (U * kK2Threads) + threadIdx.x;
+        const uint64_t e0 = sg.head + 4 * j0;
+        Seg loc;
+        loc.p = sg.p + e0;
+        loc.m = sg.m + e0;
+        loc.v = sg.v + e0;
+        loc.g = static_cast<const uint8_t*>(sg.g) + e0 * (GK == kF32 ? 4 : 2);
+        loc.w = WK == kNone ? nullptr : static_cast<void*>(static_cast<uint16_t*>(sg.w) + e0);
+        const uint64_t nv = sg.nvec;
+        const bool full = (lt + 1) * (U * kK2Threads) <= nv;
         Slot4 cur[U];
-        load_tile<GK, U>(sg, t - sg.tile_begin, cur);
-        update_tile<GK, WK, U, MATH>(sg, t - sg.tile_begin, cur, c, sc);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (full || j0 + u * kK2Threads < nv) load_slot<GK>(loc, 4 * u * kK2Threads, cur[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (full || j0 + u * kK2Threads < nv) {
+                update_slot<GK, WK, MATH>(loc, 4 * u * kK2Threads, cur[u], c, sc);
+            }
+        }
         return;
     }
     // trailing CTAs: unaligned heads/tails and non-co-alignable sub-groups
@@ -795,32 +828,65 @@ __device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d)
     return make_uint2(narrow2<kBF16>(a, b), narrow2<kBF16>(c, d));
 }
 
+// One 4-element slot of bf16 state: 3 x 8 B of p/m/v and 8 B (bf16/f16) or
+// 16 B (f32) of gradient.  A tile's slots are all loaded before the first
+// store (stores could alias later loads, so the compiler would otherwise
+// keep one slot in flight per thread).
+struct Slot3 {
+    uint2 p, m, v;
+    uint4 g;
+};
+
 template <int GK>
-__device__ __forceinline__ void bf16_state_slot(const Seg& sg, uint64_t e, const AdamConsts& c,
-                                                const StepScalars& s) {
-    uint2* P = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.p) + e);
-    uint2* M = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.m) + e);
-    uint2* V = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.v) + e);
-    const uint2 pq = __ldcs(P), mq = __ldcs(M), vq = __ldcs(V);
-    float g[4];
+__device__ __forceinline__ void bf16_state_load(const Seg& sg, uint64_t e, Slot3& q) {
+    q.p = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.p) + e));
+    q.m = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.m) + e));
+    q.v = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.v) + e));
     if constexpr (GK == kF32) {
-        const float4 t = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(sg.g) + e));
-        g[0] = t.x; g[1] = t.y; g[2] = t.z; g[3] = t.w;
+        q.g = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(sg.g) + e));
     } else {
         const uint2 t = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.g) + e));
-        g[0] = widen<GK>(t.x & 0xFFFFu); g[1] = widen<GK>(t.x >> 16);
-        g[2] = widen<GK>(t.y & 0xFFFFu); g[3] = widen<GK>(t.y >> 16);
+        q.g = make_uint4(t.x, t.y, 0u, 0u);
     }
-    float p[4] = {widen_bf16(pq.x & 0xFFFFu), widen_bf16(pq.x >> 16), widen_bf16(pq.y & 0xFFFFu),
-                  widen_bf16(pq.y >> 16)};
-    float m[4] = {widen_bf16(mq.x & 0xFFFFu), widen_bf16(mq.x >> 16), widen_bf16(mq.y & 0xFFFFu),
-                  widen_bf16(mq.y >> 16)};
-    float v[4] = {widen_bf16(vq.x & 0xFFFFu), widen_bf16(vq.x >> 16), widen_bf16(vq.y & 0xFFFFu),
-                  widen_bf16(vq.y >> 16)};
-    adam_n<4>(p, m, v, g, c, s);
-    __stcs(P, pack_bf16x4(p[0], p[1], p[2], p[3]));
-    __stcs(M, pack_bf16x4(m[0], m[1], m[2], m[3]));
-    __stcs(V, pack_bf16x4(v[0], v[1], v[2], v[3]));
+}
+
+template <bool NUM>
+__device__ __forceinline__ uint2 pack4(const float (&x)[4]) {
+    if constexpr (NUM) return make_uint2(narrow2_num<kBF16>(x[0], x[1]), narrow2_num<kBF16>(x[2], x[3]));
+    return make_uint2(narrow2<kBF16>(x[0], x[1]), narrow2<kBF16>(x[2], x[3]));
+}
+
+// P/M/V/G point at this thread's element of slot 0; slot u is u * 1024
+// elements further (compile-time offsets folded into the memory instructions).
+template <int GK>
+__device__ __forceinline__ void bf16_state_update(uint16_t* P, uint16_t* M, uint16_t* V,
+                                                  const Slot3& q, const AdamConsts& c,
+                                                  const StepScalars& s) {
+    float g[4];
+    if constexpr (GK == kF32) {
+        g[0] = __uint_as_float(q.g.x); g[1] = __uint_as_float(q.g.y);
+        g[2] = __uint_as_float(q.g.z); g[3] = __uint_as_float(q.g.w);
+    } else {
+        g[0] = widen<GK>(q.g.x & 0xFFFFu); g[1] = widen<GK>(q.g.x >> 16);
+        g[2] = widen<GK>(q.g.y & 0xFFFFu); g[3] = widen<GK>(q.g.y >> 16);
+    }
+    float p[4] = {widen_bf16(q.p.x & 0xFFFFu), widen_bf16(q.p.x >> 16), widen_bf16(q.p.y & 0xFFFFu),
+                  widen_bf16(q.p.y >> 16)};
+    float m[4] = {widen_bf16(q.m.x & 0xFFFFu), widen_bf16(q.m.x >> 16), widen_bf16(q.m.y & 0xFFFFu),
+                  widen_bf16(q.m.y >> 16)};
+    float v[4] = {widen_bf16(q.v.x & 0xFFFFu), widen_bf16(q.v.x >> 16), widen_bf16(q.v.y & 0xFFFFu),
+                  widen_bf16(q.v.y >> 16)};
+    if (s.fast && adam_fast<4>(p, m, v, g, c, s)) {
+        __stcs(reinterpret_cast<uint2*>(P), pack4<true>(p));
+        __stcs(reinterpret_cast<uint2*>(M), pack4<true>(m));
+        __stcs(reinterpret_cast<uint2*>(V), pack4<true>(v));
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) adam_elem(p[k], m[k], v[k], g[k], c, s);
+    __stcs(reinterpret_cast<uint2*>(P), pack4<false>(p));
+    __stcs(reinterpret_cast<uint2*>(M), pack4<false>(m));
+    __stcs(reinterpret_cast<uint2*>(V), pack4<false>(v));
 }
 
 template <int GK>
@@ -834,10 +900,24 @@ __global__ void __launch_bounds__(kK2Threads) k3_adam_bf16(SegTable tab, AdamArg
     if (t < tab.total_tiles) {
         const Seg& sg = tab.seg[seg_of_tile(tab, t)];
         const uint64_t lt = t - sg.tile_begin;
+        const uint64_t j0 = lt * (U * kK2Threads) + threadIdx.x;
+        const uint64_t e0 = sg.head + 4 * j0;
+        uint16_t* P = reinterpret_cast<uint16_t*>(sg.p) + e0;
+        uint16_t* M = reinterpret_cast<uint16_t*>(sg.m) + e0;
+        uint16_t* V = reinterpret_cast<uint16_t*>(sg.v) + e0;
+        const uint64_t nv = sg.nvec;
+        const bool full = (lt + 1) * (U * kK2Threads) <= nv;
+        Slot3 q[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t j = lt * (U * kK2Threads) + u * kK2Threads + threadIdx.x;
-            if (j < sg.nvec) bf16_state_slot<GK>(sg, sg.head + 4 * j, c, sc);
+            if (full || j0 + u * kK2Threads < nv) bf16_state_load<GK>(sg, e0 + 4 * u * kK2Threads, q[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (full || j0 + u * kK2Threads < nv) {
+                const int o = 4 * u * kK2Threads;
+                bf16_state_update<GK>(P + o, M + o, V + o, q[u], c, sc);
+            }
         }
         return;
     }
