@@ -1040,7 +1040,8 @@ void launch_ingest(int sk, int dk, const void* src, void* dst, uint64_t n, const
 // the device can load); each element is read once from each rank, summed in
 // rank order in fp32, scaled, stored once and tested once — the K1 pass over
 // the flat buffer disappears.  Streaming 128-bit loads; peers are read in
-// rank order with all kRsUnits units of a rank in flight together.
+// rank order, two ranks' units in flight together (rs_units(SK) 16- or
+// 32-byte units per thread per rank).
 template <int K>
 __device__ __forceinline__ void rs_load8(const void* base, uint64_t j, float (&x)[8]) {
     if constexpr (K == kF32) {
@@ -1056,6 +1057,39 @@ __device__ __forceinline__ void rs_load8(const void* base, uint64_t j, float (&x
             x[2 * k] = widen<K>(w[k] & 0xFFFFu);
             x[2 * k + 1] = widen<K>(w[k] >> 16);
         }
+    }
+}
+
+// Raw (still packed) unit: the loads of two ranks stay in flight in 2 x U
+// uint4 registers (16-bit kinds) and are widened as they are added.
+template <int K>
+struct RsRaw {
+    uint4 q[K == kF32 ? 2 : 1];
+};
+
+template <int K>
+__device__ __forceinline__ RsRaw<K> rs_raw(const void* base, uint64_t j) {
+    RsRaw<K> r;
+    if constexpr (K == kF32) {
+        const uint4* s = reinterpret_cast<const uint4*>(base) + 2 * j;
+        r.q[0] = __ldcs(s);
+        r.q[1] = __ldcs(s + 1);
+    } else {
+        r.q[0] = __ldcs(reinterpret_cast<const uint4*>(base) + j);
+    }
+    return r;
+}
+
+template <int K>
+__device__ __forceinline__ float rs_elem(const RsRaw<K>& r, int k) {
+    if constexpr (K == kF32) {
+        const uint4& q = r.q[k >> 2];
+        const uint32_t w = (k & 3) == 0 ? q.x : (k & 3) == 1 ? q.y : (k & 3) == 2 ? q.z : q.w;
+        return __uint_as_float(w);
+    } else {
+        const uint4& q = r.q[0];
+        const uint32_t w = (k >> 1) == 0 ? q.x : (k >> 1) == 1 ? q.y : (k >> 1) == 2 ? q.z : q.w;
+        return widen<K>((k & 1) ? (w >> 16) : (w & 0xFFFFu));
     }
 }
 
@@ -1110,8 +1144,8 @@ __device__ __forceinline__ bool rs_scalar(const RsArgs& a, uint64_t e) {
 }
 
 template <int SK, int DK>
-__global__ void __launch_bounds__(256) k4_reduce_check(RsArgs a) {
-    constexpr int U = kRsUnits;
+__global__ void __launch_bounds__(256, 3) k4_reduce_check(RsArgs a) {
+    constexpr int U = rs_units(SK);
     constexpr uint32_t kSrcBytes = SK == kF32 ? 4 : 2, kDstBytes = DK == kF32 ? 4 : 2;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t top = scan_word(DK).top;
@@ -1119,26 +1153,65 @@ __global__ void __launch_bounds__(256) k4_reduce_check(RsArgs a) {
     bool bad = false;
     if (blockIdx.x < a.tiles) {
         const uint64_t j0 = static_cast<uint64_t>(blockIdx.x) * U * blockDim.x + threadIdx.x;
+        const bool full = j0 + (U - 1) * static_cast<uint64_t>(blockDim.x) < a.nvec;
         float acc[U][8];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
-            if (j < a.nvec) {
-                rs_load8<SK>(static_cast<const uint8_t*>(a.src[0]) + a.head * kSrcBytes, j, acc[u]);
-            }
-        }
-        for (uint32_t r = 1; r < a.nsrc; ++r) {
-            const uint8_t* body = static_cast<const uint8_t*>(a.src[r]) + a.head * kSrcBytes;
-            float x[U][8];
+        uint32_t r;
+        {
+            // sources 0 and 1 together: acc = src0 (+ src1), the same
+            // roundings as starting from src0 and adding src1
+            const uint8_t* b0 = static_cast<const uint8_t*>(a.src[0]) + a.head * kSrcBytes;
+            const uint8_t* b1 = static_cast<const uint8_t*>(a.src[a.nsrc > 1 ? 1 : 0]) + a.head * kSrcBytes;
+            RsRaw<SK> x[U], y[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
-                if (j < a.nvec) rs_load8<SK>(body, j, x[u]);
+                if (full || j < a.nvec) {
+                    x[u] = rs_raw<SK>(b0, j);
+                    if (a.nsrc > 1) y[u] = rs_raw<SK>(b1, j);
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) acc[u][k] = __fadd_rn(acc[u][k], x[u][k]);
+                for (int k = 0; k < 8; ++k) {
+                    acc[u][k] = a.nsrc > 1 ? __fadd_rn(rs_elem<SK>(x[u], k), rs_elem<SK>(y[u], k))
+                                           : rs_elem<SK>(x[u], k);
+                }
+            }
+            r = a.nsrc > 1 ? 2 : 1;
+        }
+        for (; r + 1 < a.nsrc; r += 2) {
+            const uint8_t* b0 = static_cast<const uint8_t*>(a.src[r]) + a.head * kSrcBytes;
+            const uint8_t* b1 = static_cast<const uint8_t*>(a.src[r + 1]) + a.head * kSrcBytes;
+            RsRaw<SK> x[U], y[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
+                if (full || j < a.nvec) {
+                    x[u] = rs_raw<SK>(b0, j);
+                    y[u] = rs_raw<SK>(b1, j);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    acc[u][k] = __fadd_rn(__fadd_rn(acc[u][k], rs_elem<SK>(x[u], k)), rs_elem<SK>(y[u], k));
+                }
+            }
+        }
+        if (r < a.nsrc) {
+            const uint8_t* b0 = static_cast<const uint8_t*>(a.src[r]) + a.head * kSrcBytes;
+            RsRaw<SK> x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
+                if (full || j < a.nvec) x[u] = rs_raw<SK>(b0, j);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[u][k] = __fadd_rn(acc[u][k], rs_elem<SK>(x[u], k));
             }
         }
         uint8_t* dbody = static_cast<uint8_t*>(a.dst) + a.head * kDstBytes;

@@ -103,10 +103,10 @@ void launch_k3(int gk, const SegTable& tab, const AdamArgs& a, unsigned grid, cu
 // K4: gradient reduce-scatter with the overflow check in its epilogue
 // (SURVEY §8(f) row 2).  dst[i] = post_scale * sum_r src[r][i] (fp32, rank
 // order), stored in the stepper's gradient kind, non-finite test on the
-// stored value.  8-element units; one tile of kRsUnits x 256 units per CTA,
-// trailing CTAs for the scalar head/tail (or the whole range when the
+// stored value.  8-element units; one tile of rs_units(src kind) x 256 units
+// per CTA, trailing CTAs for the scalar head/tail (or the whole range when the
 // sources and dst cannot be co-aligned).
-constexpr int kRsUnits = 2;
+constexpr int rs_units(int sk) { return sk == kF32 ? 2 : 4; }
 struct RsArgs {
     const void* src[kMaxRanks];  // each source at the element `head` is measured from
     void* dst;
