@@ -1,0 +1,25 @@
+#!/bin/bash
+# Profiles for profiles/ (run on the GPU box from the repo root):
+#   launch list of the default bench (per-launch device time, cold/serialised)
+#   + one `ncu --set full` capture per hot kernel.
+# Summarise afterwards with tools/ncu_summary.py (see profiles/README.md).
+set -u
+TAG=${1:-r1}
+mkdir -p gpurun_out
+NCU="ncu --clock-control none"
+timeout 900 $NCU --metrics gpu__time_duration.sum --csv --log-file gpurun_out/${TAG}_launches_bench_default.csv \
+    python bench.py > gpurun_out/${TAG}_bench_under_ncu.log 2>&1
+echo "launch list rc=$?"
+FULL="$NCU --set full --import-source on -c 1"
+timeout 400 $FULL -k regex:k2_oneshot --launch-skip 3 -o gpurun_out/${TAG}_k2 \
+    python bench.py --params 268435456 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+echo "k2 rc=$?"
+timeout 400 $FULL -k regex:k1_oneshot --launch-skip 3 -o gpurun_out/${TAG}_k1 \
+    python bench.py --params 1000000000 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+echo "k1 rc=$?"
+timeout 400 $FULL -k regex:k3_adam --launch-skip 3 -o gpurun_out/${TAG}_k3 \
+    python tools/bench_k4.py --n 268435456 --reps 1 > /dev/null 2>&1
+echo "k3 rc=$?"
+timeout 400 $FULL -k regex:k4_reduce_check --launch-skip 12 -o gpurun_out/${TAG}_k4 \
+    python tools/bench_k4.py --n 134217728 --reps 1 > /dev/null 2>&1
+echo "k4 rc=$?"
