@@ -326,8 +326,13 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
 void launch_k3(const ma_subgroup* groups, uint32_t count, int gdt, const ma::AdamArgs& a,
                cudaStream_t st) {
     const DeviceInfo d = device_info();
-    constexpr int kVec = 4, kTile = ma::kK3Slots * ma::kK2Threads;
-    const uint64_t cap = static_cast<uint64_t>(d.sms) * ma::k3_blocks_per_sm(gdt);
+    static const int variant = [] {
+        const char* e = std::getenv("MA_K3_VARIANT");  // A/B only
+        return e ? std::atoi(e) : 0;
+    }();
+    constexpr int kVec = 4;
+    const int kTile = ma::k3_slots(gdt, variant) * ma::kK2Threads;
+    const uint64_t cap = static_cast<uint64_t>(d.sms) * ma::k3_blocks_per_sm(gdt, variant);
     for (uint32_t first = 0; first < count; first += ma::kMaxSegs) {
         ma::SegTable tab{};
         uint64_t tiles = 0, scalar_elems = 0;
@@ -345,7 +350,7 @@ void launch_k3(const ma_subgroup* groups, uint32_t count, int gdt, const ma::Ada
         if (tab.count == 0) continue;
         tab.total_tiles = tiles;
         const uint64_t grid = oneshot_grid(tab, kVec, scalar_elems, cap);
-        ma::launch_k3(gdt, tab, a, static_cast<unsigned>(grid), st);
+        ma::launch_k3(gdt, variant, tab, a, static_cast<unsigned>(grid), st);
         CK(cudaGetLastError());
     }
 }

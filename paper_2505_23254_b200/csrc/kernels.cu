@@ -838,14 +838,15 @@ struct Slot3 {
 };
 
 template <int GK>
-__device__ __forceinline__ void bf16_state_load(const Seg& sg, uint64_t e, Slot3& q) {
-    q.p = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.p) + e));
-    q.m = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.m) + e));
-    q.v = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.v) + e));
+__device__ __forceinline__ void bf16_state_load(const uint16_t* P, const uint16_t* M,
+                                                const uint16_t* V, const void* G, Slot3& q) {
+    q.p = __ldcs(reinterpret_cast<const uint2*>(P));
+    q.m = __ldcs(reinterpret_cast<const uint2*>(M));
+    q.v = __ldcs(reinterpret_cast<const uint2*>(V));
     if constexpr (GK == kF32) {
-        q.g = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(sg.g) + e));
+        q.g = __ldcs(reinterpret_cast<const uint4*>(G));
     } else {
-        const uint2 t = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(sg.g) + e));
+        const uint2 t = __ldcs(reinterpret_cast<const uint2*>(G));
         q.g = make_uint4(t.x, t.y, 0u, 0u);
     }
 }
@@ -889,12 +890,11 @@ __device__ __forceinline__ void bf16_state_update(uint16_t* P, uint16_t* M, uint
     __stcs(reinterpret_cast<uint2*>(V), pack4<false>(v));
 }
 
-template <int GK>
-__global__ void __launch_bounds__(kK2Threads) k3_adam_bf16(SegTable tab, AdamArgs a) {
+template <int GK, int U = kK3Slots, int MINB = 1>
+__global__ void __launch_bounds__(kK2Threads, MINB) k3_adam_bf16(SegTable tab, AdamArgs a) {
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
     const AdamConsts c = a.c;
-    constexpr int U = kK3Slots;
     // one tile per CTA (same one-shot grid as K2), then trailing CTAs
     const uint64_t t = blockIdx.x;
     if (t < tab.total_tiles) {
@@ -905,12 +905,16 @@ __global__ void __launch_bounds__(kK2Threads) k3_adam_bf16(SegTable tab, AdamArg
         uint16_t* P = reinterpret_cast<uint16_t*>(sg.p) + e0;
         uint16_t* M = reinterpret_cast<uint16_t*>(sg.m) + e0;
         uint16_t* V = reinterpret_cast<uint16_t*>(sg.v) + e0;
+        const uint8_t* G = static_cast<const uint8_t*>(sg.g) + e0 * (GK == kF32 ? 4 : 2);
         const uint64_t nv = sg.nvec;
         const bool full = (lt + 1) * (U * kK2Threads) <= nv;
         Slot3 q[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (full || j0 + u * kK2Threads < nv) bf16_state_load<GK>(sg, e0 + 4 * u * kK2Threads, q[u]);
+            if (full || j0 + u * kK2Threads < nv) {
+                const int o = 4 * u * kK2Threads;
+                bf16_state_load<GK>(P + o, M + o, V + o, G + o * (GK == kF32 ? 4 : 2), q[u]);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -1550,26 +1554,37 @@ void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs&
     });
 }
 
-int k3_blocks_per_sm(int gk) {
-    static int b[3] = {0, 0, 0};
-    if (b[gk] == 0) {
-        int x = 0;
-        if (gk == kF32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k3_adam_bf16<kF32>, kK2Threads, 0);
-        else if (gk == kBF16) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k3_adam_bf16<kBF16>, kK2Threads, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, k3_adam_bf16<kF16>, kK2Threads, 0);
-        b[gk] = x > 0 ? x : 1;
-    }
-    return b[gk];
+// K3 A/B (MA_K3_VARIANT): 0 = 4 slots held to 4 CTA/SM (64 regs,
+// production for bf16 gradients, 0.94), 1 = 4 slots unbounded (80 regs,
+// 3 CTA/SM, 0.90), 2 = 2 slots at 4 CTA/SM (0.84), 3 = 8 slots (0.89).
+int k3_slots(int gk, int variant) {
+    if (gk != kBF16) return kK3Slots;
+    return variant == 2 ? 2 : variant == 3 ? 8 : kK3Slots;
 }
 
-void launch_k3(int gk, const SegTable& tab, const AdamArgs& a, unsigned grid, cudaStream_t st) {
-    if (gk == kF32) {
-        k3_adam_bf16<kF32><<<grid, kK2Threads, 0, st>>>(tab, a);
-    } else if (gk == kBF16) {
-        k3_adam_bf16<kBF16><<<grid, kK2Threads, 0, st>>>(tab, a);
-    } else {
-        k3_adam_bf16<kF16><<<grid, kK2Threads, 0, st>>>(tab, a);
+template <typename F>
+void k3_dispatch(int gk, int variant, F&& f) {
+    if (gk == kF32) return f(k3_adam_bf16<kF32>);
+    if (gk == kF16) return f(k3_adam_bf16<kF16>);
+    switch (variant) {
+        case 1: return f(k3_adam_bf16<kBF16, 4, 1>);
+        case 2: return f(k3_adam_bf16<kBF16, 2, 4>);
+        case 3: return f(k3_adam_bf16<kBF16, 8, 1>);
+        default: return f(k3_adam_bf16<kBF16, 4, 4>);
     }
+}
+
+int k3_blocks_per_sm(int gk, int variant) {
+    int x = 0;
+    k3_dispatch(gk, variant, [&](auto fn) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, fn, kK2Threads, 0);
+    });
+    return x > 0 ? x : 1;
+}
+
+void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
+               cudaStream_t st) {
+    k3_dispatch(gk, variant, [&](auto fn) { fn<<<grid, kK2Threads, 0, st>>>(tab, a); });
 }
 
 void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s) {

@@ -98,8 +98,10 @@ void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs&
 // K3 (bf16 state): Seg p/m/v point at uint16 arrays; one tile of
 // kK3Slots x 256 slots of 4 elements per CTA, trailing CTAs for remainders.
 constexpr int kK3Slots = 4;
-int k3_blocks_per_sm(int gk);
-void launch_k3(int gk, const SegTable& tab, const AdamArgs& a, unsigned grid, cudaStream_t st);
+int k3_slots(int gk, int variant);
+int k3_blocks_per_sm(int gk, int variant);
+void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
+               cudaStream_t st);
 // K4: gradient reduce-scatter with the overflow check in its epilogue
 // (SURVEY §8(f) row 2).  dst[i] = post_scale * sum_r src[r][i] (fp32, rank
 // order), stored in the stepper's gradient kind, non-finite test on the
