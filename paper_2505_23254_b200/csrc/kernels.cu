@@ -1046,24 +1046,6 @@ void launch_ingest(int sk, int dk, const void* src, void* dst, uint64_t n, const
 // the flat buffer disappears.  Streaming 128-bit loads; peers are read in
 // rank order, two ranks' units in flight together (rs_units(SK) 16- or
 // 32-byte units per thread per rank).
-template <int K>
-__device__ __forceinline__ void rs_load8(const void* base, uint64_t j, float (&x)[8]) {
-    if constexpr (K == kF32) {
-        const float4* s = reinterpret_cast<const float4*>(base) + 2 * j;
-        const float4 a = __ldcs(s), b = __ldcs(s + 1);
-        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-        x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-    } else {
-        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(base) + j);
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            x[2 * k] = widen<K>(w[k] & 0xFFFFu);
-            x[2 * k + 1] = widen<K>(w[k] >> 16);
-        }
-    }
-}
-
 // Raw (still packed) unit: the loads of two ranks stay in flight in 2 x U
 // uint4 registers (16-bit kinds) and are widened as they are added.
 template <int K>
