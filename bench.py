@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 METRIC = "optimizer-step params/sec (overflow check+AdamW) and HBM GB/s vs B200 peak"
 LLAMA3_8B = 8_030_261_248       # proj/src/model.cpp:233
 QWEN25_14B = 14_770_033_664     # proj/src/model.cpp:239 (configs[3], sharded 8 ways)
+LLAMA3_70B = 70_553_706_496     # configs[4] (V 128256, H 8192, I 28672, L 80, kv 1024), 8 ways
 CFG1 = 67_108_864               # configs[0]: one 64M-param sub-group
 SUBGROUP = 100_000_000          # optimizer sub-group
 BYTES_PER_PARAM = 28            # 2 g + 12 pmv read + 12 pmv write + 2 w16
@@ -48,10 +49,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg4"], default="cfg2")
+    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg4", "cfg5"], default="cfg2")
     ap.add_argument("--slots", type=int, default=3, help="cfg4 staging slots")
     ap.add_argument("--slot-params", type=int, default=1 << 24, help="cfg4 params per slot")
     ap.add_argument("--params", type=int, default=0, help="override params per GPU (debug)")
+    ap.add_argument("--swap-dir", default="/tmp/memascend_swap",
+                    help="cfg5: directory of the swap store's file-backed devices")
+    ap.add_argument("--swap-gb", type=float, default=32.0,
+                    help="cfg5: optimizer state kept on the swap device (the rest in pinned DRAM)")
+    ap.add_argument("--host-slots", type=int, default=4, help="cfg5 registered host slots")
+    ap.add_argument("--io-workers", type=int, default=4, help="cfg5 swap-store workers")
+    ap.add_argument("--io-depth", type=int, default=16, help="cfg5 requests in flight per worker")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--flag-exchange", choices=["nccl", "p2p"], default="nccl",
                     help="N>1: all-reduce the skip flag with NCCL, or fuse the exchange into "
@@ -198,9 +206,13 @@ def workload_config(args, n, world):
     name = ("llama3-8b-optimizer-state-hbm" if args.config == "cfg2" and not args.params
             else "cfg1-64M-subgroup" if args.config == "cfg1" and not args.params
             else "qwen2.5-14b-shard-streamed-from-host" if args.config == "cfg4"
+            and not args.params
+            else "llama3-70b-shard-swapped-nvme+dram" if args.config == "cfg5"
             and not args.params else f"custom-{n}")
     state = ("fp32 master/m/v in the registered host pool, staged H2D/D2H"
-             if args.config == "cfg4" else "fp32 master/m/v in HBM")
+             if args.config == "cfg4" else
+             "fp32 master/m/v split between the O_DIRECT swap store and the registered host pool"
+             if args.config == "cfg5" else "fp32 master/m/v in HBM")
     return {"workload": name, "params_per_gpu": n, "subgroup_params": min(SUBGROUP, n),
             "grads": "bf16", "working_weights": "bf16", "state": state,
             "optimizer": "AdamW lr=1e-3 b1=0.9 b2=0.999 eps=1e-8 wd=0.01, loss scale 65536",
@@ -493,6 +505,187 @@ def ours_streamed(args, n, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def storage_peak(store_dir, io_workers, io_depth, nbytes=4 << 30):
+    """Measured O_DIRECT bandwidth of the swap device through the same engine
+    (one large key, write then read); returns (read GB/s, write GB/s)."""
+    import shutil
+
+    import paper_2505_23254_b200 as mab
+
+    d = os.path.join(store_dir, "peak")
+    devs = mab.DirectIoEngine.create_virtual_devices(d, 2, nbytes // 2 + (16 << 20))
+    buf = mab.aligned_host_buffer(nbytes)
+    buf[:] = 7
+    try:
+        with mab.DirectIoEngine(devs, workers=io_workers, queue_depth=io_depth) as e:
+            t0 = time.perf_counter()
+            e.write_tensor("peak", buf, nbytes)
+            t1 = time.perf_counter()
+            e.read_tensor("peak", buf)
+            t2 = time.perf_counter()
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    return nbytes / (t2 - t1) / 1e9, nbytes / (t1 - t0) / 1e9
+
+
+def ours_swapped(args, n, rank, world, local_rank):
+    """configs[4]: Llama-3-70B-shaped state sharded 8 ways (8.82 B params per
+    GPU).  fp32 master/m/v of `--swap-gb` worth of 100 M sub-groups live in
+    the O_DIRECT swap store (memascend DirectIoEngine drop-in, io_uring
+    backend, file-backed devices under --swap-dir), the rest in the
+    registered host pool; grads and working weights in HBM.
+    ma_stepper_apply_swapped reads swapped groups into registered host slots
+    ahead of use, streams every group H2D -> K2 -> D2H and writes swapped
+    groups back from a writer thread.  Bound: the swap device (24 B per
+    swapped param) and the host link (24 B per param)."""
+    import shutil
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_23254_b200 as mab
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    sub = min(SUBGROUP, n)
+    tb = (sub * 4 + 4095) // 4096 * 4096
+    offs = list(range(0, n, sub))
+    G = len(offs)
+    S = min(G, int(args.swap_gb * 1e9 // (3 * tb)))
+    swapped = set(int(i * G / S) for i in range(S)) if S else set()
+    base = rank * n
+    sdir = os.path.join(args.swap_dir, f"rank{rank}")
+    shutil.rmtree(sdir, ignore_errors=True)
+    per_dev = ((3 * tb * len(swapped)) // 2 + (64 << 20)) // 4096 * 4096
+    devs = mab.DirectIoEngine.create_virtual_devices(sdir, 2, per_dev) if swapped else []
+    store = (mab.DirectIoEngine(devs, workers=args.io_workers, queue_depth=args.io_depth)
+             if swapped else None)
+    host_ids = [k for k in range(G) if k not in swapped]
+    n_host = sum(min(sub, n - offs[k]) for k in host_ids)
+    pool = {}
+    for name in ("p", "m", "v"):  # the DRAM tier: one registered region per tensor
+        buf = mab.aligned_host_buffer(max(4, n_host * 4), register=True)
+        pool[name] = buf.view(np.float32)
+    pool["m"][:] = 0
+    pool["v"][:] = 0
+    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    hslots = args.host_slots
+    hstage = mab.aligned_host_buffer(hslots * 3 * tb, register=True)
+    dstage = torch.empty(3 * args.slots * sub, dtype=torch.float32, device=dev)
+    tmp = torch.empty(sub, dtype=torch.float32, device=dev)
+    zeros = mab.aligned_host_buffer(tb)
+    zeros[:] = 0
+    groups = []
+    at = 0
+    t_init = time.perf_counter()
+    for k, o in enumerate(offs):
+        ln = min(sub, n - o)
+        mab.gen_seeded_weights(tmp[:ln], w[o:o + ln], base=base + o, seed=1)
+        if k in swapped:
+            pslot = hstage[:tb].view(np.float32)
+            pslot[:ln] = tmp[:ln].cpu().numpy()
+            keys = tuple(f"{t}.g{k}" for t in ("master", "m", "v"))
+            store.write_tensor(keys[0], hstage[:tb], ln * 4)
+            store.write_tensor(keys[1], zeros, ln * 4)
+            store.write_tensor(keys[2], zeros, ln * 4)
+            groups.append((keys, g[o:o + ln], w[o:o + ln]))
+        else:
+            pool["p"][at:at + ln] = tmp[:ln].cpu().numpy()
+            groups.append(((pool["p"][at:at + ln], pool["m"][at:at + ln],
+                            pool["v"][at:at + ln]), g[o:o + ln], w[o:o + ln]))
+            at += ln
+    del tmp
+    t_init = time.perf_counter() - t_init
+    mab.gen_pseudo_grads(g, w, step=0, base=base, seed=1, scale=65536.0)
+    st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "bf16", device=dev)
+    stream = torch.cuda.current_stream(dev)
+    io0 = {}
+
+    def one_step():
+        st.check(g)
+        if world > 1:
+            dist.all_reduce(st.flag, op=dist.ReduceOp.MAX)
+        st.apply_swapped(store, groups, hstage, hslots, dstage, args.slots, sub)
+        st.finish()
+
+    try:
+        for _ in range(args.warmup):
+            one_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        io0 = store.stats() if store else {}
+        with ClockSampler(local_rank) as clk:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                one_step()
+            b.record(stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+        io1 = store.stats() if store else {}
+        ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms = float(ms.item())
+        backend = store.backend if store else None
+        if store:
+            store.close()
+    finally:
+        shutil.rmtree(sdir, ignore_errors=True)
+    if rank != 0:
+        return
+    rd, wr = storage_peak(args.swap_dir, args.io_workers, args.io_depth)
+    io_bytes = ((io1.get("bytes_read", 0) - io0.get("bytes_read", 0)) +
+                (io1.get("bytes_written", 0) - io0.get("bytes_written", 0))) / args.steps
+    n_sw = n - n_host
+    storage_gbs = io_bytes / (ms / 1e3) / 1e9
+    # equal bytes read and written on one device: the serial combination bounds it
+    storage_peak_gbs = 2 / (1 / rd + 1 / wr)
+    line = {
+        "metric": METRIC, "value": n * world / (ms / 1e3), "unit": "params/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference generators seeded_weight/pseudo_gradient)",
+        "config": dict(workload_config(args, n, world), swapped_params=n_sw,
+                       dram_params=n_host, swapped_groups=len(swapped), groups=G,
+                       host_slots=hslots, dev_slots=args.slots, io_backend=backend,
+                       io_workers=args.io_workers, io_depth=args.io_depth),
+        "storage": {"bound": "swap-device", "achieved": storage_gbs, "unit": "GB/s",
+                    "peak": storage_peak_gbs, "frac": storage_gbs / storage_peak_gbs,
+                    "bytes_per_step": io_bytes, "bytes_per_swapped_param": 24,
+                    "peak_read_gbs": rd, "peak_write_gbs": wr,
+                    "peak_source": "measured O_DIRECT 4 GiB write then read through the engine"},
+        "host_link": {"achieved": 24 * n / (ms / 1e3) / 1e9, "unit": "GB/s",
+                      "bytes_per_param": 24},
+        "init_seconds": t_init,
+        "gpu_launches": (1 + G + 1) * args.steps,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as ora
+
+        k = 2
+        gs = np.random.default_rng(0).standard_normal(k * sub).astype(np.float32) * 8192
+        rdir = os.path.join(args.swap_dir, "ref")
+        try:
+            secs, rio = ora.ref_swap_bench(rdir, 2, sub, k, 2, 1, gs, ora.hyper(**HYPER), 65536.0,
+                                           os.cpu_count() or 1)
+        finally:
+            shutil.rmtree(rdir, ignore_errors=True)
+        line["cpu_baseline"] = {
+            "value": k * sub / secs, "unit": "params/s", "cores": os.cpu_count() or 1,
+            "kind": "reference",
+            "sample": f"{k} swapped groups of {sub} params: the reference DirectIoEngine "
+                      "read master/m/v -> adam_step_fp32 -> write back (simulator.cpp:453-469), "
+                      "median of 2 steps after 1 warm-up; its storage rate "
+                      f"{rio / secs / 1e9:.2f} GB/s"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -502,8 +695,8 @@ def main():
     # MA_BENCH_DEVICE, collectives over MA_BENCH_BACKEND (gloo); default nccl
     local_rank = int(os.environ.get("MA_BENCH_DEVICE", local_rank))
     backend = os.environ.get("MA_BENCH_BACKEND", "nccl")
-    n = args.params or {"cfg2": LLAMA3_8B, "cfg1": CFG1,
-                        "cfg4": (QWEN25_14B + 7) // 8}[args.config]
+    n = args.params or {"cfg2": LLAMA3_8B, "cfg1": CFG1, "cfg4": (QWEN25_14B + 7) // 8,
+                        "cfg5": (LLAMA3_70B + 7) // 8}[args.config]
     if args.impl == "reference":
         reference_arm(args, n, rank, world)
         return
@@ -519,6 +712,8 @@ def main():
     try:
         if args.config == "cfg4":
             ours_streamed(args, n, rank, world, local_rank)
+        elif args.config == "cfg5":
+            ours_swapped(args, n, rank, world, local_rank)
         else:
             ours(args, n, rank, world, local_rank)
     finally:

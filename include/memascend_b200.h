@@ -292,6 +292,114 @@ MA_API int ma_host_unregister(void* ptr);
 MA_API int ma_pointer_kind(const void* ptr, int* kind);
 
 /* ------------------------------------------------------------------ */
+/* Swap store (DirectIoEngine, proj/include/memascend/direct_io.hpp:23-180,
+ * proj/src/direct_io.cpp): key-addressed tensors on raw or file-backed
+ * devices opened with O_DIRECT, payloads padded to 4096 and striped in equal
+ * granule counts across the devices, space claimed once per key (growth
+ * abandons the old extents), a per-key busy guard (MA_ERR_BUSY), a JSON
+ * manifest.  Host-side by design (north star item 4): these entry points do
+ * file I/O only and need no GPU.  Backends: MA_IO_SYNC (pread/pwrite),
+ * MA_IO_POSIX_AIO (lio_listio, the reference's), MA_IO_URING (new: one
+ * io_uring per worker, queue_depth requests in flight across tasks);
+ * MA_IO_AUTO picks io_uring when the kernel allows it, else POSIX AIO
+ * (env MEMASCEND_IO_BACKEND=sync|aio|uring overrides). */
+typedef struct ma_swap ma_swap;
+typedef struct ma_swap_op ma_swap_op;
+enum ma_io_backend { MA_IO_AUTO = 0, MA_IO_SYNC = 1, MA_IO_POSIX_AIO = 2, MA_IO_URING = 3 };
+typedef struct ma_swap_device {
+    const char* path;
+    uint64_t capacity_bytes; /* positive multiple of 4096 */
+    int kind;                /* 0 raw_block, 1 file_backed_virtual */
+} ma_swap_device;
+typedef struct ma_swap_config {
+    uint32_t workers;     /* >= 1 (reference default 2) */
+    uint32_t queue_depth; /* requests in flight per worker (reference default 8) */
+    int backend;          /* ma_io_backend */
+    int cache_bypass;     /* open with O_DIRECT */
+    const char* manifest_path; /* NULL/"" = volatile table */
+} ma_swap_config;
+typedef struct ma_swap_extent {
+    uint32_t device_index;
+    uint64_t device_offset;
+    uint64_t length;
+} ma_swap_extent;
+typedef struct ma_swap_stats {
+    uint64_t bytes_written, bytes_read, write_requests, read_requests, submitted_ios,
+        abandoned_bytes;
+} ma_swap_stats;
+typedef void (*ma_io_trace_fn)(void* user, uint32_t device, uint64_t offset, uint64_t length,
+                               int write);
+MA_API int ma_swap_create(const ma_swap_device* devs, uint32_t ndev, const ma_swap_config* cfg,
+                          ma_swap** out);
+MA_API int ma_swap_destroy(ma_swap* s); /* saves the manifest when configured */
+/* allocate_extents: *count = number of extents (at most cap copied to out). */
+MA_API int ma_swap_allocate(ma_swap* s, const char* key, uint64_t logical_bytes,
+                            ma_swap_extent* out, uint32_t cap, uint32_t* count);
+/* src/dst must be 4096-aligned and cover the padded length.  The _async
+ * forms return an op to pass to ma_swap_wait (which frees it); the key stays
+ * busy until then. */
+MA_API int ma_swap_write(ma_swap* s, const char* key, const void* src, uint64_t src_bytes,
+                         uint64_t logical_bytes);
+MA_API int ma_swap_read(ma_swap* s, const char* key, void* dst, uint64_t dst_bytes,
+                        uint64_t* logical_bytes);
+MA_API int ma_swap_write_async(ma_swap* s, const char* key, const void* src, uint64_t src_bytes,
+                               uint64_t logical_bytes, ma_swap_op** op);
+MA_API int ma_swap_read_async(ma_swap* s, const char* key, void* dst, uint64_t dst_bytes,
+                              ma_swap_op** op);
+MA_API int ma_swap_wait(ma_swap_op* op, uint64_t* logical_bytes);
+MA_API int ma_swap_contains(ma_swap* s, const char* key, int* out);
+MA_API int ma_swap_location(ma_swap* s, const char* key, uint64_t* logical, uint64_t* padded,
+                            ma_swap_extent* out, uint32_t cap, uint32_t* count);
+/* All keys, sorted, NUL-separated; *needed = bytes required. */
+MA_API int ma_swap_keys(ma_swap* s, char* buf, uint64_t cap, uint64_t* needed);
+MA_API int ma_swap_get_stats(ma_swap* s, ma_swap_stats* out);
+MA_API int ma_swap_info(ma_swap* s, int* backend, uint64_t* total_capacity,
+                        uint32_t* device_count);
+MA_API int ma_swap_set_trace(ma_swap* s, ma_io_trace_fn fn, void* user);
+MA_API int ma_swap_save_manifest(ma_swap* s);
+/* dir/vdev<i>.img, i < count, each `bytes` long (preallocated). */
+MA_API int ma_swap_create_virtual_devices(const char* dir, uint32_t count, uint64_t bytes);
+MA_API int ma_swap_uring_available(void);
+/* SharedCursor (direct_io.hpp:69-92): per-device next-free offsets; with a
+ * path the counters live in that file under flock (cross-process). */
+typedef struct ma_cursor ma_cursor;
+MA_API int ma_cursor_open(uint32_t devices, const char* path, ma_cursor** out);
+MA_API int ma_cursor_close(ma_cursor* c);
+MA_API int ma_cursor_advance(ma_cursor* c, uint32_t device, uint64_t bytes, uint64_t* old);
+MA_API int ma_cursor_position(ma_cursor* c, uint32_t device, uint64_t* pos);
+MA_API int ma_cursor_restore(ma_cursor* c, uint32_t device, uint64_t pos);
+
+/* Swapped update (config 5: state on NVMe, simulator.cpp:453-469's
+ * read master/m/v -> adam_step_fp32 -> write back, as a pipeline).  For a
+ * group with keys, its fp32 master/m/v live in the swap store under
+ * key_p/key_m/key_v (n <= slot_elems); for a group with NULL keys they live
+ * in registered host memory at p/m/v (the DRAM tier).  g/w are on the
+ * device.  Swapped groups are read into one of host_slots registered host
+ * slots (h_staging, 4096-aligned, host_slots x 3 x align4096(4*slot_elems)
+ * bytes) up to host_slots-1 groups ahead, copied into one of dev_slots
+ * device slots (d_staging, dev_slots x 3 x slot_elems floats), updated by K2
+ * on `stream`, copied back and written to the store by a writer thread
+ * while later groups are read and updated.  A skipped step moves nothing
+ * (*skipped = 1).  Returns when every swapped group is back in the store;
+ * host-resident write-backs are ordered before `stream`. */
+typedef struct ma_swap_group {
+    const char* key_p;
+    const char* key_m;
+    const char* key_v;
+    float* p;
+    float* m;
+    float* v;
+    const void* g;
+    void* w;
+    uint64_t n;
+} ma_swap_group;
+MA_API int ma_stepper_apply_swapped(ma_stepper* s, ma_swap* e, const ma_swap_group* groups,
+                                    uint32_t count, void* h_staging, uint32_t host_slots,
+                                    float* d_staging, uint32_t dev_slots, uint64_t slot_elems,
+                                    void* stream, void* h2d_stream, void* d2h_stream,
+                                    int* skipped);
+
+/* ------------------------------------------------------------------ */
 /* Verification hooks (used by tests/; they run the product device code). */
 /* FNV-1a-64 of every 2^block_log2 consecutive fp32->kind conversions over
  * all 2^32 inputs, through the same device cast K2 uses; out_host has

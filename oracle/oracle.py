@@ -321,6 +321,9 @@ def ref():
                                                         C.c_uint64, C.c_void_p, C.c_float,
                                                         C.c_uint32, C.POINTER(C.c_int),
                                                         C.POINTER(C.c_double)]
+        R.ref_swap_bench.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
+                                     C.c_uint32, C.c_void_p, C.c_void_p, C.c_float, C.c_uint32,
+                                     C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         R.ref_fp16_from_float.restype = C.c_uint16
         R.ref_fp16_from_float.argtypes = [C.c_float]
         R.ref_bf16_from_float.restype = C.c_uint16
@@ -353,6 +356,21 @@ def ref_fused_overflow_check(g, workers=1, chunk_bytes=1 << 20, early_exit=True,
     if r:
         raise ValueError(ref().ref_last_error().decode())
     return bool(of.value), (first.value if of.value and track else None)
+
+
+def ref_swap_bench(directory, devices, group_elems, groups, steps, warmup, g, h: Hyper, scale,
+                   workers, io_workers=2):
+    """The reference's swapped step (DirectIoEngine read -> adam_step_fp32 ->
+    write, simulator.cpp:453-469) on `groups` groups stored in `directory`;
+    returns (median seconds per step, storage bytes moved per step)."""
+    hv = ref_hyper_array(h)
+    secs, io = C.c_double(), C.c_double()
+    r = ref().ref_swap_bench(directory.encode(), devices, group_elems, groups, steps, warmup,
+                             _ptr(g), _ptr(hv), scale, workers, io_workers, C.byref(secs),
+                             C.byref(io))
+    if r:
+        raise ValueError(ref().ref_last_error().decode())
+    return secs.value, io.value
 
 
 def ref_bench_step(g, p, m, v, w, w_kind, subgroup, t, h: Hyper, scale, workers):

@@ -5,7 +5,9 @@
 // oracle/_ref/libmemascend_ref.so.  Loaded via ctypes by tests/ (to pin the
 // restatement in memascend_oracle.c) and by bench.py's reference arm /
 // cpu_baseline leg (the reference's own CPU path, timed on the host cores).
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -14,6 +16,7 @@
 #include <thread>
 #include <vector>
 
+#include "memascend/direct_io.hpp"
 #include "memascend/error.hpp"
 #include "memascend/halfprec.hpp"
 #include "memascend/model.hpp"
@@ -222,6 +225,77 @@ int ref_bench_step(const float* g, float* p, float* m, float* v, std::uint16_t* 
             }
         }
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+// The reference's swapped optimizer step (configs[4]; simulator.cpp:453-469,
+// mixed branch): per group read master/m/v from its DirectIoEngine,
+// adam_step_fp32, write master/m/v back, refresh the working weights.  The
+// store lives in `dir` (file-backed virtual devices, O_DIRECT); `groups`
+// groups of `group_elems` are initialised (seeded weights, zero moments) and
+// then `warmup + steps` steps run with fixed gradients.  workers > 1 splits
+// Adam and the cast (the reference's simulator passes workers = 1).
+// *seconds = median wall seconds per step; *io_bytes = bytes moved per step.
+int ref_swap_bench(const char* dir, std::uint32_t devices, std::uint64_t group_elems,
+                   std::uint32_t groups, std::uint32_t steps, std::uint32_t warmup,
+                   const float* g, const float* hyper, float scale, std::uint32_t workers,
+                   std::uint32_t io_workers, double* seconds, double* io_bytes) {
+    return guarded([&] {
+        const std::uint64_t tbytes = (group_elems * 4 + 4095) / 4096 * 4096;
+        const std::uint64_t per_dev =
+            ((3 * tbytes * groups) / devices + (16u << 20)) / 4096 * 4096;
+        auto devset = DirectIoEngine::create_virtual_devices(dir, devices, per_dev);
+        EngineConfig cfg;
+        cfg.workers = io_workers;
+        DirectIoEngine engine(devset, cfg);
+        auto alloc = [&](std::uint64_t b) {
+            return static_cast<float*>(std::aligned_alloc(4096, b));
+        };
+        float* master = alloc(tbytes);
+        float* m = alloc(tbytes);
+        float* v = alloc(tbytes);
+        std::vector<std::uint16_t> w16(group_elems);
+        auto bytes = [&](float* p) { return std::span<std::byte>(reinterpret_cast<std::byte*>(p), tbytes); };
+        for (std::uint32_t k = 0; k < groups; ++k) {
+            for (std::uint64_t i = 0; i < group_elems; ++i)
+                master[i] = seeded_weight(1, k * group_elems + i);
+            std::memset(m, 0, tbytes);
+            engine.write_tensor("master.g" + std::to_string(k), bytes(master), group_elems * 4);
+            engine.write_tensor("m.g" + std::to_string(k), bytes(m), group_elems * 4);
+            engine.write_tensor("v.g" + std::to_string(k), bytes(m), group_elems * 4);
+        }
+        const AdamHyper h = to_hyper(hyper);
+        std::vector<double> times;
+        const auto io0 = engine.stats();
+        for (std::uint32_t s = 0; s < warmup + steps; ++s) {
+            const auto t0 = std::chrono::steady_clock::now();
+            for (std::uint32_t k = 0; k < groups; ++k) {
+                const std::string id = "g" + std::to_string(k);
+                engine.read_tensor("m." + id, bytes(m));
+                engine.read_tensor("v." + id, bytes(v));
+                engine.read_tensor("master." + id, bytes(master));
+                adam_step_fp32({master, group_elems}, {m, group_elems}, {v, group_elems},
+                               {g + k * group_elems, group_elems}, s + 1, h, scale, workers);
+                engine.write_tensor("master." + id, bytes(master), group_elems * 4);
+                engine.write_tensor("m." + id, bytes(m), group_elems * 4);
+                engine.write_tensor("v." + id, bytes(v), group_elems * 4);
+                parallel_slices(group_elems, workers, [&](std::uint64_t b, std::uint64_t e) {
+                    for (std::uint64_t i = b; i < e; ++i) w16[i] = bf16_from_float(master[i]);
+                });
+            }
+            if (s >= warmup)
+                times.push_back(
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        }
+        const auto io1 = engine.stats();
+        std::sort(times.begin(), times.end());
+        *seconds = times[times.size() / 2];
+        *io_bytes = static_cast<double>((io1.bytes_read - io0.bytes_read) +
+                                        (io1.bytes_written - io0.bytes_written)) /
+                    (warmup + steps);
+        std::free(master);
+        std::free(m);
+        std::free(v);
     });
 }
 

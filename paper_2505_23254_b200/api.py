@@ -263,6 +263,41 @@ class Stepper:
             _stream_ptr(h2d_stream), _stream_ptr(d2h_stream), C.byref(skipped)))
         return bool(skipped.value)
 
+    def apply_swapped(self, store: "DirectIoEngine", groups, host_staging, host_slots,
+                      dev_staging, dev_slots, slot_elems, stream=None, h2d_stream=None,
+                      d2h_stream=None) -> bool:
+        """Config 5: groups are (keys, g, w) with keys = (key_p, key_m, key_v)
+        of the fp32 master/m/v in `store`, or ((p, m, v), g, w) with p/m/v in
+        registered host memory.  host_staging: registered, 4096-aligned host
+        buffer of host_slots x 3 x align4096(4 * slot_elems) bytes;
+        dev_staging: device fp32 tensor of 3 * dev_slots * slot_elems.
+        Returns True when the step was skipped (nothing read or written)."""
+        arr = (capi.SwapGroup * len(groups))()
+        keep = []
+        for k, (state, g, w) in enumerate(groups):
+            n = g.numel()
+            if isinstance(state[0], str):
+                keys = [x.encode() for x in state]
+                keep.append(keys)
+                arr[k] = capi.SwapGroup(keys[0], keys[1], keys[2], None, None, None,
+                                        g.data_ptr(), w.data_ptr() if w is not None else None, n)
+            else:
+                p, m, v = (_raw(x)[0] for x in state)
+                arr[k] = capi.SwapGroup(None, None, None, p, m, v, g.data_ptr(),
+                                        w.data_ptr() if w is not None else None, n)
+        if h2d_stream is None:
+            self._h2d = getattr(self, "_h2d", None) or torch.cuda.Stream(device=dev_staging.device)
+            h2d_stream = self._h2d
+        if d2h_stream is None:
+            self._d2h = getattr(self, "_d2h", None) or torch.cuda.Stream(device=dev_staging.device)
+            d2h_stream = self._d2h
+        skipped = C.c_int()
+        check(capi.lib().ma_stepper_apply_swapped(
+            self._h, store.handle, arr, len(arr), _raw(host_staging)[0], host_slots,
+            dev_staging.data_ptr(), dev_slots, slot_elems, _stream_ptr(stream),
+            _stream_ptr(h2d_stream), _stream_ptr(d2h_stream), C.byref(skipped)))
+        return bool(skipped.value)
+
     def finish(self, stream=None):
         check(capi.lib().ma_stepper_finish_async(self._h, _stream_ptr(stream)))
 
@@ -391,6 +426,149 @@ def gen_pseudo_grads(g, w, step, base=0, seed=1, scale=65536.0, d_scale=None, g_
 def plant_bits(buf, index, bits, kind=None, stream=None):
     bp, _, dt = _info(buf, kind)
     check(capi.lib().ma_plant_bits_async(bp, dt, index, bits, _stream_ptr(stream)))
+
+
+# ----------------------------------------------------------------- swap store
+class DirectIoEngine:
+    """DirectIoEngine (proj/include/memascend/direct_io.hpp:94-178) over
+    ma_swap_*: key-addressed O_DIRECT tensor store striped over devices.
+    devices: list of (path, capacity_bytes[, kind]) or create_virtual_devices'
+    result; backend "auto" | "sync" | "aio" | "uring"."""
+
+    def __init__(self, devices, workers=2, queue_depth=8, backend="auto", cache_bypass=True,
+                 manifest_path=None):
+        devs = (capi.SwapDevice * max(1, len(devices)))()
+        self._paths = [d[0].encode() for d in devices]
+        for i, d in enumerate(devices):
+            devs[i] = capi.SwapDevice(self._paths[i], d[1], d[2] if len(d) > 2 else 1)
+        cfg = capi.SwapConfig(workers, queue_depth, capi.IO_BACKENDS[backend],
+                              1 if cache_bypass else 0,
+                              manifest_path.encode() if manifest_path else None)
+        h = C.c_void_p()
+        check(capi.lib().ma_swap_create(devs, len(devices), C.byref(cfg), C.byref(h)))
+        self.handle = h.value
+        self._trace = None
+
+    def close(self):
+        if getattr(self, "handle", None):
+            check(capi.lib().ma_swap_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @staticmethod
+    def create_virtual_devices(directory: str, count: int, nbytes: int):
+        check(capi.lib().ma_swap_create_virtual_devices(directory.encode(), count, nbytes))
+        return [(f"{directory}/vdev{d}.img", nbytes, 1) for d in range(count)]
+
+    @property
+    def backend(self) -> str:
+        b = C.c_int()
+        check(capi.lib().ma_swap_info(self.handle, C.byref(b), None, None))
+        return {v: k for k, v in capi.IO_BACKENDS.items()}[b.value]
+
+    @property
+    def total_capacity(self) -> int:
+        t = C.c_uint64()
+        check(capi.lib().ma_swap_info(self.handle, None, C.byref(t), None))
+        return t.value
+
+    def allocate_extents(self, key: str, logical: int):
+        ext = (capi.SwapExtent * 64)()
+        n = C.c_uint32()
+        check(capi.lib().ma_swap_allocate(self.handle, key.encode(), logical, ext, 64,
+                                          C.byref(n)))
+        return [(e.device_index, e.device_offset, e.length) for e in ext[:n.value]]
+
+    def write_tensor(self, key: str, src, logical: int) -> None:
+        ptr, nbytes = _raw(src)
+        check(capi.lib().ma_swap_write(self.handle, key.encode(), ptr, nbytes, logical))
+
+    def read_tensor(self, key: str, dst) -> int:
+        ptr, nbytes = _raw(dst)
+        out = C.c_uint64()
+        check(capi.lib().ma_swap_read(self.handle, key.encode(), ptr, nbytes, C.byref(out)))
+        return out.value
+
+    def write_tensor_async(self, key: str, src, logical: int) -> "SwapOp":
+        ptr, nbytes = _raw(src)
+        op = C.c_void_p()
+        check(capi.lib().ma_swap_write_async(self.handle, key.encode(), ptr, nbytes, logical,
+                                             C.byref(op)))
+        return SwapOp(op.value, src)
+
+    def read_tensor_async(self, key: str, dst) -> "SwapOp":
+        ptr, nbytes = _raw(dst)
+        op = C.c_void_p()
+        check(capi.lib().ma_swap_read_async(self.handle, key.encode(), ptr, nbytes, C.byref(op)))
+        return SwapOp(op.value, dst)
+
+    def contains(self, key: str) -> bool:
+        r = C.c_int()
+        check(capi.lib().ma_swap_contains(self.handle, key.encode(), C.byref(r)))
+        return bool(r.value)
+
+    def location(self, key: str) -> dict:
+        lg, pd, n = C.c_uint64(), C.c_uint64(), C.c_uint32()
+        ext = (capi.SwapExtent * 64)()
+        check(capi.lib().ma_swap_location(self.handle, key.encode(), C.byref(lg), C.byref(pd),
+                                          ext, 64, C.byref(n)))
+        return {"logical": lg.value, "padded": pd.value,
+                "extents": [(e.device_index, e.device_offset, e.length) for e in ext[:n.value]]}
+
+    def stats(self) -> dict:
+        st = capi.SwapStats()
+        check(capi.lib().ma_swap_get_stats(self.handle, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in capi.SwapStats._fields_}
+
+    def set_io_trace(self, fn) -> None:
+        """fn(device, offset, length, write) per device-level submission."""
+        self._trace = capi.IO_TRACE_FN(lambda _u, d, o, n, w: fn(d, o, n, bool(w))) if fn else None
+        check(capi.lib().ma_swap_set_trace(self.handle, self._trace or capi.IO_TRACE_FN(), None))
+
+    def save_manifest(self) -> None:
+        check(capi.lib().ma_swap_save_manifest(self.handle))
+
+
+class SwapOp:
+    """An in-flight store operation; wait() returns the logical length and
+    raises the op's error.  The key stays busy until then."""
+
+    def __init__(self, handle, buf):
+        self._h, self._buf = handle, buf
+
+    def wait(self) -> int:
+        if self._h is None:
+            raise MemAscendError(4, "operation already waited on")
+        out = C.c_uint64()
+        h, self._h = self._h, None
+        check(capi.lib().ma_swap_wait(h, C.byref(out)))
+        return out.value
+
+
+def uring_available() -> bool:
+    return bool(capi.lib().ma_swap_uring_available())
+
+
+def aligned_host_buffer(nbytes: int, register: bool = False) -> np.ndarray:
+    """A 4096-aligned uint8 host array (the swap store's O_DIRECT buffers),
+    optionally registered for DMA (PinnedAllocator's registered state)."""
+    raw = np.empty(nbytes + 4096, np.uint8)
+    off = (-raw.ctypes.data) % 4096
+    buf = raw[off:off + nbytes]
+    if register:
+        host_register(buf)
+    return buf
 
 
 # ----------------------------------------------------------------- host memory

@@ -67,6 +67,35 @@ class StepState(C.Structure):
                 ("growth_interval", C.c_uint32)]
 
 
+class SwapDevice(C.Structure):
+    _fields_ = [("path", C.c_char_p), ("capacity_bytes", C.c_uint64), ("kind", C.c_int)]
+
+
+class SwapConfig(C.Structure):
+    _fields_ = [("workers", C.c_uint32), ("queue_depth", C.c_uint32), ("backend", C.c_int),
+                ("cache_bypass", C.c_int), ("manifest_path", C.c_char_p)]
+
+
+class SwapExtent(C.Structure):
+    _fields_ = [("device_index", C.c_uint32), ("device_offset", C.c_uint64),
+                ("length", C.c_uint64)]
+
+
+class SwapStats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("bytes_written", "bytes_read", "write_requests",
+                                          "read_requests", "submitted_ios", "abandoned_bytes")]
+
+
+class SwapGroup(C.Structure):
+    _fields_ = [("key_p", C.c_char_p), ("key_m", C.c_char_p), ("key_v", C.c_char_p),
+                ("p", C.c_void_p), ("m", C.c_void_p), ("v", C.c_void_p), ("g", C.c_void_p),
+                ("w", C.c_void_p), ("n", C.c_uint64)]
+
+
+IO_AUTO, IO_SYNC, IO_POSIX_AIO, IO_URING = 0, 1, 2, 3
+IO_BACKENDS = {"auto": IO_AUTO, "sync": IO_SYNC, "aio": IO_POSIX_AIO, "uring": IO_URING}
+IO_TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int)
+
 # (name, restype, argtypes) for every symbol the header declares
 _VP, _U64, _I, _U32, _F = C.c_void_p, C.c_uint64, C.c_int, C.c_uint32, C.c_float
 SIGNATURES = [
@@ -108,6 +137,32 @@ SIGNATURES = [
     ("ma_gen_seeded_weights_async", _I, [_VP, _VP, _I, _U64, _U64, _U64, _VP]),
     ("ma_gen_pseudo_grads_async", _I, [_VP, _I, _VP, _I, _U64, _U64, _U64, _U64, _VP, _F, _VP]),
     ("ma_plant_bits_async", _I, [_VP, _I, _U64, _U32, _VP]),
+    ("ma_swap_create", _I, [C.POINTER(SwapDevice), _U32, C.POINTER(SwapConfig), C.POINTER(_VP)]),
+    ("ma_swap_destroy", _I, [_VP]),
+    ("ma_swap_allocate", _I, [_VP, C.c_char_p, _U64, C.POINTER(SwapExtent), _U32,
+                              C.POINTER(_U32)]),
+    ("ma_swap_write", _I, [_VP, C.c_char_p, _VP, _U64, _U64]),
+    ("ma_swap_read", _I, [_VP, C.c_char_p, _VP, _U64, C.POINTER(_U64)]),
+    ("ma_swap_write_async", _I, [_VP, C.c_char_p, _VP, _U64, _U64, C.POINTER(_VP)]),
+    ("ma_swap_read_async", _I, [_VP, C.c_char_p, _VP, _U64, C.POINTER(_VP)]),
+    ("ma_swap_wait", _I, [_VP, C.POINTER(_U64)]),
+    ("ma_swap_contains", _I, [_VP, C.c_char_p, C.POINTER(_I)]),
+    ("ma_swap_location", _I, [_VP, C.c_char_p, C.POINTER(_U64), C.POINTER(_U64),
+                              C.POINTER(SwapExtent), _U32, C.POINTER(_U32)]),
+    ("ma_swap_keys", _I, [_VP, _VP, _U64, C.POINTER(_U64)]),
+    ("ma_swap_get_stats", _I, [_VP, C.POINTER(SwapStats)]),
+    ("ma_swap_info", _I, [_VP, C.POINTER(_I), C.POINTER(_U64), C.POINTER(_U32)]),
+    ("ma_swap_set_trace", _I, [_VP, IO_TRACE_FN, _VP]),
+    ("ma_swap_save_manifest", _I, [_VP]),
+    ("ma_swap_create_virtual_devices", _I, [C.c_char_p, _U32, _U64]),
+    ("ma_swap_uring_available", _I, []),
+    ("ma_cursor_open", _I, [_U32, C.c_char_p, C.POINTER(_VP)]),
+    ("ma_cursor_close", _I, [_VP]),
+    ("ma_cursor_advance", _I, [_VP, _U32, _U64, C.POINTER(_U64)]),
+    ("ma_cursor_position", _I, [_VP, _U32, C.POINTER(_U64)]),
+    ("ma_cursor_restore", _I, [_VP, _U32, _U64]),
+    ("ma_stepper_apply_swapped", _I, [_VP, _VP, C.POINTER(SwapGroup), _U32, _VP, _U32, _VP, _U32,
+                                      _U64, _VP, _VP, _VP, C.POINTER(_I)]),
     ("ma_host_register", _I, [_VP, _U64]),
     ("ma_host_unregister", _I, [_VP]),
     ("ma_pointer_kind", _I, [_VP, C.POINTER(_I)]),

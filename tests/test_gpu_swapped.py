@@ -1,0 +1,132 @@
+"""Config 5 path on the B200: optimizer state in the swap store (NVMe tier)
+and in registered host memory (DRAM tier), streamed store -> registered host
+slot -> HBM -> K2 -> back by ma_stepper_apply_swapped, against the
+reference's per-step digests (tests/golden/workload.json, produced by the
+unmodified reference) — bit-exact — plus the I/O accounting of
+simulator.cpp:436-469 (a skipped step reads and writes no state)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a B200", allow_module_level=True)
+
+import paper_2505_23254_b200 as mab  # noqa: E402
+from oracle import oracle as ora  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def u2f(x):
+    return float(np.uint32(x).view(np.float32))
+
+
+def fnv_f32(a) -> str:
+    return ora.fnv_hex(np.ascontiguousarray(a, np.float32))
+
+
+def fnv16(t) -> str:
+    return ora.fnv_hex(t.view(torch.int16).cpu().numpy().view(np.uint16))
+
+
+def align4k(n):
+    return (n + 4095) // 4096 * 4096
+
+
+@pytest.mark.parametrize("backend", ["auto", "sync", "aio"])
+@pytest.mark.parametrize("host_slots,dev_slots,tier", [(2, 2, "all-swapped"), (3, 2, "mixed"),
+                                                       (4, 3, "mixed")])
+def test_swapped_apply_workload_golden(golden, tmp_path, backend, host_slots, dev_slots, tier):
+    c = next(x for x in golden("workload.json")["cases"] if x["name"] == "cfg_bf16_n100003")
+    n, sub, seed = c["n"], c["subgroup"], c["seed"]
+    hyper = mab.AdamHyper(lr=u2f(c["lr"]), beta1=u2f(c["beta1"]), beta2=u2f(c["beta2"]),
+                          eps=u2f(c["eps"]), weight_decay=u2f(c["wd"]))
+    pd = torch.empty(n, dtype=torch.float32, device=DEV)
+    w = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    g = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    mab.gen_seeded_weights(pd, w, seed=seed)
+    p0 = pd.cpu().numpy()
+    offs = list(range(0, n, sub))
+    slot = align4k(sub) // 4 * 4  # elements per slot (multiple of 4, >= sub)
+    devs = mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 2, 64 << 20)
+    store = mab.DirectIoEngine(devs, workers=2, queue_depth=8, backend=backend)
+    # tiering: "mixed" keeps every other group in registered host DRAM
+    swapped = [tier == "all-swapped" or k % 2 == 0 for k in range(len(offs))]
+    host = {}
+    groups = []
+    buf = mab.aligned_host_buffer(align4k(sub * 4))
+    for k, o in enumerate(offs):
+        ln = min(sub, n - o)
+        if swapped[k]:
+            for name, arr in (("master", p0[o:o + ln]), ("m", np.zeros(ln, np.float32)),
+                              ("v", np.zeros(ln, np.float32))):
+                buf.view(np.float32)[:ln] = arr
+                store.write_tensor(f"{name}.g{k}", buf, ln * 4)
+            groups.append(((f"master.g{k}", f"m.g{k}", f"v.g{k}"), g[o:o + ln], w[o:o + ln]))
+        else:
+            t = [torch.tensor(p0[o:o + ln]).pin_memory(), torch.zeros(ln).pin_memory(),
+                 torch.zeros(ln).pin_memory()]
+            host[k] = t
+            groups.append((tuple(t), g[o:o + ln], w[o:o + ln]))
+    hstage = mab.aligned_host_buffer(host_slots * 3 * align4k(slot * 4), register=True)
+    dstage = torch.empty(3 * dev_slots * slot, dtype=torch.float32, device=DEV)
+    st = mab.Stepper(hyper, c["init_scale"], c["growth_interval"], "bf16", "bf16")
+
+    def gather(name, idx):
+        out = np.empty(n, np.float32)
+        rb = mab.aligned_host_buffer(align4k(sub * 4))
+        for k, o in enumerate(offs):
+            ln = min(sub, n - o)
+            if swapped[k]:
+                assert store.read_tensor(f"{name}.g{k}", rb) == ln * 4
+                out[o:o + ln] = rb.view(np.float32)[:ln]
+            else:
+                out[o:o + ln] = host[k][idx].numpy()
+        return out
+
+    n_sw = sum(swapped)
+    for s, want in enumerate(c["per_step"]):
+        mab.gen_pseudo_grads(g, w, step=s, seed=seed, d_scale=st.scale_t)
+        for f in c["faults"]:
+            if f["step"] == s:
+                mab.plant_bits(g, f["index"] % n, f["bits"])
+        st.check(g)
+        before = store.stats()
+        skipped = st.apply_swapped(store, groups, hstage, host_slots, dstage, dev_slots, slot)
+        st.finish()
+        torch.cuda.synchronize()
+        after = store.stats()
+        assert skipped == want["overflow"]
+        moved = (after["read_requests"] - before["read_requests"],
+                 after["write_requests"] - before["write_requests"])
+        assert moved == ((0, 0) if skipped else (3 * n_sw, 3 * n_sw)), (s, moved)
+        for key, idx, name in (("p", 0, "master"), ("m", 1, "m"), ("v", 2, "v")):
+            assert fnv_f32(gather(name, idx)) == want[f"{key}_fnv"], (s, key)
+        assert fnv16(w) == want["w_fnv"], s
+    store.close()
+    mab.host_unregister(hstage)
+
+
+def test_swapped_rejects_bad_staging(tmp_path):
+    devs = mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 1, 16 << 20)
+    store = mab.DirectIoEngine(devs)
+    n = 4096
+    g = torch.zeros(n, dtype=torch.bfloat16, device=DEV)
+    w = torch.zeros(n, dtype=torch.bfloat16, device=DEV)
+    st = mab.Stepper(mab.AdamHyper(), 65536.0, 2000, "bf16", "bf16")
+    dstage = torch.empty(3 * 2 * n, dtype=torch.float32, device=DEV)
+    unregistered = mab.aligned_host_buffer(2 * 3 * n * 4)
+    with pytest.raises(mab.MemAscendError) as ei:
+        st.apply_swapped(store, [(("a", "b", "c"), g, w)], unregistered, 2, dstage, 2, n)
+    assert ei.value.code == "invalid-argument"
+    hstage = mab.aligned_host_buffer(2 * 3 * n * 4, register=True)
+    with pytest.raises(mab.MemAscendError) as ei:  # group larger than a slot
+        st.apply_swapped(store, [(("a", "b", "c"), g, w)], hstage, 2, dstage, 2, n // 2)
+    assert ei.value.code == "size-violation"
+    st.check(g)
+    with pytest.raises(mab.MemAscendError) as ei:  # keys never written
+        st.apply_swapped(store, [(("a", "b", "c"), g, w)], hstage, 2, dstage, 2, n)
+    assert ei.value.code == "not-found"
+    mab.host_unregister(hstage)
+    store.close()
