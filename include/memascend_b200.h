@@ -400,6 +400,51 @@ MA_API int ma_stepper_apply_swapped(ma_stepper* s, ma_swap* e, const ma_swap_gro
                                     int* skipped);
 
 /* ------------------------------------------------------------------ */
+/* Device-side adaptive pool + weight prefetch.
+ * PAPER.md §4.2: the adaptive buffer pool "extends naturally to GDS-based
+ * offloading, which necessitates similar buffer management on the GPU".
+ * ma_dpool is that pool in HBM: one cudaMalloc'd backing carved into
+ * exact-fit slot classes (pool.cpp:22-68 planning: stride = payload rounded
+ * to 4096, classes laid out back to back); a tensor takes the tightest class
+ * whose payload fits (pool.cpp:111-131).  ma_prefetcher is the layer-wise
+ * parameter swapper of simulator.cpp:367-425 moved onto the GPU: tensors
+ * submitted in order are read from the swap store into registered host
+ * slots (store workers), copied into device slots on the prefetcher's copy
+ * stream and handed out by acquire (the consumer's stream waits on the
+ * copy's event; no host sync), and a slot returns to the pool at release
+ * (reuse ordered after the consumer's work by an event).  Prefetch depth is
+ * bounded by the device slots (the pool's in-flight blocks) and by
+ * host_slots. */
+typedef struct ma_dpool ma_dpool;
+typedef struct ma_dpool_stats {
+    uint64_t capacity_bytes;  /* sum of slot payloads (pool_capacity) */
+    uint64_t backing_bytes;   /* HBM reserved (4096-rounded strides) */
+    uint64_t peak_live_bytes; /* largest sum of checked-out payloads */
+    uint64_t live_bytes;
+    uint64_t checkout_count;
+    uint64_t checkin_count;
+} ma_dpool_stats;
+MA_API int ma_dpool_create(const uint64_t* slot_payload_bytes, const uint32_t* slot_counts,
+                           uint32_t nclasses, ma_dpool** out);
+MA_API int ma_dpool_destroy(ma_dpool* p);
+MA_API int ma_dpool_get_stats(ma_dpool* p, ma_dpool_stats* out);
+
+typedef struct ma_prefetcher ma_prefetcher;
+/* h_staging: registered host memory, 4096-aligned, host_slots x h_slot_bytes
+ * (h_slot_bytes a multiple of 4096 covering the largest padded tensor). */
+MA_API int ma_prefetcher_create(ma_swap* store, ma_dpool* pool, void* h_staging,
+                                uint64_t h_slot_bytes, uint32_t host_slots, ma_prefetcher** out);
+/* Queue `key` (a tensor in the store) for prefetch; keys are served in order. */
+MA_API int ma_prefetch_submit(ma_prefetcher* f, const char* key);
+/* Blocks until `key`'s copy is enqueued, makes `stream` wait for it and
+ * returns its device address and logical length. */
+MA_API int ma_prefetch_acquire(ma_prefetcher* f, const char* key, void* stream, void** dptr,
+                               uint64_t* bytes);
+/* Returns `key`'s device slot; its next user waits for `stream`'s work so far. */
+MA_API int ma_prefetch_release(ma_prefetcher* f, const char* key, void* stream);
+MA_API int ma_prefetcher_destroy(ma_prefetcher* f);
+
+/* ------------------------------------------------------------------ */
 /* Verification hooks (used by tests/; they run the product device code). */
 /* FNV-1a-64 of every 2^block_log2 consecutive fp32->kind conversions over
  * all 2^32 inputs, through the same device cast K2 uses; out_host has

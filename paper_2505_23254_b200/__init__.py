@@ -8,7 +8,9 @@ tests and bench; it never computes anything itself.
 """
 from .capi import LIB_PATH, AdamHyper, MemAscendError, lib  # noqa: F401
 from .api import (  # noqa: F401
+    DevicePool,
     DirectIoEngine,
+    WeightPrefetcher,
     aligned_host_buffer,
     uring_available,
     OptimizerState,

@@ -556,6 +556,82 @@ class SwapOp:
         return out.value
 
 
+class DevicePool:
+    """Exact-fit slot pool in HBM (ma_dpool): classes = [(payload_bytes,
+    slot_count), ...], planned like pool.cpp:22-68 (4096-rounded strides)."""
+
+    def __init__(self, classes):
+        nb = (C.c_uint64 * len(classes))(*[c[0] for c in classes])
+        nc = (C.c_uint32 * len(classes))(*[c[1] for c in classes])
+        h = C.c_void_p()
+        check(capi.lib().ma_dpool_create(nb, nc, len(classes), C.byref(h)))
+        self.handle = h.value
+
+    def stats(self) -> dict:
+        st = capi.DPoolStats()
+        check(capi.lib().ma_dpool_get_stats(self.handle, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in capi.DPoolStats._fields_}
+
+    def close(self):
+        if getattr(self, "handle", None):
+            check(capi.lib().ma_dpool_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class _DeviceBytes:
+    """__cuda_array_interface__ view of a device allocation (no copy)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class WeightPrefetcher:
+    """Store -> registered host slot -> HBM slot pipeline (ma_prefetcher):
+    submit(key) in consumption order; acquire(key, stream) returns a uint8
+    device tensor view of the slot (stream waits for its copy);
+    release(key, stream) returns the slot after stream's work so far."""
+
+    def __init__(self, store: "DirectIoEngine", pool: DevicePool, host_slots: int,
+                 host_slot_bytes: int):
+        self.staging = aligned_host_buffer(host_slots * host_slot_bytes, register=True)
+        h = C.c_void_p()
+        check(capi.lib().ma_prefetcher_create(store.handle, pool.handle, self.staging.ctypes.data,
+                                              host_slot_bytes, host_slots, C.byref(h)))
+        self.handle = h.value
+        self._keep = (store, pool)
+
+    def submit(self, key: str) -> None:
+        check(capi.lib().ma_prefetch_submit(self.handle, key.encode()))
+
+    def acquire(self, key: str, stream=None):
+        ptr, n = C.c_void_p(), C.c_uint64()
+        check(capi.lib().ma_prefetch_acquire(self.handle, key.encode(), _stream_ptr(stream),
+                                             C.byref(ptr), C.byref(n)))
+        return torch.as_tensor(_DeviceBytes(ptr.value, n.value), device="cuda")
+
+    def release(self, key: str, stream=None) -> None:
+        check(capi.lib().ma_prefetch_release(self.handle, key.encode(), _stream_ptr(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            check(capi.lib().ma_prefetcher_destroy(self.handle))
+            self.handle = None
+            host_unregister(self.staging)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 def uring_available() -> bool:
     return bool(capi.lib().ma_swap_uring_available())
 

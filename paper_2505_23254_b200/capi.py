@@ -92,6 +92,11 @@ class SwapGroup(C.Structure):
                 ("w", C.c_void_p), ("n", C.c_uint64)]
 
 
+class DPoolStats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("capacity_bytes", "backing_bytes", "peak_live_bytes",
+                                          "live_bytes", "checkout_count", "checkin_count")]
+
+
 IO_AUTO, IO_SYNC, IO_POSIX_AIO, IO_URING = 0, 1, 2, 3
 IO_BACKENDS = {"auto": IO_AUTO, "sync": IO_SYNC, "aio": IO_POSIX_AIO, "uring": IO_URING}
 IO_TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int)
@@ -163,6 +168,14 @@ SIGNATURES = [
     ("ma_cursor_restore", _I, [_VP, _U32, _U64]),
     ("ma_stepper_apply_swapped", _I, [_VP, _VP, C.POINTER(SwapGroup), _U32, _VP, _U32, _VP, _U32,
                                       _U64, _VP, _VP, _VP, C.POINTER(_I)]),
+    ("ma_dpool_create", _I, [_VP, _VP, _U32, C.POINTER(_VP)]),
+    ("ma_dpool_destroy", _I, [_VP]),
+    ("ma_dpool_get_stats", _I, [_VP, C.POINTER(DPoolStats)]),
+    ("ma_prefetcher_create", _I, [_VP, _VP, _VP, _U64, _U32, C.POINTER(_VP)]),
+    ("ma_prefetch_submit", _I, [_VP, C.c_char_p]),
+    ("ma_prefetch_acquire", _I, [_VP, C.c_char_p, _VP, C.POINTER(_VP), C.POINTER(_U64)]),
+    ("ma_prefetch_release", _I, [_VP, C.c_char_p, _VP]),
+    ("ma_prefetcher_destroy", _I, [_VP]),
     ("ma_host_register", _I, [_VP, _U64]),
     ("ma_host_unregister", _I, [_VP]),
     ("ma_pointer_kind", _I, [_VP, C.POINTER(_I)]),

@@ -1,0 +1,134 @@
+"""Device-side adaptive pool + weight prefetch on the
+B200: tensors stream swap store -> registered host slot -> exact-fit HBM slot
+in submission order; contents bit-exact, slot reuse fenced after the
+consumer's work (a consumer that releases without synchronising still sees
+its own tensor), pool accounting as pool.cpp keeps it, errors by code."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a B200", allow_module_level=True)
+
+import paper_2505_23254_b200 as mab  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+# a toy GQA decoder: (name, bytes) per layer + the two global tensors
+PER_LAYER = [("q", 1 << 20), ("k", (256 << 10) + 100), ("v", (256 << 10) + 100), ("o", 1 << 20),
+             ("gate", 3 << 20), ("up", 3 << 20), ("down", 3 << 20)]
+GLOBAL = ("emb", (4 << 20) + 2)
+
+
+def inventory(layers):
+    inv = [GLOBAL]
+    for li in range(layers):
+        inv += [(f"layer{li}.{n}", b) for n, b in PER_LAYER]
+    inv.append(("head", GLOBAL[1]))
+    return inv
+
+
+def adaptive_classes(inflight):
+    # pool.cpp:36-42: global members + members_per_layer x inflight blocks
+    return [(GLOBAL[1], 2), (3 << 20, 3 * inflight), (1 << 20, 2 * inflight),
+            ((256 << 10) + 100, 2 * inflight)]
+
+
+def fill_store(tmp_path, inv):
+    devs = mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 2, 64 << 20)
+    store = mab.DirectIoEngine(devs, workers=2, queue_depth=16)
+    data = {}
+    for k, (name, nb) in enumerate(inv):
+        buf = mab.aligned_host_buffer((nb + 4095) // 4096 * 4096)
+        buf[:] = np.random.default_rng(k).integers(0, 256, buf.size, dtype=np.uint8)
+        store.write_tensor(name, buf, nb)
+        data[name] = buf[:nb].copy()
+    return store, data
+
+
+@pytest.mark.parametrize("inflight,host_slots", [(1, 1), (2, 3), (3, 8)])
+def test_prefetch_stream_bitexact(tmp_path, inflight, host_slots):
+    layers = 5
+    inv = inventory(layers)
+    store, data = fill_store(tmp_path, inv)
+    pool = mab.DevicePool(adaptive_classes(inflight))
+    pf = mab.WeightPrefetcher(store, pool, host_slots, 5 << 20)
+    for name, _ in inv:
+        pf.submit(name)
+    stream = torch.cuda.current_stream()
+    sums = {}
+    held = []
+    emb = pf.acquire("emb")
+    sums["emb"] = emb.to(torch.int64).sum()
+    for li in range(layers):
+        for n, _ in PER_LAYER:
+            key = f"layer{li}.{n}"
+            t = pf.acquire(key)
+            assert t.numel() == len(data[key])
+            sums[key] = t.to(torch.int64).sum()          # consumer work on `stream`
+            if li == 2 and n == "up":                     # one full byte compare too
+                assert (t.cpu().numpy() == data[key]).all()
+            held.append(key)
+        for key in held:                                  # block done: release, no sync
+            pf.release(key, stream)
+        held = []
+    head = pf.acquire("head")
+    sums["head"] = head.to(torch.int64).sum()
+    assert (head.cpu().numpy() == data["head"]).all()
+    pf.release("emb", stream)
+    pf.release("head", stream)
+    torch.cuda.synchronize()
+    for name, _ in inv:
+        assert int(sums[name]) == int(data[name].astype(np.int64).sum()), name
+    st = pool.stats()
+    assert st["checkout_count"] == st["checkin_count"] == len(inv)
+    assert st["live_bytes"] == 0
+    assert st["capacity_bytes"] == sum(b * c for b, c in adaptive_classes(inflight))
+    assert st["peak_live_bytes"] <= st["capacity_bytes"]
+    assert st["backing_bytes"] == sum((b + 4095) // 4096 * 4096 * c
+                                      for b, c in adaptive_classes(inflight))
+    pf.close()
+    pool.close()
+    store.close()
+
+
+def test_adaptive_vs_monolithic_backing(tmp_path):
+    """PAPER.md §4.2 on the GPU: exact-fit classes vs largest-tensor slots."""
+    mono = mab.DevicePool([(GLOBAL[1], 2 + 7 * 2)])
+    adap = mab.DevicePool(adaptive_classes(2))
+    assert adap.stats()["backing_bytes"] < 0.5 * mono.stats()["backing_bytes"]
+    mono.close()
+    adap.close()
+
+
+def test_prefetch_errors(tmp_path):
+    inv = inventory(1)
+    store, _ = fill_store(tmp_path, inv)
+    pool = mab.DevicePool([(1 << 20, 1)])  # nothing bigger than 1 MiB fits
+    pf = mab.WeightPrefetcher(store, pool, 2, 5 << 20)
+    with pytest.raises(mab.MemAscendError) as ei:
+        pf.acquire("layer0.q")
+    assert ei.value.code == "not-found"                   # never submitted
+    pf.submit("layer0.gate")
+    pf.submit("layer0.q")
+    with pytest.raises(mab.MemAscendError) as ei:
+        pf.acquire("layer0.gate")
+    assert ei.value.code == "size-violation"              # fits no device class
+    with pytest.raises(mab.MemAscendError) as ei:
+        pf.submit("layer0.q")
+    assert ei.value.code == "already-checked-out"
+    t = pf.acquire("layer0.q")
+    assert t.numel() == 1 << 20
+    with pytest.raises(mab.MemAscendError) as ei:
+        pf.release("layer0.o")
+    assert ei.value.code == "lifecycle"
+    pf.release("layer0.q")
+    pf.submit("missing-key")
+    with pytest.raises(mab.MemAscendError) as ei:
+        pf.acquire("missing-key")
+    assert ei.value.code == "not-found"
+    pf.submit("layer0.o")                                 # left in flight: close drains it
+    pf.close()
+    assert pool.stats()["live_bytes"] == 0
+    pool.close()
+    store.close()

@@ -1,0 +1,130 @@
+#!/usr/bin/env python
+"""Weight-prefetch benchmark for the device-side adaptive pool (SURVEY.md
+§8(f) row 4): Llama-3-8B bf16 working weights (one rank, 16.06 GB) in the
+O_DIRECT swap store are streamed, in forward order, store -> registered host
+slot -> exact-fit HBM slot (ma_prefetcher), each consumed on the GPU by K1
+(the overflow check reads every byte of it in HBM) and released by block, the
+hold pattern of simulator.cpp:367-425 with N blocks in flight.  Reports the
+storage->HBM rate against the store's measured concurrent read rate, and the
+HBM the pool reserves in adaptive vs monolithic mode (the bench-pool report,
+memascend_cli.cpp:186-268, for the device pool).
+
+    python tools/bench_prefetch.py [--inflight 2] [--dir /tmp/ma_prefetch]
+"""
+import argparse
+import json
+import os
+import shutil
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2505_23254_b200 as mab  # noqa: E402
+
+# Llama-3-8B (model.cpp:233 preset): V 128256, H 4096, I 14336, L 32, kv 1024
+V, H, I, L, KV = 128256, 4096, 14336, 32, 1024
+PER_LAYER = [("q", H * H), ("k", KV * H), ("v", KV * H), ("o", H * H), ("gate", I * H),
+             ("up", I * H), ("down", H * I)]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dir", default="/tmp/ma_prefetch")
+    ap.add_argument("--inflight", type=int, default=2)
+    ap.add_argument("--host-slots", type=int, default=4)
+    ap.add_argument("--io-workers", type=int, default=4)
+    ap.add_argument("--io-depth", type=int, default=32)
+    ap.add_argument("--layers", type=int, default=L)
+    ap.add_argument("--passes", type=int, default=2)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    inv = [("emb", V * H * 2)] + [(f"layer{li}.{n}", e * 2) for li in range(a.layers)
+                                  for n, e in PER_LAYER] + [("head", V * H * 2)]
+    total = sum(b for _, b in inv)
+    shutil.rmtree(a.dir, ignore_errors=True)
+    devs = mab.DirectIoEngine.create_virtual_devices(a.dir, 2, total // 2 + (256 << 20))
+    store = mab.DirectIoEngine(devs, workers=a.io_workers, queue_depth=a.io_depth)
+    try:
+        src = mab.aligned_host_buffer((V * H * 2 + 4095) // 4096 * 4096)
+        src.view(np.uint16)[:] = 0x3F80  # bf16 1.0: finite, so K1 never trips
+        t0 = time.perf_counter()
+        for name, nb in inv:
+            store.write_tensor(name, src, nb)
+        t_write = time.perf_counter() - t0
+        classes = {
+            "adaptive": [(V * H * 2, 2), (I * H * 2, 3 * a.inflight), (H * H * 2, 2 * a.inflight),
+                         (KV * H * 2, 2 * a.inflight)],
+            "monolithic": [(V * H * 2, 2 + 7 * a.inflight)],
+        }
+        backing = {}
+        for mode, cls in classes.items():
+            p = mab.DevicePool(cls)
+            backing[mode] = p.stats()["backing_bytes"]
+            p.close()
+        pool = mab.DevicePool(classes["adaptive"])
+        pf = mab.WeightPrefetcher(store, pool, a.host_slots, (V * H * 2 + 4095) // 4096 * 4096)
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        stream = torch.cuda.current_stream()
+        times = []
+        for _ in range(a.passes):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for name, _ in inv:
+                pf.submit(name)
+            held = []
+            for name, nb in inv:
+                t = pf.acquire(name)
+                mab.overflow_check_async(t.view(torch.bfloat16), flag)
+                if name.startswith("layer"):
+                    held.append(name)
+                    if name.endswith(".down"):
+                        for k in held:
+                            pf.release(k, stream)
+                        held = []
+            pf.release("emb", stream)
+            pf.release("head", stream)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        assert int(flag.item()) == 0
+        st = pool.stats()
+        pf.close()
+        pool.close()
+        # the store's own concurrent read rate (same settings, 4 x 1 GiB keys)
+        keys = [f"peak{i}" for i in range(4)]
+        bufs = [mab.aligned_host_buffer(1 << 30) for _ in keys]
+        for k, b in zip(keys, bufs):
+            store.write_tensor(k, b, 1 << 30)
+        t0 = time.perf_counter()
+        for op in [store.read_tensor_async(k, b) for k, b in zip(keys, bufs)]:
+            op.wait()
+        read_peak = 4 * (1 << 30) / (time.perf_counter() - t0) / 1e9
+    finally:
+        store.close()
+        shutil.rmtree(a.dir, ignore_errors=True)
+    best = min(times)
+    line = {
+        "workload": "llama3-8b bf16 weights, forward order, store -> host slot -> HBM slot -> K1",
+        "bytes_per_pass": total, "tensors": len(inv), "inflight_blocks": a.inflight,
+        "seconds_per_pass": times, "achieved_gbs": total / best / 1e9,
+        "storage_read_peak_gbs": read_peak, "frac": total / best / 1e9 / read_peak,
+        "store_write_gbs": total / t_write / 1e9,
+        "device_pool": {"adaptive_backing_bytes": backing["adaptive"],
+                        "monolithic_backing_bytes": backing["monolithic"],
+                        "saving": 1 - backing["adaptive"] / backing["monolithic"],
+                        "peak_live_bytes": st["peak_live_bytes"],
+                        "capacity_bytes": st["capacity_bytes"],
+                        "fragmentation": 1 - st["peak_live_bytes"] / st["capacity_bytes"]},
+        "host_slots": a.host_slots, "io_workers": a.io_workers, "io_depth": a.io_depth,
+    }
+    print(json.dumps(line), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(line, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
