@@ -46,7 +46,7 @@ def main():
                                   for n, e in PER_LAYER] + [("head", V * H * 2)]
     total = sum(b for _, b in inv)
     shutil.rmtree(a.dir, ignore_errors=True)
-    devs = mab.DirectIoEngine.create_virtual_devices(a.dir, 2, total // 2 + (256 << 20))
+    devs = mab.DirectIoEngine.create_virtual_devices(a.dir, 2, total // 2 + (2304 << 20))
     store = mab.DirectIoEngine(devs, workers=a.io_workers, queue_depth=a.io_depth)
     try:
         src = mab.aligned_host_buffer((V * H * 2 + 4095) // 4096 * 4096)
@@ -93,15 +93,22 @@ def main():
         st = pool.stats()
         pf.close()
         pool.close()
-        # the store's own concurrent read rate (same settings, 4 x 1 GiB keys)
-        keys = [f"peak{i}" for i in range(4)]
-        bufs = [mab.aligned_host_buffer(1 << 30) for _ in keys]
-        for k, b in zip(keys, bufs):
-            store.write_tensor(k, b, 1 << 30)
-        t0 = time.perf_counter()
-        for op in [store.read_tensor_async(k, b) for k, b in zip(keys, bufs)]:
-            op.wait()
-        read_peak = 4 * (1 << 30) / (time.perf_counter() - t0) / 1e9
+        # the bound: the same reads, same order, same host slots, no GPU
+        # (storage -> registered host memory only), best of `passes`
+        slot = (V * H * 2 + 4095) // 4096 * 4096
+        bufs = [mab.aligned_host_buffer(slot) for _ in range(a.host_slots)]
+        read_times = []
+        for _ in range(a.passes):
+            t0 = time.perf_counter()
+            window = []
+            for k, (name, _) in enumerate(inv):
+                if len(window) == a.host_slots:
+                    window.pop(0).wait()
+                window.append(store.read_tensor_async(name, bufs[k % a.host_slots]))
+            for op in window:
+                op.wait()
+            read_times.append(time.perf_counter() - t0)
+        read_peak = total / min(read_times) / 1e9
     finally:
         store.close()
         shutil.rmtree(a.dir, ignore_errors=True)
@@ -110,7 +117,8 @@ def main():
         "workload": "llama3-8b bf16 weights, forward order, store -> host slot -> HBM slot -> K1",
         "bytes_per_pass": total, "tensors": len(inv), "inflight_blocks": a.inflight,
         "seconds_per_pass": times, "achieved_gbs": total / best / 1e9,
-        "storage_read_peak_gbs": read_peak, "frac": total / best / 1e9 / read_peak,
+        "storage_read_peak_gbs": read_peak,
+        "storage_peak_source": "same reads, order and host slots without the GPU stages", "frac": total / best / 1e9 / read_peak,
         "store_write_gbs": total / t_write / 1e9,
         "device_pool": {"adaptive_backing_bytes": backing["adaptive"],
                         "monolithic_backing_bytes": backing["monolithic"],
