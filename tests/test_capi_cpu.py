@@ -86,3 +86,9 @@ def test_no_device_fails_loudly(so_path):
     rs = C.c_void_p()
     rec = (C.c_ubyte * capi.RS_HANDLE_BYTES)()
     assert lib.ma_rs_create(2, 0, buf, 4, 1, C.byref(rs), rec) == 101
+    # the device pool and the prefetcher are GPU objects: no host stand-in
+    nb = (C.c_uint64 * 1)(1 << 20)
+    nc = (C.c_uint32 * 1)(2)
+    dp = C.c_void_p()
+    assert lib.ma_dpool_create(nb, nc, 1, C.byref(dp)) == 101
+    assert b"no CPU fallback" in lib.ma_last_error()
