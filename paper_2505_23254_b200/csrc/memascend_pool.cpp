@@ -13,6 +13,7 @@
 
 #include "memascend/error.hpp"
 #include "memascend/model.hpp"
+#include "memascend/device_pool.hpp"
 #include "memascend/pool.hpp"
 #include "memascend_b200.h"
 
@@ -445,6 +446,84 @@ double fragmentation(std::uint64_t capacity_bytes, std::uint64_t peak_live_bytes
     if (capacity_bytes == 0) raise(ErrorCode::invalid_argument, "fragmentation over zero capacity");
     if (peak_live_bytes > capacity_bytes) raise(ErrorCode::invalid_argument, "peak live bytes exceed capacity");
     return static_cast<double>(capacity_bytes - peak_live_bytes) / static_cast<double>(capacity_bytes);
+}
+
+}  // namespace memascend
+
+// ------------------------------------------------------------------ device pool
+// include/memascend/device_pool.hpp: the same class plan, backed in HBM by
+// ma_dpool; the prefetcher over ma_prefetcher.
+namespace memascend {
+
+namespace {
+
+void check_status(int status) {
+    if (status == MA_OK) return;
+    const std::string msg = ma_last_error();
+    if (status >= 1 && status <= 17) raise(static_cast<ErrorCode>(status - 1), msg);
+    raise(ErrorCode::device_error, msg);
+}
+
+}  // namespace
+
+DevicePool::DevicePool(const std::vector<TensorDescriptor>& inventory, PoolMode mode,
+                       std::uint64_t inflight_blocks) {
+    const Layout L = layout_for(inventory, mode, inflight_blocks);
+    classes_ = L.classes;
+    std::vector<std::uint64_t> bytes;
+    std::vector<std::uint32_t> counts;
+    for (const auto& c : classes_) {
+        bytes.push_back(c.slot_payload_bytes);
+        counts.push_back(static_cast<std::uint32_t>(c.slot_count));
+    }
+    check_status(ma_dpool_create(bytes.data(), counts.data(),
+                                 static_cast<std::uint32_t>(bytes.size()), &h_));
+}
+
+DevicePool::~DevicePool() {
+    if (h_) ma_dpool_destroy(h_);
+}
+
+PoolStats DevicePool::stats() const {
+    ma_dpool_stats s{};
+    check_status(ma_dpool_get_stats(h_, &s));
+    PoolStats out;
+    out.capacity_bytes = s.capacity_bytes;
+    out.backing_bytes = s.backing_bytes;
+    out.peak_live_bytes = s.peak_live_bytes;
+    out.live_bytes = s.live_bytes;
+    out.checkout_count = s.checkout_count;
+    out.checkin_count = s.checkin_count;
+    return out;
+}
+
+WeightPrefetcher::WeightPrefetcher(DirectIoEngine& store, DevicePool& pool,
+                                   std::uint32_t host_slots, std::uint64_t host_slot_bytes) {
+    const std::uint64_t slot = (host_slot_bytes + kGranule - 1) / kGranule * kGranule;
+    if (host_slots == 0 || slot == 0)
+        raise(ErrorCode::invalid_argument, "prefetcher needs >= 1 host slot of > 0 bytes");
+    staging_ = PinnedAllocator::global().allocate(slot * host_slots,
+                                                  {AllocPolicyKind::alignment_free});
+    check_status(ma_prefetcher_create(store.handle(), pool.handle(), staging_.data(), slot,
+                                      host_slots, &h_));
+}
+
+WeightPrefetcher::~WeightPrefetcher() {
+    if (h_) ma_prefetcher_destroy(h_);
+}
+
+void WeightPrefetcher::submit(const std::string& key) {
+    check_status(ma_prefetch_submit(h_, key.c_str()));
+}
+
+void* WeightPrefetcher::acquire(const std::string& key, void* stream, std::uint64_t* bytes) {
+    void* d = nullptr;
+    check_status(ma_prefetch_acquire(h_, key.c_str(), stream, &d, bytes));
+    return d;
+}
+
+void WeightPrefetcher::release(const std::string& key, void* stream) {
+    check_status(ma_prefetch_release(h_, key.c_str(), stream));
 }
 
 }  // namespace memascend

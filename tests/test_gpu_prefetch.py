@@ -132,3 +132,24 @@ def test_prefetch_errors(tmp_path):
     assert pool.stats()["live_bytes"] == 0
     pool.close()
     store.close()
+
+
+def test_cpp_device_pool_and_prefetcher(tmp_path):
+    """include/memascend/device_pool.hpp from C++: class plan equals the
+    reference Pool's pool_capacity() on the llama3.1-8b inventory; a toy
+    model's tensors stream through WeightPrefetcher bit-exactly."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2505_23254_b200", "lib")
+    exe = str(tmp_path / "device_pool_check")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"),
+                    "-I", "/usr/local/cuda/include", os.path.join(root, "tests", "cpp",
+                                                               "device_pool_check.cpp"),
+                    "-o", exe, "-L", lib, "-lmemascend", "-lmemascend_b200",
+                    "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}",
+                    "-Wl,-rpath,/usr/local/cuda/lib64", "-pthread"], check=True)
+    p = subprocess.run([exe, str(tmp_path / "store")], capture_output=True, text=True,
+                       timeout=300)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stdout + p.stderr
