@@ -1,7 +1,7 @@
 """Multi-rank step (BASELINE configs[2]): per-rank K1, one
 all-reduce(max) of the flag, identical skip decisions on every rank.
 
-The world-size-2 runs use torch.distributed with the gloo backend on
+The world-size 2/4/8 runs use torch.distributed with the gloo backend on
 127.0.0.1.  The CPU test drives the product's ShardStepper with an
 oracle-backed shard (test infrastructure); the GPU test drives it with the
 B200 kernels (DeviceShard, both ranks on cuda:0).  Both are compared with a
@@ -20,7 +20,8 @@ import torch.multiprocessing as mp
 from oracle import oracle as ora
 from paper_2505_23254_b200.shard import (FaultPlan, ShardStepper, shard_range, subgroup_bounds)
 
-N_TOTAL, SUBGROUP, STEPS, SEED, WORLD = 1_000_003, 100_000, 10, 1, 2
+N_TOTAL, SUBGROUP, STEPS, SEED = 1_000_003, 100_000, 10, 1
+WORLDS = [2, 4, 8]  # BASELINE configs[2]: the injection run at 2/4/8 ranks
 HYP = dict(lr=1e-3, weight_decay=0.01)
 
 
@@ -72,7 +73,7 @@ class OracleShard:
         self.flag[0] = 0
 
 
-def _worker(rank, port, out_dir, device_backend, p2p=False):
+def _worker(rank, port, out_dir, device_backend, p2p=False, WORLD=2):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
@@ -117,7 +118,7 @@ def _worker(rank, port, out_dir, device_backend, p2p=False):
         dist.destroy_process_group()
 
 
-def _check_against_single_process(out_dir):
+def _check_against_single_process(out_dir, WORLD):
     plan = FaultPlan(N_TOTAL, SUBGROUP, seed=7)
     faults = [(p.step, p.index, p.bits) for s in range(STEPS) for p in plan.at(s)]
     want = ora.train(N_TOTAL, STEPS, SEED, g_kind="bf16", w_kind="bf16", hyp=ora.hyper(**HYP),
@@ -155,33 +156,38 @@ def test_fault_plan_is_deterministic_and_rank_local():
                                                  for s in range(20)]
     ks = {sum(not p.control for p in plan.at(s)) for s in range(60)}
     assert ks == {0, 1, 3}
-    for s in range(20):
-        local = [p for r in range(WORLD)
-                 for p in plan.local(s, *shard_range(N_TOTAL, WORLD, r, SUBGROUP))]
-        assert sorted(local, key=lambda p: p.index) == sorted(plan.at(s), key=lambda p: p.index)
+    for world in WORLDS:
+        for s in range(20):
+            local = [p for r in range(world)
+                     for p in plan.local(s, *shard_range(N_TOTAL, world, r, SUBGROUP))]
+            assert (sorted(local, key=lambda p: p.index) ==
+                    sorted(plan.at(s), key=lambda p: p.index))
 
 
-def test_two_ranks_gloo_cpu_matches_single_process():
+@pytest.mark.parametrize("world", WORLDS)
+def test_ranks_gloo_cpu_match_single_process(world):
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(free_port(), d, False), nprocs=WORLD, join=True)
-        _check_against_single_process(d)
+        mp.spawn(_worker, args=(free_port(), d, False, False, world), nprocs=world, join=True)
+        _check_against_single_process(d, world)
 
 
 @pytest.mark.gpu
-def test_two_ranks_on_b200_matches_single_process():
+@pytest.mark.parametrize("world", WORLDS)
+def test_ranks_on_b200_match_single_process(world):
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(free_port(), d, True), nprocs=WORLD, join=True)
-        _check_against_single_process(d)
+        mp.spawn(_worker, args=(free_port(), d, True, False, world), nprocs=world, join=True)
+        _check_against_single_process(d, world)
 
 
 @pytest.mark.gpu
-def test_two_ranks_on_b200_peer_exchange_fused_in_k1():
+@pytest.mark.parametrize("world", WORLDS)
+def test_ranks_on_b200_peer_exchange_fused_in_k1(world):
     """Same run with the skip decision exchanged by K1's last CTA through
     peer memory (ma_stepper_check_xchg_async) instead of an all-reduce."""
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(free_port(), d, True, True), nprocs=WORLD, join=True)
-        _check_against_single_process(d)
+        mp.spawn(_worker, args=(free_port(), d, True, True, world), nprocs=world, join=True)
+        _check_against_single_process(d, world)
