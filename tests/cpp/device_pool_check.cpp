@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -62,8 +63,12 @@ int main(int argc, char** argv) {
         for (const auto& t : inv) pf.submit(t.name);
         cudaStream_t st;
         cudaStreamCreate(&st);
+        // the trainer's hold pattern (simulator.cpp:384-401): a block's
+        // tensors are checked in once the whole block has been consumed
+        std::map<std::string, size_t> block_size;
+        for (const auto& t : inv)
+            if (is_per_layer_role(t.role)) block_size[t.name.substr(0, t.name.find('.'))] += 1;
         std::vector<std::string> held, step_held;
-        std::string current;
         for (size_t k = 0; k < inv.size(); ++k) {
             const auto& t = inv[k];
             std::uint64_t nb = 0;
@@ -77,13 +82,11 @@ int main(int argc, char** argv) {
                 step_held.push_back(t.name);
                 continue;
             }
-            const std::string group = t.name.substr(0, t.name.find('.'));
-            if (group != current && !held.empty()) {
+            held.push_back(t.name);
+            if (held.size() == block_size[t.name.substr(0, t.name.find('.'))]) {
                 for (auto& h : held) pf.release(h, st);
                 held.clear();
             }
-            current = group;
-            held.push_back(t.name);
         }
         for (auto& h : held) pf.release(h, st);
         for (auto& h : step_held) pf.release(h, st);

@@ -151,5 +151,5 @@ def test_cpp_device_pool_and_prefetcher(tmp_path):
                     "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}",
                     "-Wl,-rpath,/usr/local/cuda/lib64", "-pthread"], check=True)
     p = subprocess.run([exe, str(tmp_path / "store")], capture_output=True, text=True,
-                       timeout=300)
+                       timeout=120)
     assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stdout + p.stderr
