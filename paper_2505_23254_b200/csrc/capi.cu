@@ -20,6 +20,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.cuh"
 #include "memascend_b200.h"
 #include "swap.hpp"
@@ -27,6 +29,13 @@
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range per entry point (header-only NVTX v3: free unless a tool such as
+// nsys / ncu --nvtx attaches), SURVEY.md §5 "tracing".
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct Status {
     int code;
@@ -470,6 +479,7 @@ int ma_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor) {
 
 int ma_overflow_check_async(const void* grads, uint64_t n, int g_dtype, uint32_t* d_flag,
                             uint64_t* d_first_index, void* stream) {
+    NvtxRange nvtx_range("ma_overflow_check_async");
     return guarded([&] {
         check_grad_dtype(g_dtype);
         if (!d_flag) fail(MA_ERR_INVALID_ARGUMENT, "null flag pointer");
@@ -481,6 +491,7 @@ int ma_overflow_check_async(const void* grads, uint64_t n, int g_dtype, uint32_t
 
 int ma_overflow_check(const void* grads, uint64_t n, int g_dtype, int track_first_index,
                       int* overflow, uint64_t* first_index) {
+    NvtxRange nvtx_range("ma_overflow_check");
     return guarded([&] {
         check_grad_dtype(g_dtype);
         if (!overflow) fail(MA_ERR_INVALID_ARGUMENT, "null result pointer");
@@ -529,6 +540,7 @@ int ma_overflow_check(const void* grads, uint64_t n, int g_dtype, int track_firs
 int ma_adam_step_async(float* p, float* m, float* v, const void* g, int g_dtype, uint64_t n,
                        uint64_t t, const ma_adam_hyper* h, float loss_scale, void* w_out,
                        int w_dtype, const uint32_t* d_skip_flag, void* stream) {
+    NvtxRange nvtx_range("ma_adam_step_async");
     return guarded([&] {
         check_grad_dtype(g_dtype);
         check_w_dtype(w_dtype);
@@ -540,6 +552,7 @@ int ma_adam_step_async(float* p, float* m, float* v, const void* g, int g_dtype,
 
 int ma_adam_step(float* p, float* m, float* v, const void* g, int g_dtype, uint64_t n,
                  uint64_t t, const ma_adam_hyper* h, float loss_scale, void* w_out, int w_dtype) {
+    NvtxRange nvtx_range("ma_adam_step");
     return guarded([&] {
         check_grad_dtype(g_dtype);
         check_w_dtype(w_dtype);
@@ -609,6 +622,7 @@ int ma_adam_step(float* p, float* m, float* v, const void* g, int g_dtype, uint6
 
 int ma_adam_step_bf16(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, uint64_t n,
                       uint64_t t, const ma_adam_hyper* h, float loss_scale) {
+    NvtxRange nvtx_range("ma_adam_step_bf16");
     return guarded([&] {
         const ma::AdamArgs a = explicit_args(h, t, loss_scale, nullptr);
         if (n == 0) return;
@@ -706,6 +720,7 @@ int ma_stepper_destroy(ma_stepper* s) {
 }
 
 int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void* stream) {
+    NvtxRange nvtx_range("ma_stepper_check_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (n && !g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
@@ -716,6 +731,7 @@ int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void* strea
 
 int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
                                 uint64_t chunk_elems, void* stream, void* copy_stream) {
+    NvtxRange nvtx_range("ma_stepper_check_host_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (n == 0) return;
@@ -864,6 +880,7 @@ int ma_xchg_destroy(ma_xchg* x) {
 
 int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n, ma_xchg* x,
                                 void* stream) {
+    NvtxRange nvtx_range("ma_stepper_check_xchg_async");
     return guarded([&] {
         if (!s || !x) fail(MA_ERR_INVALID_ARGUMENT, "null stepper / exchange");
         if (!x->ready) fail(MA_ERR_LIFECYCLE, "peer exchange not opened (ma_xchg_open)");
@@ -878,6 +895,7 @@ int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n, ma_xch
 
 int ma_stepper_ingest_async(ma_stepper* s, const void* src, int src_dtype, void* dst, uint64_t n,
                             void* stream) {
+    NvtxRange nvtx_range("ma_stepper_ingest_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         check_grad_dtype(src_dtype);
@@ -899,6 +917,7 @@ float* ma_stepper_scale(ma_stepper* s) { return s ? &s->d_st->scale : nullptr; }
 
 int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
                            void* stream) {
+    NvtxRange nvtx_range("ma_stepper_apply_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
@@ -915,6 +934,7 @@ int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t co
 
 int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups, uint32_t count,
                                 void* stream) {
+    NvtxRange nvtx_range("ma_stepper_apply_bf16_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
@@ -940,6 +960,7 @@ int ma_stepper_apply_streamed(ma_stepper* s, const ma_subgroup* groups, uint32_t
                               float* d_staging, uint64_t slot_elems, uint32_t slots,
                               void* stream, void* h2d_stream, void* d2h_stream,
                               int* skipped) {
+    NvtxRange nvtx_range("ma_stepper_apply_streamed");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
@@ -1009,6 +1030,7 @@ int ma_stepper_apply_swapped(ma_stepper* s, ma_swap* e, const ma_swap_group* gro
                              uint32_t count, void* h_staging, uint32_t host_slots,
                              float* d_staging, uint32_t dev_slots, uint64_t slot_elems,
                              void* stream, void* h2d_stream, void* d2h_stream, int* skipped) {
+    NvtxRange nvtx_range("ma_stepper_apply_swapped");
     return guarded([&] {
         if (!s || !e) fail(MA_ERR_INVALID_ARGUMENT, "null stepper or swap store");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
@@ -1100,6 +1122,7 @@ int ma_stepper_apply_swapped(ma_stepper* s, ma_swap* e, const ma_swap_group* gro
                 }
                 int code = 0;
                 std::string msg;
+                NvtxRange wr("ma_swapped_writeback");
                 const cudaError_t ce = cudaEventSynchronize(host_ev(wb.hslot));
                 if (ce != cudaSuccess) {
                     code = MA_ERR_CUDA;
@@ -1252,6 +1275,7 @@ int ma_stepper_apply_swapped(ma_stepper* s, ma_swap* e, const ma_swap_group* gro
 }
 
 int ma_stepper_finish_async(ma_stepper* s, void* stream) {
+    NvtxRange nvtx_range("ma_stepper_finish_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         ma::launch_step_finish(s->d_st, s->d_log, as_stream(stream));
@@ -1535,6 +1559,7 @@ extern "C" {
 
 int ma_stepper_reduce_check_async(ma_stepper* s, const void* const* srcs, int nsrc, int src_dtype,
                                   uint64_t n, float post_scale, void* dst, void* stream) {
+    NvtxRange nvtx_range("ma_stepper_reduce_check_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         check_grad_dtype(src_dtype);
@@ -1634,6 +1659,7 @@ int ma_rs_destroy(ma_rs* r) {
 
 int ma_stepper_reduce_scatter_async(ma_stepper* s, ma_rs* r, uint64_t base, uint64_t n,
                                     float post_scale, void* dst, void* stream) {
+    NvtxRange nvtx_range("ma_stepper_reduce_scatter_async");
     return guarded([&] {
         if (!s || !r) fail(MA_ERR_INVALID_ARGUMENT, "null stepper / reduce-scatter");
         if (!r->ready) fail(MA_ERR_LIFECYCLE, "reduce-scatter not opened (ma_rs_open)");
