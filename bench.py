@@ -182,12 +182,38 @@ def cpu_model():
     return "unknown"
 
 
+def reference_swapped_run(args, steps, warmup, threads, groups=2):
+    """configs[4] reference arm: the reference's own swapped step
+    (DirectIoEngine read master/m/v -> adam_step_fp32 -> write back,
+    simulator.cpp:453-469) on `groups` 100 M sub-groups in --swap-dir."""
+    import shutil
+
+    from oracle import oracle as ora
+
+    gs = np.random.default_rng(0).standard_normal(groups * SUBGROUP).astype(np.float32) * 8192
+    rdir = os.path.join(args.swap_dir, "ref-arm")
+    try:
+        secs, io = ora.ref_swap_bench(rdir, 2, SUBGROUP, groups, steps, warmup, gs,
+                                      ora.hyper(**HYPER), 65536.0, threads)
+    finally:
+        shutil.rmtree(rdir, ignore_errors=True)
+    return {"value": groups * SUBGROUP / secs, "unit": "params/s", "cores": threads,
+            "kind": "reference", "seconds_per_step": secs,
+            "sample": f"{groups} swapped groups of {SUBGROUP} params in the reference "
+                      f"DirectIoEngine: read master/m/v -> adam_step_fp32 -> write back "
+                      f"(simulator.cpp:453-469), median of {steps} steps after {warmup} warm-up, "
+                      f"{threads} threads, storage {io / secs / 1e9:.2f} GB/s"}
+
+
 def reference_arm(args, n_per_gpu, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = min(args.cpu_sample, n_per_gpu)
-    res = cpu_reference_run(sample, max(1, args.steps), max(1, args.warmup), threads)
+    if args.config == "cfg5":
+        res = reference_swapped_run(args, max(1, min(args.steps, 3)), 1, threads)
+    else:
+        sample = min(args.cpu_sample, n_per_gpu)
+        res = cpu_reference_run(sample, max(1, args.steps), max(1, args.warmup), threads)
     line = {
         "metric": METRIC, "value": res["value"], "unit": "params/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -679,23 +705,8 @@ def ours_swapped(args, n, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as ora
-
-        k = 2
-        gs = np.random.default_rng(0).standard_normal(k * sub).astype(np.float32) * 8192
-        rdir = os.path.join(args.swap_dir, "ref")
-        try:
-            secs, rio = ora.ref_swap_bench(rdir, 2, sub, k, 2, 1, gs, ora.hyper(**HYPER), 65536.0,
-                                           os.cpu_count() or 1)
-        finally:
-            shutil.rmtree(rdir, ignore_errors=True)
-        line["cpu_baseline"] = {
-            "value": k * sub / secs, "unit": "params/s", "cores": os.cpu_count() or 1,
-            "kind": "reference",
-            "sample": f"{k} swapped groups of {sub} params: the reference DirectIoEngine "
-                      "read master/m/v -> adam_step_fp32 -> write back (simulator.cpp:453-469), "
-                      "median of 2 steps after 1 warm-up; its storage rate "
-                      f"{rio / secs / 1e9:.2f} GB/s"}
+        res = reference_swapped_run(args, 2, 1, os.cpu_count() or 1)
+        line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
 
 
