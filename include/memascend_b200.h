@@ -398,6 +398,27 @@ MA_API int ma_stepper_apply_swapped(ma_stepper* s, ma_swap* e, const ma_swap_gro
                                     float* d_staging, uint32_t dev_slots, uint64_t slot_elems,
                                     void* stream, void* h2d_stream, void* d2h_stream,
                                     int* skipped);
+/* Pure-bf16 form (OptimPrecision::pure_bf16; simulator.cpp:470-486 swaps the
+ * bf16 m/v under "m.<g>"/"v.<g>" with 2-byte elements): per group the bf16
+ * momentum/variance come from the store (key_m/key_v) or the registered DRAM
+ * tier (m/v), the bf16 weights p stay on the device and are updated in place
+ * by K3.  Host slots are host_slots x 2 x align4096(2 * slot_elems) bytes,
+ * device slots dev_slots x 2 x slot_elems bf16; slot_elems a multiple of 8.
+ * 4 B per swapped parameter each way instead of 12. */
+typedef struct ma_swap_group_bf16 {
+    const char* key_m;
+    const char* key_v;
+    uint16_t* m;
+    uint16_t* v;
+    uint16_t* p;
+    const void* g;
+    uint64_t n;
+} ma_swap_group_bf16;
+MA_API int ma_stepper_apply_swapped_bf16(ma_stepper* s, ma_swap* e,
+                                         const ma_swap_group_bf16* groups, uint32_t count,
+                                         void* h_staging, uint32_t host_slots, void* d_staging,
+                                         uint32_t dev_slots, uint64_t slot_elems, void* stream,
+                                         void* h2d_stream, void* d2h_stream, int* skipped);
 
 /* ------------------------------------------------------------------ */
 /* Device-side adaptive pool + weight prefetch.

@@ -298,6 +298,38 @@ class Stepper:
             _stream_ptr(h2d_stream), _stream_ptr(d2h_stream), C.byref(skipped)))
         return bool(skipped.value)
 
+    def apply_swapped_bf16(self, store: "DirectIoEngine", groups, host_staging, host_slots,
+                           dev_staging, dev_slots, slot_elems, stream=None, h2d_stream=None,
+                           d2h_stream=None) -> bool:
+        """Pure-bf16 swapped update (K3): groups are (state, p, g) with state
+        = (key_m, key_v) in `store` or (m, v) bf16 arrays in registered host
+        memory, p the device bf16 weights.  host_staging: host_slots x 2 x
+        align4096(2 * slot_elems) bytes; dev_staging: 2 * dev_slots *
+        slot_elems bf16 (any 2-byte dtype)."""
+        arr = (capi.SwapGroupBf16 * len(groups))()
+        keep = []
+        for k, (state, p, g) in enumerate(groups):
+            if isinstance(state[0], str):
+                keys = [x.encode() for x in state]
+                keep.append(keys)
+                arr[k] = capi.SwapGroupBf16(keys[0], keys[1], None, None, p.data_ptr(),
+                                            g.data_ptr(), p.numel())
+            else:
+                arr[k] = capi.SwapGroupBf16(None, None, _raw(state[0])[0], _raw(state[1])[0],
+                                            p.data_ptr(), g.data_ptr(), p.numel())
+        if h2d_stream is None:
+            self._h2d = getattr(self, "_h2d", None) or torch.cuda.Stream(device=dev_staging.device)
+            h2d_stream = self._h2d
+        if d2h_stream is None:
+            self._d2h = getattr(self, "_d2h", None) or torch.cuda.Stream(device=dev_staging.device)
+            d2h_stream = self._d2h
+        skipped = C.c_int()
+        check(capi.lib().ma_stepper_apply_swapped_bf16(
+            self._h, store.handle, arr, len(arr), _raw(host_staging)[0], host_slots,
+            dev_staging.data_ptr(), dev_slots, slot_elems, _stream_ptr(stream),
+            _stream_ptr(h2d_stream), _stream_ptr(d2h_stream), C.byref(skipped)))
+        return bool(skipped.value)
+
     def finish(self, stream=None):
         check(capi.lib().ma_stepper_finish_async(self._h, _stream_ptr(stream)))
 

@@ -97,6 +97,11 @@ class DPoolStats(C.Structure):
                                           "live_bytes", "checkout_count", "checkin_count")]
 
 
+class SwapGroupBf16(C.Structure):
+    _fields_ = [("key_m", C.c_char_p), ("key_v", C.c_char_p), ("m", C.c_void_p),
+                ("v", C.c_void_p), ("p", C.c_void_p), ("g", C.c_void_p), ("n", C.c_uint64)]
+
+
 IO_AUTO, IO_SYNC, IO_POSIX_AIO, IO_URING = 0, 1, 2, 3
 IO_BACKENDS = {"auto": IO_AUTO, "sync": IO_SYNC, "aio": IO_POSIX_AIO, "uring": IO_URING}
 IO_TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int)
@@ -176,6 +181,8 @@ SIGNATURES = [
     ("ma_prefetch_acquire", _I, [_VP, C.c_char_p, _VP, C.POINTER(_VP), C.POINTER(_U64)]),
     ("ma_prefetch_release", _I, [_VP, C.c_char_p, _VP]),
     ("ma_prefetcher_destroy", _I, [_VP]),
+    ("ma_stepper_apply_swapped_bf16", _I, [_VP, _VP, C.POINTER(SwapGroupBf16), _U32, _VP, _U32,
+                                           _VP, _U32, _U64, _VP, _VP, _VP, C.POINTER(_I)]),
     ("ma_host_register", _I, [_VP, _U64]),
     ("ma_host_unregister", _I, [_VP]),
     ("ma_pointer_kind", _I, [_VP, C.POINTER(_I)]),

@@ -16,6 +16,7 @@
 #include <mutex>
 #include <condition_variable>
 #include <deque>
+#include <functional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -1026,251 +1027,337 @@ int ma_stepper_apply_streamed(ma_stepper* s, const ma_subgroup* groups, uint32_t
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// The swapped pipeline shared by the fp32 (K2) and pure-bf16 (K3) forms.
+// Each group moves `ntens` tensors of `esize`-byte elements: from the swap
+// store (keys) through a registered host slot, or from the registered DRAM
+// tier (host pointers), into a device slot; `launch` runs the update on the
+// compute stream over the device slot's tensors; everything flows back the
+// same way.
+struct SwapPlan {
+    uint32_t count = 0;
+    int ntens = 3;
+    uint64_t esize = 4;
+    std::function<const char*(uint32_t, int)> key;  // nullptr: DRAM tier
+    std::function<char*(uint32_t, int)> host;       // DRAM-tier tensor base
+    std::function<uint64_t(uint32_t)> n;
+    std::function<void(uint32_t, uint64_t, uint64_t, char* const*, cudaStream_t)> launch;
+};
+
+void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_staging,
+                 uint32_t host_slots, void* d_staging, uint32_t dev_slots, uint64_t slot_elems,
+                 void* stream, void* h2d_stream, void* d2h_stream, int* skipped) {
+    if (!s || !e) fail(MA_ERR_INVALID_ARGUMENT, "null stepper or swap store");
+    if (!d_staging || slot_elems == 0 || dev_slots < 2 || dev_slots > 16)
+        fail(MA_ERR_INVALID_ARGUMENT, "device staging needs 2..16 slots of slot_elems > 0");
+    if (slot_elems % 8) fail(MA_ERR_ALIGNMENT, "slot_elems must be a multiple of 8");
+    const int T = plan.ntens;
+    const uint64_t E = plan.esize;
+    const uint64_t tb = (slot_elems * E + ma::swp::kGranule - 1) / ma::swp::kGranule *
+                        ma::swp::kGranule;  // one tensor in a host slot
+    uint32_t n_swapped = 0;
+    for (uint32_t k = 0; k < plan.count; ++k) {
+        int keys = 0;
+        for (int t = 0; t < T; ++t) keys += plan.key(k, t) ? 1 : 0;
+        if (keys && keys != T)
+            fail(MA_ERR_INVALID_ARGUMENT, "a swapped group needs a key for every state tensor");
+        if (keys && plan.n(k) > slot_elems)
+            fail(MA_ERR_SIZE_VIOLATION, "swapped group " + std::to_string(k) + " has " +
+                                            std::to_string(plan.n(k)) + " elements > slot_elems");
+        if (!keys && plan.n(k))
+            for (int t = 0; t < T; ++t)
+                if (!plan.host(k, t))
+                    fail(MA_ERR_INVALID_ARGUMENT, "host-resident group without its state tensors");
+        n_swapped += keys ? 1 : 0;
+    }
+    if (n_swapped) {
+        if (!h_staging || host_slots < 2)
+            fail(MA_ERR_INVALID_ARGUMENT, "swapped groups need >= 2 host slots");
+        if (reinterpret_cast<uintptr_t>(h_staging) % ma::swp::kGranule)
+            fail(MA_ERR_ALIGNMENT, "host staging must be 4096-aligned");
+        const void* alias;
+        if (classify(h_staging, &alias) != 2)
+            fail(MA_ERR_INVALID_ARGUMENT,
+                 "host staging must be registered host memory (ma_host_register)");
+    }
+    cudaStream_t cs = as_stream(stream);
+    cudaStream_t hs = as_stream(h2d_stream);
+    cudaStream_t ds = as_stream(d2h_stream);
+    // a skipped step reads and writes no optimizer state (simulator.cpp:438-441)
+    uint32_t flag = 0;
+    CK(cudaMemcpyAsync(&flag, &s->d_st->flag, 4, cudaMemcpyDeviceToHost, cs));
+    CK(cudaStreamSynchronize(cs));
+    if (skipped) *skipped = flag ? 1 : 0;
+    s->last = cs;
+    if (flag) return;
+    stepper_grow_bc(s, s->issued + 1);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    ma::swp::Engine& eng = *e->e;
+    char* hbase = static_cast<char*>(h_staging);
+    char* dbase = static_cast<char*>(d_staging);
+    auto hslot_ptr = [&](uint32_t h, int t) { return hbase + (static_cast<uint64_t>(T) * h + t) * tb; };
+    auto dslot_ptr = [&](uint32_t d, int t) {
+        return dbase + (static_cast<uint64_t>(T) * d + t) * slot_elems * E;
+    };
+    // events: [0] entry, [1 + 3*d + {0 h2d, 1 update, 2 d2h}] device slots,
+    // [1 + 3*dev_slots + h] host slot's D2H — all created here: the writer
+    // thread must not touch s->events
+    s->event(3 * dev_slots + host_slots);
+    const std::vector<cudaEvent_t> evs(s->events.begin(),
+                                       s->events.begin() + 1 + 3 * dev_slots + host_slots);
+    cudaEvent_t entry = evs[0];
+    auto dev_ev = [&](uint32_t d, int kind) { return evs[1 + 3 * d + kind]; };
+    auto host_ev = [&](uint32_t h) { return evs[1 + 3 * dev_slots + h]; };
+    CK(cudaEventRecord(entry, cs));
+    CK(cudaStreamWaitEvent(hs, entry, 0));
+
+    // writer thread: waits for a host slot's D2H, writes the group's state
+    // back to the store, frees the slot
+    struct WB {
+        uint32_t group, hslot;
+    };
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<WB> wq;
+    std::vector<char> hfree(host_slots, 1);
+    bool closing = false;
+    int werr_code = 0;
+    std::string werr;
+    std::thread writer([&] {
+        cudaSetDevice(dev);
+        for (;;) {
+            WB wb;
+            {
+                std::unique_lock<std::mutex> lock(mu);
+                cv.wait(lock, [&] { return closing || !wq.empty(); });
+                if (wq.empty()) return;
+                wb = wq.front();
+                wq.pop_front();
+            }
+            int code = 0;
+            std::string msg;
+            NvtxRange wr("ma_swapped_writeback");
+            const cudaError_t ce = cudaEventSynchronize(host_ev(wb.hslot));
+            if (ce != cudaSuccess) {
+                code = MA_ERR_CUDA;
+                msg = std::string("cudaEventSynchronize: ") + cudaGetErrorString(ce);
+            } else {
+                std::vector<ma::swp::Op*> ops(T, nullptr);
+                for (int t = 0; t < T; ++t) {
+                    try {
+                        ops[t] = eng.submit_write(plan.key(wb.group, t), hslot_ptr(wb.hslot, t),
+                                                  tb, plan.n(wb.group) * E);
+                    } catch (const ma::swp::Failure& f) {
+                        if (!code) code = f.code, msg = f.msg;
+                    }
+                }
+                for (int t = 0; t < T; ++t) {
+                    if (!ops[t]) continue;
+                    try {
+                        eng.wait(ops[t]);
+                    } catch (const ma::swp::Failure& f) {
+                        if (!code) code = f.code, msg = f.msg;
+                    }
+                }
+            }
+            std::lock_guard<std::mutex> lock(mu);
+            if (code && !werr_code) werr_code = code, werr = msg;
+            hfree[wb.hslot] = 1;
+            cv.notify_all();
+        }
+    });
+
+    // reads: swapped groups in order, each into a free host slot
+    std::vector<uint32_t> swapped;
+    for (uint32_t k = 0; k < plan.count; ++k)
+        if (plan.key(k, 0)) swapped.push_back(k);
+    struct Pending {
+        uint32_t hslot = 0;
+        std::vector<ma::swp::Op*> ops;
+    };
+    std::vector<Pending> pend(plan.count);
+    size_t next_read = 0;
+    auto claim_slot = [&](bool block) -> int {
+        std::unique_lock<std::mutex> lock(mu);
+        for (;;) {
+            if (werr_code) return -2;
+            for (uint32_t h = 0; h < host_slots; ++h)
+                if (hfree[h]) {
+                    hfree[h] = 0;
+                    return static_cast<int>(h);
+                }
+            if (!block) return -1;
+            cv.wait(lock);
+        }
+    };
+    auto submit_reads = [&](uint32_t k, uint32_t h) {
+        pend[k].hslot = h;
+        pend[k].ops.assign(T, nullptr);
+        for (int t = 0; t < T; ++t)
+            pend[k].ops[t] = eng.submit_read(plan.key(k, t), hslot_ptr(h, t), tb);
+    };
+    auto drain_reads = [&] {  // error path: never leave I/O into the slots in flight
+        for (auto& p : pend)
+            for (auto*& op : p.ops)
+                if (op) {
+                    try {
+                        eng.wait(op);
+                    } catch (const ma::swp::Failure&) {
+                    }
+                    op = nullptr;
+                }
+    };
+    auto stop_writer = [&] {
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            closing = true;
+        }
+        cv.notify_all();
+        writer.join();
+    };
+    try {
+        std::vector<bool> dused(dev_slots, false);
+        uint64_t chunk_no = 0;
+        for (uint32_t k = 0; k < plan.count; ++k) {
+            const bool keyed = plan.key(k, 0) != nullptr;
+            // keep the read-ahead full: block only for this group's own slot
+            while (next_read < swapped.size()) {
+                const bool mine = swapped[next_read] == k;
+                const int h = claim_slot(mine);
+                if (h == -2) fail(werr_code, werr);
+                if (h < 0) break;
+                submit_reads(swapped[next_read], static_cast<uint32_t>(h));
+                ++next_read;
+            }
+            if (keyed) {
+                for (auto*& op : pend[k].ops) {
+                    ma::swp::Op* o = op;
+                    op = nullptr;
+                    eng.wait(o);
+                }
+            }
+            const uint64_t n = plan.n(k);
+            for (uint64_t off = 0; off < n; off += slot_elems, ++chunk_no) {
+                const uint64_t len = std::min(slot_elems, n - off);
+                const uint32_t d = static_cast<uint32_t>(chunk_no % dev_slots);
+                char* dp[3];
+                char* hp[3];
+                for (int t = 0; t < T; ++t) {
+                    dp[t] = dslot_ptr(d, t);
+                    hp[t] = keyed ? hslot_ptr(pend[k].hslot, t) : plan.host(k, t) + off * E;
+                }
+                if (dused[d]) CK(cudaStreamWaitEvent(hs, dev_ev(d, 2), 0));
+                for (int t = 0; t < T; ++t)
+                    CK(cudaMemcpyAsync(dp[t], hp[t], len * E, cudaMemcpyHostToDevice, hs));
+                CK(cudaEventRecord(dev_ev(d, 0), hs));
+                CK(cudaStreamWaitEvent(cs, dev_ev(d, 0), 0));
+                plan.launch(k, off, len, dp, cs);
+                CK(cudaEventRecord(dev_ev(d, 1), cs));
+                CK(cudaStreamWaitEvent(ds, dev_ev(d, 1), 0));
+                for (int t = 0; t < T; ++t)
+                    CK(cudaMemcpyAsync(hp[t], dp[t], len * E, cudaMemcpyDeviceToHost, ds));
+                CK(cudaEventRecord(dev_ev(d, 2), ds));
+                dused[d] = true;
+            }
+            if (keyed) {
+                CK(cudaEventRecord(host_ev(pend[k].hslot), ds));
+                std::lock_guard<std::mutex> lock(mu);
+                wq.push_back(WB{k, pend[k].hslot});
+                cv.notify_all();
+            }
+        }
+        for (uint32_t d = 0; d < dev_slots; ++d)
+            if (dused[d]) CK(cudaStreamWaitEvent(cs, dev_ev(d, 2), 0));
+    } catch (...) {
+        drain_reads();
+        stop_writer();
+        throw;
+    }
+    stop_writer();
+    if (werr_code) fail(werr_code, werr);
+}
+
+ma::AdamArgs stepper_args(ma_stepper* s) {
+    ma::AdamArgs a{};
+    a.c = s->c;
+    a.skip = &s->d_st->flag;
+    a.st = s->d_st;
+    a.bc_table = s->d_bc;
+    return a;
+}
+
+}  // namespace
+
+extern "C" {
+
 int ma_stepper_apply_swapped(ma_stepper* s, ma_swap* e, const ma_swap_group* groups,
                              uint32_t count, void* h_staging, uint32_t host_slots,
                              float* d_staging, uint32_t dev_slots, uint64_t slot_elems,
                              void* stream, void* h2d_stream, void* d2h_stream, int* skipped) {
     NvtxRange nvtx_range("ma_stepper_apply_swapped");
     return guarded([&] {
-        if (!s || !e) fail(MA_ERR_INVALID_ARGUMENT, "null stepper or swap store");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        if (!d_staging || slot_elems == 0 || dev_slots < 2 || dev_slots > 16)
-            fail(MA_ERR_INVALID_ARGUMENT, "device staging needs 2..16 slots of slot_elems > 0");
-        if (slot_elems % 4) fail(MA_ERR_ALIGNMENT, "slot_elems must be a multiple of 4");
-        const uint64_t tb = (slot_elems * 4 + ma::swp::kGranule - 1) / ma::swp::kGranule *
-                            ma::swp::kGranule;  // one tensor in a host slot
-        uint32_t n_swapped = 0;
-        for (uint32_t k = 0; k < count; ++k) {
+        SwapPlan plan;
+        plan.count = count;
+        plan.ntens = 3;
+        plan.esize = 4;
+        plan.key = [&](uint32_t k, int t) {
+            return t == 0 ? groups[k].key_p : t == 1 ? groups[k].key_m : groups[k].key_v;
+        };
+        plan.host = [&](uint32_t k, int t) {
+            return reinterpret_cast<char*>(t == 0 ? groups[k].p : t == 1 ? groups[k].m : groups[k].v);
+        };
+        plan.n = [&](uint32_t k) { return groups[k].n; };
+        const int gdt = s ? s->g_dtype : 0, wdt = s ? s->w_dtype : 0;
+        const uint64_t ges = elem_bytes(gdt);
+        plan.launch = [&](uint32_t k, uint64_t off, uint64_t len, char* const* d, cudaStream_t st) {
             const ma_swap_group& gr = groups[k];
-            const bool keyed = gr.key_p || gr.key_m || gr.key_v;
-            if (keyed && !(gr.key_p && gr.key_m && gr.key_v))
-                fail(MA_ERR_INVALID_ARGUMENT, "a swapped group needs all three keys");
-            if (keyed && gr.n > slot_elems)
-                fail(MA_ERR_SIZE_VIOLATION, "swapped group " + std::to_string(k) + " has " +
-                                                std::to_string(gr.n) + " elements > slot_elems");
-            if (!keyed && gr.n && !(gr.p && gr.m && gr.v))
-                fail(MA_ERR_INVALID_ARGUMENT, "host-resident group without p/m/v");
-            n_swapped += keyed ? 1 : 0;
-        }
-        if (n_swapped) {
-            if (!h_staging || host_slots < 2)
-                fail(MA_ERR_INVALID_ARGUMENT, "swapped groups need >= 2 host slots");
-            if (reinterpret_cast<uintptr_t>(h_staging) % ma::swp::kGranule)
-                fail(MA_ERR_ALIGNMENT, "host staging must be 4096-aligned");
-            const void* alias;
-            if (classify(h_staging, &alias) != 2)
-                fail(MA_ERR_INVALID_ARGUMENT,
-                     "host staging must be registered host memory (ma_host_register)");
-        }
-        cudaStream_t cs = as_stream(stream);
-        cudaStream_t hs = as_stream(h2d_stream);
-        cudaStream_t ds = as_stream(d2h_stream);
-        // a skipped step reads and writes no optimizer state (simulator.cpp:438-441)
-        uint32_t flag = 0;
-        CK(cudaMemcpyAsync(&flag, &s->d_st->flag, 4, cudaMemcpyDeviceToHost, cs));
-        CK(cudaStreamSynchronize(cs));
-        if (skipped) *skipped = flag ? 1 : 0;
-        s->last = cs;
-        if (flag) return;
-        stepper_grow_bc(s, s->issued + 1);
-        ma::AdamArgs a{};
-        a.c = s->c;
-        a.skip = &s->d_st->flag;
-        a.st = s->d_st;
-        a.bc_table = s->d_bc;
-        int dev = 0;
-        CK(cudaGetDevice(&dev));
-        ma::swp::Engine& eng = *e->e;
-        char* hbase = static_cast<char*>(h_staging);
-        auto hslot_ptr = [&](uint32_t hs_i, int t) {
-            return reinterpret_cast<float*>(hbase + (3ull * hs_i + t) * tb);
+            ma_subgroup part{reinterpret_cast<float*>(d[0]), reinterpret_cast<float*>(d[1]),
+                             reinterpret_cast<float*>(d[2]),
+                             static_cast<const uint8_t*>(gr.g) + off * ges,
+                             gr.w ? static_cast<uint8_t*>(gr.w) + off * 2 : nullptr, len};
+            launch_k2(&part, 1, gdt, wdt, stepper_args(s), st);
         };
-        // events: [0] entry, [1 + 3*d + {0 h2d, 1 k2, 2 d2h}] device slots,
-        // [1 + 3*dev_slots + h] host slot's D2H
-        // (all created here: the writer thread must not touch s->events)
-        s->event(3 * dev_slots + host_slots);
-        const std::vector<cudaEvent_t> evs(s->events.begin(),
-                                           s->events.begin() + 1 + 3 * dev_slots + host_slots);
-        cudaEvent_t entry = evs[0];
-        auto dev_ev = [&](uint32_t d, int kind) { return evs[1 + 3 * d + kind]; };
-        auto host_ev = [&](uint32_t h) { return evs[1 + 3 * dev_slots + h]; };
-        CK(cudaEventRecord(entry, cs));
-        CK(cudaStreamWaitEvent(hs, entry, 0));
+        run_swapped(s, e, plan, h_staging, host_slots, d_staging, dev_slots, slot_elems, stream,
+                    h2d_stream, d2h_stream, skipped);
+    });
+}
 
-        // writer thread: waits for a host slot's D2H, writes master/m/v back,
-        // frees the slot
-        struct WB {
-            uint32_t group, hslot;
-        };
-        std::mutex mu;
-        std::condition_variable cv;
-        std::deque<WB> wq;
-        std::vector<char> hfree(host_slots, 1);
-        bool closing = false;
-        int werr_code = 0;
-        std::string werr;
-        std::thread writer([&] {
-            cudaSetDevice(dev);
-            for (;;) {
-                WB wb;
-                {
-                    std::unique_lock<std::mutex> lock(mu);
-                    cv.wait(lock, [&] { return closing || !wq.empty(); });
-                    if (wq.empty()) return;
-                    wb = wq.front();
-                    wq.pop_front();
-                }
-                int code = 0;
-                std::string msg;
-                NvtxRange wr("ma_swapped_writeback");
-                const cudaError_t ce = cudaEventSynchronize(host_ev(wb.hslot));
-                if (ce != cudaSuccess) {
-                    code = MA_ERR_CUDA;
-                    msg = std::string("cudaEventSynchronize: ") + cudaGetErrorString(ce);
-                } else {
-                    const ma_swap_group& gr = groups[wb.group];
-                    const char* keys[3] = {gr.key_p, gr.key_m, gr.key_v};
-                    ma::swp::Op* ops[3] = {nullptr, nullptr, nullptr};
-                    for (int t = 0; t < 3; ++t) {
-                        try {
-                            ops[t] = eng.submit_write(keys[t], hslot_ptr(wb.hslot, t), tb, gr.n * 4);
-                        } catch (const ma::swp::Failure& f) {
-                            if (!code) code = f.code, msg = f.msg;
-                        }
-                    }
-                    for (int t = 0; t < 3; ++t) {
-                        if (!ops[t]) continue;
-                        try {
-                            eng.wait(ops[t]);
-                        } catch (const ma::swp::Failure& f) {
-                            if (!code) code = f.code, msg = f.msg;
-                        }
-                    }
-                }
-                std::lock_guard<std::mutex> lock(mu);
-                if (code && !werr_code) werr_code = code, werr = msg;
-                hfree[wb.hslot] = 1;
-                cv.notify_all();
-            }
-        });
-
-        // reads: swapped groups in order, each into a free host slot
-        std::vector<uint32_t> swapped;
+int ma_stepper_apply_swapped_bf16(ma_stepper* s, ma_swap* e, const ma_swap_group_bf16* groups,
+                                  uint32_t count, void* h_staging, uint32_t host_slots,
+                                  void* d_staging, uint32_t dev_slots, uint64_t slot_elems,
+                                  void* stream, void* h2d_stream, void* d2h_stream,
+                                  int* skipped) {
+    NvtxRange nvtx_range("ma_stepper_apply_swapped_bf16");
+    return guarded([&] {
+        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
         for (uint32_t k = 0; k < count; ++k)
-            if (groups[k].key_p) swapped.push_back(k);
-        struct Pending {
-            uint32_t hslot = 0;
-            ma::swp::Op* ops[3] = {nullptr, nullptr, nullptr};
+            if (groups[k].n && !groups[k].p)
+                fail(MA_ERR_INVALID_ARGUMENT, "pure-bf16 groups need their device weights");
+        SwapPlan plan;
+        plan.count = count;
+        plan.ntens = 2;
+        plan.esize = 2;
+        plan.key = [&](uint32_t k, int t) { return t == 0 ? groups[k].key_m : groups[k].key_v; };
+        plan.host = [&](uint32_t k, int t) {
+            return reinterpret_cast<char*>(t == 0 ? groups[k].m : groups[k].v);
         };
-        std::vector<Pending> pend(count);
-        size_t next_read = 0;
-        auto claim_slot = [&](bool block) -> int {
-            std::unique_lock<std::mutex> lock(mu);
-            for (;;) {
-                if (werr_code) return -2;
-                for (uint32_t h = 0; h < host_slots; ++h)
-                    if (hfree[h]) {
-                        hfree[h] = 0;
-                        return static_cast<int>(h);
-                    }
-                if (!block) return -1;
-                cv.wait(lock);
-            }
+        plan.n = [&](uint32_t k) { return groups[k].n; };
+        const int gdt = s ? s->g_dtype : 0;
+        const uint64_t ges = elem_bytes(gdt);
+        plan.launch = [&](uint32_t k, uint64_t off, uint64_t len, char* const* d, cudaStream_t st) {
+            const ma_swap_group_bf16& gr = groups[k];
+            ma_subgroup part{reinterpret_cast<float*>(gr.p + off), reinterpret_cast<float*>(d[0]),
+                             reinterpret_cast<float*>(d[1]),
+                             static_cast<const uint8_t*>(gr.g) + off * ges, nullptr, len};
+            launch_k3(&part, 1, gdt, stepper_args(s), st);
         };
-        auto submit_reads = [&](uint32_t k, uint32_t h) {
-            const ma_swap_group& gr = groups[k];
-            pend[k].hslot = h;
-            const char* keys[3] = {gr.key_p, gr.key_m, gr.key_v};
-            for (int t = 0; t < 3; ++t) pend[k].ops[t] = eng.submit_read(keys[t], hslot_ptr(h, t), tb);
-        };
-        auto drain_reads = [&] {  // error path: never leave I/O into the slots in flight
-            for (auto& p : pend)
-                for (auto*& op : p.ops)
-                    if (op) {
-                        try {
-                            eng.wait(op);
-                        } catch (const ma::swp::Failure&) {
-                        }
-                        op = nullptr;
-                    }
-        };
-        auto stop_writer = [&] {
-            {
-                std::lock_guard<std::mutex> lock(mu);
-                closing = true;
-            }
-            cv.notify_all();
-            writer.join();
-        };
-        try {
-            std::vector<bool> dused(dev_slots, false);
-            uint64_t chunk_no = 0;
-            for (uint32_t k = 0; k < count; ++k) {
-                const ma_swap_group& gr = groups[k];
-                const bool keyed = gr.key_p != nullptr;
-                // keep the read-ahead full: block only for this group's own slot
-                while (next_read < swapped.size()) {
-                    const bool mine = swapped[next_read] == k;
-                    const int h = claim_slot(mine);
-                    if (h == -2) fail(werr_code, werr);
-                    if (h < 0) break;
-                    submit_reads(swapped[next_read], static_cast<uint32_t>(h));
-                    ++next_read;
-                }
-                if (keyed) {
-                    for (auto*& op : pend[k].ops) {
-                        ma::swp::Op* o = op;
-                        op = nullptr;
-                        try {
-                            eng.wait(o);
-                        } catch (const ma::swp::Failure& f) {
-                            fail(f.code, f.msg);
-                        }
-                    }
-                }
-                const uint64_t ges = elem_bytes(s->g_dtype);
-                for (uint64_t off = 0; off < gr.n; off += slot_elems, ++chunk_no) {
-                    const uint64_t len = std::min(slot_elems, gr.n - off);
-                    const uint32_t d = static_cast<uint32_t>(chunk_no % dev_slots);
-                    float* sp = d_staging + static_cast<uint64_t>(d) * 3 * slot_elems;
-                    float* sm = sp + slot_elems;
-                    float* sv = sm + slot_elems;
-                    float* hp = keyed ? hslot_ptr(pend[k].hslot, 0) : gr.p + off;
-                    float* hm = keyed ? hslot_ptr(pend[k].hslot, 1) : gr.m + off;
-                    float* hv = keyed ? hslot_ptr(pend[k].hslot, 2) : gr.v + off;
-                    if (dused[d]) CK(cudaStreamWaitEvent(hs, dev_ev(d, 2), 0));
-                    CK(cudaMemcpyAsync(sp, hp, len * 4, cudaMemcpyHostToDevice, hs));
-                    CK(cudaMemcpyAsync(sm, hm, len * 4, cudaMemcpyHostToDevice, hs));
-                    CK(cudaMemcpyAsync(sv, hv, len * 4, cudaMemcpyHostToDevice, hs));
-                    CK(cudaEventRecord(dev_ev(d, 0), hs));
-                    CK(cudaStreamWaitEvent(cs, dev_ev(d, 0), 0));
-                    ma_subgroup part{sp, sm, sv, static_cast<const uint8_t*>(gr.g) + off * ges,
-                                     gr.w ? static_cast<uint8_t*>(gr.w) + off * 2 : nullptr, len};
-                    launch_k2(&part, 1, s->g_dtype, s->w_dtype, a, cs);
-                    CK(cudaEventRecord(dev_ev(d, 1), cs));
-                    CK(cudaStreamWaitEvent(ds, dev_ev(d, 1), 0));
-                    CK(cudaMemcpyAsync(hp, sp, len * 4, cudaMemcpyDeviceToHost, ds));
-                    CK(cudaMemcpyAsync(hm, sm, len * 4, cudaMemcpyDeviceToHost, ds));
-                    CK(cudaMemcpyAsync(hv, sv, len * 4, cudaMemcpyDeviceToHost, ds));
-                    CK(cudaEventRecord(dev_ev(d, 2), ds));
-                    dused[d] = true;
-                }
-                if (keyed) {
-                    CK(cudaEventRecord(host_ev(pend[k].hslot), ds));
-                    std::lock_guard<std::mutex> lock(mu);
-                    wq.push_back(WB{k, pend[k].hslot});
-                    cv.notify_all();
-                }
-            }
-            for (uint32_t d = 0; d < dev_slots; ++d)
-                if (dused[d]) CK(cudaStreamWaitEvent(cs, dev_ev(d, 2), 0));
-        } catch (...) {
-            drain_reads();
-            stop_writer();
-            throw;
-        }
-        stop_writer();
-        if (werr_code) fail(werr_code, werr);
+        run_swapped(s, e, plan, h_staging, host_slots, d_staging, dev_slots, slot_elems, stream,
+                    h2d_stream, d2h_stream, skipped);
     });
 }
 

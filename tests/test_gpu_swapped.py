@@ -130,3 +130,83 @@ def test_swapped_rejects_bad_staging(tmp_path):
     assert ei.value.code == "not-found"
     mab.host_unregister(hstage)
     store.close()
+
+
+def _bf16_run(t, c, sub, mode, tmp_path, fault=None, host_slots=3, dev_slots=2):
+    """Pure-bf16 run of the reference trainer's workload (test_simulator.cpp:44-51):
+    mode "hbm" = K3 over HBM state (ma_stepper_apply_bf16_async), "swapped" =
+    m/v in the store, "mixed" = every other group's m/v in registered DRAM."""
+    n, seed = t["n"], c["seed"]
+    w = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    g = torch.empty(n, dtype=torch.float32, device=DEV)
+    mab.gen_seeded_weights(None, w, n=n, seed=seed)
+    st = mab.Stepper(mab.AdamHyper(), 65536.0, 2000, "f32", "none")
+    offs = list(range(0, n, sub))
+    store = None
+    moved = []
+    if mode == "hbm":
+        m = torch.zeros(n, dtype=torch.int16, device=DEV)
+        v = torch.zeros(n, dtype=torch.int16, device=DEV)
+        groups = [(w[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub]) for o in offs]
+    else:
+        devs = mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 2, 16 << 20)
+        store = mab.DirectIoEngine(devs, backend="auto")
+        zeros = mab.aligned_host_buffer(align4k(sub * 2))
+        zeros[:] = 0
+        groups = []
+        for k, o in enumerate(offs):
+            ln = min(sub, n - o)
+            if mode == "swapped" or k % 2 == 0:
+                for name in ("m", "v"):
+                    store.write_tensor(f"{name}.g{k}", zeros, ln * 2)
+                groups.append(((f"m.g{k}", f"v.g{k}"), w[o:o + ln], g[o:o + ln]))
+            else:
+                mv = (torch.zeros(ln, dtype=torch.int16).pin_memory(),
+                      torch.zeros(ln, dtype=torch.int16).pin_memory())
+                groups.append((mv, w[o:o + ln], g[o:o + ln]))
+        slot = align4k(sub * 2) // 2
+        hstage = mab.aligned_host_buffer(host_slots * 2 * align4k(slot * 2), register=True)
+        dstage = torch.empty(2 * dev_slots * slot, dtype=torch.int16, device=DEV)
+    for s in range(c["steps"]):
+        mab.gen_pseudo_grads(g, w, step=s, seed=seed, d_scale=st.scale_t)
+        if fault and fault[0] == s:
+            mab.plant_bits(g, fault[1], fault[2])
+        st.check(g)
+        if mode == "hbm":
+            st.apply_bf16(groups)
+        else:
+            before = store.stats()["read_requests"]
+            st.apply_swapped_bf16(store, groups, hstage, host_slots, dstage, dev_slots, slot)
+            moved.append(store.stats()["read_requests"] - before)
+        st.finish()
+    torch.cuda.synchronize()
+    out = dict(w=fnv16(w), scale=st.state()["scale"], moved=moved)
+    if store:
+        store.close()
+        mab.host_unregister(hstage)
+    return out
+
+
+@pytest.mark.parametrize("mode", ["swapped", "mixed"])
+@pytest.mark.parametrize("sub", [10007 * 2, 53248])
+def test_swapped_pure_bf16_reference_digest(golden, tmp_path, mode, sub):
+    """Pure-bf16 swapped step (bf16 m/v in the store, weights in HBM, K3)
+    reproduces the reference simulator's pure-bf16 digest bit for bit."""
+    t = golden("trainer.json")
+    c = next(x for x in t["cases"] if x["pure_bf16"])
+    r = _bf16_run(t, c, sub, mode, tmp_path)
+    assert r["w"] == c["sim_digest"]
+    assert r["scale"] == c["final_scale"]
+
+
+def test_swapped_pure_bf16_skip_moves_nothing(golden, tmp_path):
+    """A planted NaN: the swapped run skips the step without touching the
+    store and stays bitwise equal to the in-HBM K3 run."""
+    t = golden("trainer.json")
+    c = next(x for x in t["cases"] if x["pure_bf16"])
+    fault = (3, 4242, 0x7FC00000)
+    a = _bf16_run(t, c, 20014, "hbm", tmp_path, fault)
+    b = _bf16_run(t, c, 20014, "swapped", tmp_path, fault)
+    assert a["w"] == b["w"] and a["scale"] == b["scale"] == 65536.0 / 2
+    groups = (t["n"] + 20013) // 20014
+    assert b["moved"] == [0 if s == 3 else 2 * groups for s in range(c["steps"])]
