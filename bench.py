@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--host-slots", type=int, default=6, help="cfg5 registered host slots")
     ap.add_argument("--io-workers", type=int, default=4, help="cfg5 swap-store workers")
     ap.add_argument("--io-depth", type=int, default=32, help="cfg5 requests in flight per worker")
+    ap.add_argument("--precision", choices=["mixed", "pure_bf16"], default="mixed",
+                    help="cfg5 optimizer state: fp32 master/m/v (K2) or bf16 m/v + bf16 "
+                         "weights (OptimPrecision::pure_bf16, K3)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--flag-exchange", choices=["nccl", "p2p"], default="nccl",
                     help="N>1: all-reduce the skip flag with NCCL, or fuse the exchange into "
@@ -710,6 +713,135 @@ def ours_swapped(args, n, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def ours_swapped_bf16(args, n, rank, world, local_rank):
+    """configs[4] in the reference's pure-bf16 mode (SURVEY §8(f) row 1,
+    simulator.cpp:470-486): bf16 weights in HBM updated in place by K3, bf16
+    m/v of `--swap-gb` worth of sub-groups in the swap store, the rest in the
+    registered DRAM pool.  8 B per swapped parameter on the storage device
+    instead of 24."""
+    import shutil
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_23254_b200 as mab
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    sub = min(SUBGROUP, n)
+    tb = (sub * 2 + 4095) // 4096 * 4096
+    offs = list(range(0, n, sub))
+    G = len(offs)
+    S = min(G, int(args.swap_gb * 1e9 // (2 * tb)))
+    swapped = set(int(i * G / S) for i in range(S)) if S else set()
+    base = rank * n
+    sdir = os.path.join(args.swap_dir, f"rank{rank}")
+    shutil.rmtree(sdir, ignore_errors=True)
+    per_dev = ((2 * tb * len(swapped)) // 2 + (64 << 20)) // 4096 * 4096
+    devs = mab.DirectIoEngine.create_virtual_devices(sdir, 2, per_dev) if swapped else []
+    store = (mab.DirectIoEngine(devs, workers=args.io_workers, queue_depth=args.io_depth)
+             if swapped else None)
+    host_ids = [k for k in range(G) if k not in swapped]
+    n_host = sum(min(sub, n - offs[k]) for k in host_ids)
+    pool = {}
+    for name in ("m", "v"):
+        buf = mab.aligned_host_buffer(max(8, n_host * 2), register=True)
+        buf[:] = 0
+        pool[name] = buf.view(np.uint16)
+    w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    mab.gen_seeded_weights(None, w, n=n, base=base, seed=1)
+    zeros = mab.aligned_host_buffer(tb)
+    zeros[:] = 0
+    groups = []
+    at = 0
+    t_init = time.perf_counter()
+    for k, o in enumerate(offs):
+        ln = min(sub, n - o)
+        if k in swapped:
+            keys = (f"m.g{k}", f"v.g{k}")
+            for key in keys:
+                store.write_tensor(key, zeros, ln * 2)
+            groups.append((keys, w[o:o + ln], g[o:o + ln]))
+        else:
+            groups.append(((pool["m"][at:at + ln], pool["v"][at:at + ln]), w[o:o + ln],
+                           g[o:o + ln]))
+            at += ln
+    t_init = time.perf_counter() - t_init
+    mab.gen_pseudo_grads(g, w, step=0, base=base, seed=1, scale=65536.0)
+    st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "none", device=dev)
+    hslots = args.host_slots
+    hstage = mab.aligned_host_buffer(hslots * 2 * tb, register=True)
+    dstage = torch.empty(2 * args.slots * sub, dtype=torch.int16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step():
+        st.check(g)
+        if world > 1:
+            dist.all_reduce(st.flag, op=dist.ReduceOp.MAX)
+        st.apply_swapped_bf16(store, groups, hstage, hslots, dstage, args.slots, sub)
+        st.finish()
+
+    try:
+        for _ in range(args.warmup):
+            one_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        io0 = store.stats() if store else {}
+        with ClockSampler(local_rank) as clk:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                one_step()
+            b.record(stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+        io1 = store.stats() if store else {}
+        ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms = float(ms.item())
+        backend = store.backend if store else None
+        if store:
+            store.close()
+    finally:
+        shutil.rmtree(sdir, ignore_errors=True)
+    if rank != 0:
+        return
+    pk = storage_peak(args.swap_dir, args.io_workers, args.io_depth)
+    io_bytes = ((io1.get("bytes_read", 0) - io0.get("bytes_read", 0)) +
+                (io1.get("bytes_written", 0) - io0.get("bytes_written", 0))) / args.steps
+    storage_gbs = io_bytes / (ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": n * world / (ms / 1e3), "unit": "params/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (reference generators seeded_weight/pseudo_gradient)",
+        "config": dict(workload_config(args, n, world), optimizer_precision="pure_bf16",
+                       state="bf16 weights in HBM; bf16 m/v split between the O_DIRECT swap "
+                             "store and the registered host pool",
+                       swapped_params=n - n_host, dram_params=n_host,
+                       swapped_groups=len(swapped), groups=G, host_slots=hslots,
+                       dev_slots=args.slots, io_backend=backend, io_workers=args.io_workers,
+                       io_depth=args.io_depth),
+        "storage": {"bound": "swap-device", "achieved": storage_gbs, "unit": "GB/s",
+                    "peak": pk["mixed"], "frac": storage_gbs / pk["mixed"],
+                    "bytes_per_step": io_bytes, "bytes_per_swapped_param": 8,
+                    "peak_read_gbs": pk["read"], "peak_write_gbs": pk["write"],
+                    "peak_source": "measured O_DIRECT through the engine, same settings: 4 x 1 GiB "
+                                   "keys, 2 rewritten while 2 are read"},
+        "host_link": {"achieved": 8 * n / (ms / 1e3) / 1e9, "unit": "GB/s",
+                      "bytes_per_param": 8},
+        "init_seconds": t_init,
+        "gpu_launches": (1 + G + 1) * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -736,6 +868,8 @@ def main():
     try:
         if args.config == "cfg4":
             ours_streamed(args, n, rank, world, local_rank)
+        elif args.config == "cfg5" and args.precision == "pure_bf16":
+            ours_swapped_bf16(args, n, rank, world, local_rank)
         elif args.config == "cfg5":
             ours_swapped(args, n, rank, world, local_rank)
         else:
