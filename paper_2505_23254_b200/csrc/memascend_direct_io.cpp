@@ -186,72 +186,94 @@ DeviceSet DirectIoEngine::create_virtual_devices(const std::string& dir, std::ui
 }
 
 // ------------------------------------------------------------ FsBaselineStore
+namespace {
+
+// Owns one descriptor; every transfer is a full-length positional loop.
+class File {
+public:
+    File(const std::string& path, int flags) : path_(path), fd_(::open(path.c_str(), flags, 0644)) {}
+    ~File() {
+        if (fd_ >= 0) ::close(fd_);
+    }
+    bool ok() const { return fd_ >= 0; }
+    std::uint64_t size() const {
+        struct stat st {};
+        return ::fstat(fd_, &st) == 0 ? static_cast<std::uint64_t>(st.st_size) : 0;
+    }
+    // pwrite until `bytes` are out
+    void put(const std::byte* src, std::uint64_t bytes) {
+        std::uint64_t at = 0;
+        while (at < bytes) {
+            const ssize_t k = ::pwrite(fd_, src + at, bytes - at, static_cast<off_t>(at));
+            if (k <= 0) raise(ErrorCode::io_error, "write to '" + path_ + "' stopped short");
+            at += static_cast<std::uint64_t>(k);
+        }
+    }
+    // pread in `chunk`-sized requests until `bytes` are in (or end of file)
+    std::uint64_t get(std::byte* dst, std::uint64_t bytes, std::uint64_t chunk) {
+        std::uint64_t at = 0;
+        while (at < bytes) {
+            const ssize_t k = ::pread(fd_, dst + at, chunk - at, static_cast<off_t>(at));
+            if (k < 0) raise(ErrorCode::io_error, "read of '" + path_ + "': " + std::strerror(errno));
+            if (k == 0) break;
+            at += static_cast<std::uint64_t>(k);
+        }
+        return at;
+    }
+    void truncate(std::uint64_t bytes) {
+        if (::ftruncate(fd_, static_cast<off_t>(bytes)) != 0)
+            raise(ErrorCode::io_error, "cannot set the length of '" + path_ + "'");
+    }
+
+private:
+    std::string path_;
+    int fd_;
+};
+
+void require_granule_aligned(const void* p, const std::string& what) {
+    if (reinterpret_cast<std::uintptr_t>(p) % kIoGranule)
+        raise(ErrorCode::alignment, what + " is not 4096-aligned");
+}
+
+}  // namespace
+
 FsBaselineStore::FsBaselineStore(std::string dir, bool cache_bypass)
     : dir_(std::move(dir)), cache_bypass_(cache_bypass) {
     std::filesystem::create_directories(dir_);
 }
 
 std::string FsBaselineStore::path_for(const std::string& key) const {
-    std::string name;
-    for (char c : key) name.push_back(std::isalnum(static_cast<unsigned char>(c)) ? c : '_');
-    return dir_ + "/" + name + ".tensor";
+    std::string file = dir_ + "/";
+    for (unsigned char c : key) file += std::isalnum(c) ? static_cast<char>(c) : '_';
+    return file + ".tensor";
 }
 
 void FsBaselineStore::write(const std::string& key, std::span<const std::byte> src,
                             std::uint64_t logical_bytes) {
     if (logical_bytes == 0)
-        raise(ErrorCode::invalid_argument, "zero-length write for '" + key + "' (min 4096 on disk)");
-    if (reinterpret_cast<std::uintptr_t>(src.data()) % kIoGranule)
-        raise(ErrorCode::alignment, "write source for '" + key + "' is not 4096-aligned");
+        raise(ErrorCode::invalid_argument, "'" + key + "': a tensor file holds at least one byte");
+    require_granule_aligned(src.data(), "source buffer of '" + key + "'");
     const std::uint64_t padded = align_up(logical_bytes, kIoGranule);
     if (src.size() < padded)
-        raise(ErrorCode::size_violation, "write source must cover the padded length");
-    const std::string path = path_for(key);
-    const int fd = ::open(path.c_str(), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC |
-                                            (cache_bypass_ ? O_DIRECT : 0), 0644);
-    if (fd < 0) raise(ErrorCode::io_error, "cannot open '" + path + "': " + std::strerror(errno));
-    for (std::uint64_t done = 0; done < padded;) {
-        const ssize_t n = ::pwrite(fd, src.data() + done, padded - done, static_cast<off_t>(done));
-        if (n <= 0) {
-            ::close(fd);
-            raise(ErrorCode::io_error, "short write to '" + path + "'");
-        }
-        done += static_cast<std::uint64_t>(n);
-    }
-    // the file length records the logical size
-    if (::ftruncate(fd, static_cast<off_t>(logical_bytes)) != 0) {
-        ::close(fd);
-        raise(ErrorCode::io_error, "ftruncate failed on '" + path + "'");
-    }
-    ::close(fd);
+        raise(ErrorCode::size_violation, "source buffer of '" + key + "' is shorter than " +
+                                             std::to_string(padded) + " bytes");
+    File f(path_for(key), O_CREAT | O_WRONLY | O_TRUNC | O_CLOEXEC | (cache_bypass_ ? O_DIRECT : 0));
+    if (!f.ok()) raise(ErrorCode::io_error, "open '" + path_for(key) + "': " + std::strerror(errno));
+    f.put(src.data(), padded);  // O_DIRECT moves whole granules ...
+    f.truncate(logical_bytes);  // ... and the length records the logical size
 }
 
 std::uint64_t FsBaselineStore::read(const std::string& key, std::span<std::byte> dst) {
-    if (reinterpret_cast<std::uintptr_t>(dst.data()) % kIoGranule)
-        raise(ErrorCode::alignment, "read destination for '" + key + "' is not 4096-aligned");
-    const std::string path = path_for(key);
-    const int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC | (cache_bypass_ ? O_DIRECT : 0));
-    if (fd < 0) raise(ErrorCode::not_found, "no tensor file '" + path + "'");
-    struct stat st {};
-    ::fstat(fd, &st);
-    const std::uint64_t logical = static_cast<std::uint64_t>(st.st_size);
+    require_granule_aligned(dst.data(), "destination buffer of '" + key + "'");
+    File f(path_for(key), O_RDONLY | O_CLOEXEC | (cache_bypass_ ? O_DIRECT : 0));
+    if (!f.ok()) raise(ErrorCode::not_found, "'" + key + "' has no tensor file");
+    const std::uint64_t logical = f.size();
     const std::uint64_t padded = align_up(logical, kIoGranule);
-    if (dst.size() < padded) {
-        ::close(fd);
-        raise(ErrorCode::size_violation, "read destination must cover the padded length");
-    }
-    std::uint64_t done = 0;
-    while (done < logical) {
-        const ssize_t n = ::pread(fd, dst.data() + done, padded - done, static_cast<off_t>(done));
-        if (n < 0) {
-            ::close(fd);
-            raise(ErrorCode::io_error, "read failed on '" + path + "': " + std::strerror(errno));
-        }
-        if (n == 0) break;
-        done += static_cast<std::uint64_t>(n);
-    }
-    ::close(fd);
-    if (done < logical) raise(ErrorCode::io_error, "short read on '" + path + "'");
+    if (dst.size() < padded)
+        raise(ErrorCode::size_violation, "destination buffer of '" + key + "' is shorter than " +
+                                             std::to_string(padded) + " bytes");
+    if (f.get(dst.data(), logical, padded) < logical)
+        raise(ErrorCode::io_error, "'" + key + "' ended before its recorded length");
     return logical;
 }
 
