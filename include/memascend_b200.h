@@ -229,6 +229,19 @@ MA_API int ma_rs_error(ma_rs* r, int* timed_out);
 MA_API int ma_rs_destroy(ma_rs* r);
 MA_API int ma_stepper_reduce_scatter_async(ma_stepper* s, ma_rs* r, uint64_t base, uint64_t n,
                                            float post_scale, void* dst, void* stream);
+/* Update fused with the weight all-gather (the collective that follows the
+ * optimizer step in ZeRO data parallelism: every rank needs every partition's
+ * new working weights for the next forward).  `ag` is an ma_rs created over
+ * each rank's FULL-LENGTH working-weight buffer (dtype = the stepper's
+ * w_dtype) and opened with all ranks' records.  groups[k].w must lie inside
+ * this rank's buffer; K2 stores every updated working weight into this
+ * rank's buffer AND, over NVLink through the IPC mappings, at the same offset
+ * into every peer's buffer — no separate all-gather pass, the peer stores
+ * overlap the HBM-bound update.  An entry barrier (all ranks are done with
+ * the previous weights) and an exit barrier (all pushes complete) bracket it;
+ * a skipped step stores nothing anywhere.  At most 8 ranks. */
+MA_API int ma_stepper_apply_allgather_async(ma_stepper* s, const ma_subgroup* groups,
+                                            uint32_t count, ma_rs* ag, void* stream);
 /* Device uint32 holding this step's overflow flag (for the cross-rank OR). */
 MA_API uint32_t* ma_stepper_flag(ma_stepper* s);
 /* Device float holding the current loss scale (gradient producers read it). */

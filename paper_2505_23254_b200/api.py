@@ -237,6 +237,14 @@ class Stepper:
         arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
         check(capi.lib().ma_stepper_apply_async(self._h, arr, len(arr), _stream_ptr(stream)))
 
+    def apply_allgather(self, groups, ag: "GradReduceScatter", stream=None):
+        """K2 fused with the weight all-gather: `ag` shares every rank's
+        full-length working-weight buffer (a GradReduceScatter over it);
+        groups' w are views of this rank's buffer."""
+        arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
+        check(capi.lib().ma_stepper_apply_allgather_async(self._h, arr, len(arr), ag._h,
+                                                          _stream_ptr(stream)))
+
     def apply_bf16(self, groups, stream=None):
         """Pure-bf16 mode: groups of (p_bf16, m_bf16, v_bf16, g) tensors (K3)."""
         arr = (capi.SubgroupBf16 * len(groups))()

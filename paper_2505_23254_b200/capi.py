@@ -135,6 +135,7 @@ SIGNATURES = [
     ("ma_rs_error", _I, [_VP, C.POINTER(_I)]),
     ("ma_rs_destroy", _I, [_VP]),
     ("ma_stepper_reduce_scatter_async", _I, [_VP, _VP, _U64, _U64, _F, _VP, _VP]),
+    ("ma_stepper_apply_allgather_async", _I, [_VP, C.POINTER(Subgroup), _U32, _VP, _VP]),
     ("ma_stepper_flag", _VP, [_VP]),
     ("ma_stepper_scale", _VP, [_VP]),
     ("ma_stepper_apply_async", _I, [_VP, C.POINTER(Subgroup), _U32, _VP]),

@@ -298,9 +298,11 @@ uint64_t oneshot_grid(const ma::SegTable& tab, int vec, uint64_t scalar_elems, u
 }
 
 void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, const ma::AdamArgs& a,
-               cudaStream_t st) {
+               cudaStream_t st, bool allgather = false) {
     const DeviceInfo d = device_info();
-    const int variant = ma::k2_effective_variant(gdt, wdt, k2_variant());
+    // the fused all-gather runs in the production one-shot shape (variant 14)
+    const int variant = allgather ? ma::kK2DefaultVariant
+                                  : ma::k2_effective_variant(gdt, wdt, k2_variant());
     int vec, tile_vectors;
     bool stream;
     ma::k2_variant_shape(variant, &vec, &tile_vectors, &stream);
@@ -334,7 +336,10 @@ void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, cons
             }
             grid = std::max<uint64_t>(grid, 1);
         }
-        ma::launch_k2(gdt, wdt, variant, tab, a, static_cast<unsigned>(grid), st);
+        if (allgather)
+            ma::launch_k2_allgather(gdt, wdt, tab, a, static_cast<unsigned>(grid), st);
+        else
+            ma::launch_k2(gdt, wdt, variant, tab, a, static_cast<unsigned>(grid), st);
         CK(cudaGetLastError());
     }
 }
@@ -1768,6 +1773,54 @@ int ma_stepper_reduce_scatter_async(ma_stepper* s, ma_rs* r, uint64_t base, uint
         alignas(16) static const uint32_t dummy[4] = {0, 0, 0, 0};  // never written (n == 0)
         launch_reduce(s, srcs.data(), world, r->dtype, n, post_scale, n ? dst : const_cast<uint32_t*>(dummy),
                       r->x->d_desc, r->x->epoch, st);
+        s->last = st;
+    });
+}
+
+int ma_stepper_apply_allgather_async(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
+                                     ma_rs* ag, void* stream) {
+    NvtxRange nvtx_range("ma_stepper_apply_allgather_async");
+    return guarded([&] {
+        if (!s || !ag) fail(MA_ERR_INVALID_ARGUMENT, "null stepper / peer weight set");
+        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
+        if (!ag->ready) fail(MA_ERR_LIFECYCLE, "peer weight set not opened (ma_rs_open)");
+        if (s->w_dtype == MA_DT_NONE || ag->dtype != s->w_dtype)
+            fail(MA_ERR_INVALID_ARGUMENT,
+                 "the peer buffers must hold the stepper's working-weight kind");
+        const int world = ag->x->world, rank = ag->x->rank;
+        if (world - 1 > ma::kMaxAgPeers)
+            fail(MA_ERR_INVALID_ARGUMENT, "the fused all-gather spans at most 8 ranks");
+        const char* local = static_cast<const char*>(ag->grads[rank]);
+        const char* local_end = local + ag->n_total * 2;
+        for (uint32_t k = 0; k < count; ++k) {
+            if (groups[k].n == 0) continue;
+            const char* w = static_cast<const char*>(groups[k].w);
+            if (!w || w < local || w + groups[k].n * 2 > local_end)
+                fail(MA_ERR_INVALID_ARGUMENT, "sub-group " + std::to_string(k) +
+                                                  "'s working weights are not inside this "
+                                                  "rank's shared weight buffer");
+        }
+        const cudaStream_t st = as_stream(stream);
+        stepper_grow_bc(s, s->issued + 1);
+        ma::AdamArgs a{};
+        a.c = s->c;
+        a.skip = &s->d_st->flag;
+        a.st = s->d_st;
+        a.bc_table = s->d_bc;
+        for (int k = 0; k < world; ++k)
+            if (k != rank)
+                a.peers.delta[a.peers.n++] =
+                    static_cast<long long>(static_cast<const char*>(ag->grads[k]) - local);
+        // entry: every rank is done with its copy of the previous weights
+        // (a rank missing here forces this rank's skip, like the exchange)
+        ag->x->epoch += 1;
+        ma::launch_peer_barrier(ag->x->d_desc, ag->x->epoch, &s->d_st->flag, st);
+        CK(cudaGetLastError());
+        launch_k2(groups, count, s->g_dtype, s->w_dtype, a, st, /*allgather=*/true);
+        // exit: every rank's pushes into every buffer are complete
+        ag->x->epoch += 1;
+        ma::launch_peer_barrier(ag->x->d_desc, ag->x->epoch, nullptr, st);
+        CK(cudaGetLastError());
         s->last = st;
     });
 }

@@ -334,15 +334,35 @@ __device__ __forceinline__ float load_grad1(const void* g, uint64_t e) {
     return widen<GK>(reinterpret_cast<const uint16_t*>(g)[e]);
 }
 
-template <int GK, int WK>
+// working-weight stores; with AG also into every peer's weight buffer
+// (fully unrolled over the peer slots so the deltas stay kernel parameters)
+template <int AG, typename T>
+__device__ __forceinline__ void store_w(T* dst, T val, const PeerW& pw) {
+    if constexpr (sizeof(T) >= 8) {
+        __stcs(dst, val);
+    } else {
+        *dst = val;
+    }
+    if constexpr (AG != 0) {
+#pragma unroll
+        for (int r = 0; r < kMaxAgPeers; ++r)
+            if (r < static_cast<int>(pw.n))
+                *reinterpret_cast<T*>(reinterpret_cast<char*>(dst) + pw.delta[r]) = val;
+    }
+}
+
+__device__ __constant__ PeerW kNoPeers = {};
+
+template <int GK, int WK, int AG = 0>
 __device__ __forceinline__ void adam_scalar(const Seg& sg, uint64_t e, const AdamConsts& c,
-                                            const StepScalars& s) {
+                                            const StepScalars& s, const PeerW& pw = kNoPeers) {
     float p = sg.p[e], m = sg.m[e], v = sg.v[e];
     adam_elem(p, m, v, load_grad1<GK>(sg.g, e), c, s);
     sg.p[e] = p;
     sg.m[e] = m;
     sg.v[e] = v;
-    if constexpr (WK != kNone) reinterpret_cast<uint16_t*>(sg.w)[e] = narrow<WK>(p);
+    if constexpr (WK != kNone)
+        store_w<AG>(reinterpret_cast<uint16_t*>(sg.w) + e, narrow<WK>(p), pw);
 }
 
 template <int GK, int WK, int VEC>
@@ -460,9 +480,10 @@ __device__ __forceinline__ void load_slot(const Seg& sg, uint64_t e, Slot4& s) {
 
 // MATH: 0 = production (hoisted-guard fast path, exact fallback), 1 = probe
 // (approximate div/sqrt, never production), 2 = exact intrinsics only (A/B)
-template <int GK, int WK, int MATH = 0>
+template <int GK, int WK, int MATH = 0, int AG = 0>
 __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
-                                            const AdamConsts& c, const StepScalars& sc) {
+                                            const AdamConsts& c, const StepScalars& sc,
+                                            const PeerW& pw = kNoPeers) {
     float g0, g1, g2, g3;
     if constexpr (GK == kF32) {
         g0 = __uint_as_float(s.g.x);
@@ -496,8 +517,9 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
             __stcs(reinterpret_cast<float4*>(sg.m + e), make_float4(m[0], m[1], m[2], m[3]));
             __stcs(reinterpret_cast<float4*>(sg.v + e), make_float4(v[0], v[1], v[2], v[3]));
             if constexpr (WK != kNone) {
-                __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.w) + e),
-                       make_uint2(narrow2_num<WK>(p[0], p[1]), narrow2_num<WK>(p[2], p[3])));
+                store_w<AG>(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.w) + e),
+                            make_uint2(narrow2_num<WK>(p[0], p[1]), narrow2_num<WK>(p[2], p[3])),
+                            pw);
             }
             return;
         }
@@ -513,7 +535,8 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
     if constexpr (WK != kNone) {
         const uint32_t lo = narrow2<WK>(s.p.x, s.p.y);
         const uint32_t hi = narrow2<WK>(s.p.z, s.p.w);
-        __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.w) + e), make_uint2(lo, hi));
+        store_w<AG>(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.w) + e),
+                    make_uint2(lo, hi), pw);
     }
 }
 
@@ -608,7 +631,7 @@ __device__ __forceinline__ uint32_t seg_of_tile(const SegTable& tab, uint64_t t)
     return lo;
 }
 
-template <int GK, int WK, int U, int MATH = 0, int MINB = 1>
+template <int GK, int WK, int U, int MATH = 0, int MINB = 1, int AG = 0>
 __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, AdamArgs a) {
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
@@ -637,7 +660,7 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, Ada
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (full || j0 + u * kK2Threads < nv) {
-                update_slot<GK, WK, MATH>(loc, 4 * u * kK2Threads, cur[u], c, sc);
+                update_slot<GK, WK, MATH, AG>(loc, 4 * u * kK2Threads, cur[u], c, sc, a.peers);
             }
         }
         return;
@@ -652,11 +675,12 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, Ada
             const uint64_t tail_begin = sg.head + sg.nvec * 4;
             const uint64_t extra = sg.head + (sg.n - tail_begin);
             for (uint64_t i = threadIdx.x; i < extra; i += blockDim.x) {
-                adam_scalar<GK, WK>(sg, i < sg.head ? i : tail_begin + (i - sg.head), c, sc);
+                adam_scalar<GK, WK, AG>(sg, i < sg.head ? i : tail_begin + (i - sg.head), c, sc,
+                                        a.peers);
             }
         } else {
             for (uint64_t e = q * blockDim.x + threadIdx.x; e < sg.n; e += nq * blockDim.x) {
-                adam_scalar<GK, WK>(sg, e, c, sc);
+                adam_scalar<GK, WK, AG>(sg, e, c, sc, a.peers);
             }
         }
     }
@@ -1534,6 +1558,18 @@ void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs&
         K2Kernel<decltype(G)::value, decltype(W)::value, decltype(V)::value>::fn
             <<<grid, kK2Threads, 0, st>>>(tab, a);
     });
+}
+
+void launch_k2_allgather(int gk, int wk, const SegTable& tab, const AdamArgs& a, unsigned grid,
+                         cudaStream_t st) {
+#define MA_AG(G, W)                                                                    \
+    if (gk == G && wk == W) {                                                          \
+        k2_oneshot<G, W, 4, 0, 1, 1><<<grid, kK2Threads, 0, st>>>(tab, a);             \
+        return;                                                                        \
+    }
+    MA_AG(kF32, kBF16) MA_AG(kF32, kF16) MA_AG(kBF16, kBF16) MA_AG(kBF16, kF16)
+    MA_AG(kF16, kBF16) MA_AG(kF16, kF16)
+#undef MA_AG
 }
 
 // K3 A/B (MA_K3_VARIANT): 0 = 4 slots held to 4 CTA/SM (64 regs,

@@ -66,6 +66,16 @@ struct SegTable {
     uint64_t total_tiles;
 };
 
+// Fused weight all-gather (ma_stepper_apply_allgather_async): K2 also
+// stores each rank's updated working weights into every peer's full-length
+// weight buffer over NVLink (CUDA IPC mappings); delta[r] is the byte offset
+// from a local working-weight address to the same element in peer r's buffer.
+constexpr int kMaxAgPeers = 7;  // one NVSwitch box: 8 ranks
+struct PeerW {
+    long long delta[kMaxAgPeers];
+    uint32_t n;
+};
+
 struct AdamArgs {
     AdamConsts c;
     // explicit step (ma_adam_step*): used when st == nullptr
@@ -73,6 +83,7 @@ struct AdamArgs {
     const uint32_t* skip;    // optional skip flag
     const StepDev* st;       // optional device-resident scaler
     const float2* bc_table;  // (1-b1^t, 1-b2^t) for t = 1.. when st != nullptr
+    PeerW peers;             // fused all-gather targets (launch_k2_allgather only)
 };
 
 // Host-side launchers (defined next to the kernels in kernels.cu so every
@@ -93,6 +104,9 @@ void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream);
 // one tile per CTA: grid = total_tiles + trailing CTAs for the scalar remainder
 bool k2_variant_oneshot(int variant);
 int k2_blocks_per_sm(int gk, int wk, int variant);
+// K2 (production one-shot shape) with the fused weight all-gather
+void launch_k2_allgather(int gk, int wk, const SegTable& tab, const AdamArgs& a, unsigned grid,
+                         cudaStream_t st);
 void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st);
 // K3 (bf16 state): Seg p/m/v point at uint16 arrays; one tile of
