@@ -663,6 +663,8 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, Ada
                 update_slot<GK, WK, MATH, AG>(loc, 4 * u * kK2Threads, cur[u], c, sc, a.peers);
             }
         }
+        // peer stores reach system scope before the exit barrier's release
+        if constexpr (AG != 0) __threadfence_system();
         return;
     }
     // trailing CTAs: unaligned heads/tails and non-co-alignable sub-groups
@@ -684,6 +686,7 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, Ada
             }
         }
     }
+    if constexpr (AG != 0) __threadfence_system();
 }
 
 // -------------------------------------------------------------- K2 TMA
