@@ -109,6 +109,79 @@ __global__ void __launch_bounds__(kThreads) probe_oneshot(float* __restrict__ p,
     }
 }
 
+// 256-bit global accesses (sm_100: LDG.E.256 / STG.E.256)
+struct F8 {
+    float x[8];
+};
+__device__ __forceinline__ F8 ld256(const float* p) {
+    F8 r;
+    asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
+                   "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st256(float* p, const F8& r) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.x[0]),
+                 "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]), "f"(r.x[5]), "f"(r.x[6]),
+                 "f"(r.x[7])
+                 : "memory");
+}
+
+template <int U>
+__global__ void copy_oneshot256(const float* __restrict__ a, float* __restrict__ b, uint64_t n8) {
+    const uint64_t base = blockIdx.x * static_cast<uint64_t>(blockDim.x) * U + threadIdx.x;
+    F8 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint64_t i = base + u * blockDim.x;
+        if (i < n8) r[u] = ld256(a + 8 * i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint64_t i = base + u * blockDim.x;
+        if (i < n8) st256(b + 8 * i, r[u]);
+    }
+}
+
+// the 5-stream pattern with 8-element slots: p/m/v by 32-byte accesses,
+// g/w by 16-byte ones
+template <int U>
+__global__ void __launch_bounds__(kThreads) probe_oneshot256(float* __restrict__ p,
+                                                             float* __restrict__ m,
+                                                             float* __restrict__ v,
+                                                             const uint16_t* __restrict__ g,
+                                                             uint16_t* __restrict__ w,
+                                                             uint64_t nslots8) {
+    const uint64_t base = blockIdx.x * static_cast<uint64_t>(blockDim.x) * U + threadIdx.x;
+    F8 a[U], b[U], c[U];
+    uint4 gg[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint64_t j = base + u * blockDim.x;
+        if (j < nslots8) {
+            a[u] = ld256(p + 8 * j);
+            b[u] = ld256(m + 8 * j);
+            c[u] = ld256(v + 8 * j);
+            gg[u] = __ldcs(reinterpret_cast<const uint4*>(g) + j);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint64_t j = base + u * blockDim.x;
+        if (j < nslots8) {
+            const float d = __uint_as_float(gg[u].x << 16) * 1e-9f;
+            a[u].x[0] += d; b[u].x[1] += d; c[u].x[2] += d;
+            st256(p + 8 * j, a[u]);
+            st256(m + 8 * j, b[u]);
+            st256(v + 8 * j, c[u]);
+            __stcs(reinterpret_cast<uint4*>(w) + j,
+                   make_uint4(__float_as_uint(a[u].x[0]) >> 16, __float_as_uint(a[u].x[2]) >> 16,
+                              __float_as_uint(a[u].x[4]) >> 16, __float_as_uint(a[u].x[6]) >> 16));
+        }
+    }
+}
+
 int main() {
     const uint64_t n = 1ull << 31;  // 2 Gi elements: 56 GiB of traffic per pass
     float *state, *p, *m, *v;
@@ -172,5 +245,16 @@ int main() {
          28.0 * n, "one-shot 5-stream U2");
     time([&] { probe_oneshot<4><<<(nslots + 1023) / 1024, kThreads>>>(p, m, v, g, w, nslots); },
          28.0 * n, "one-shot 5-stream U4");
+    const uint64_t n8 = n / 8;
+    time([&] { copy_oneshot256<2><<<(n8 + 511) / 512, 256>>>(p, m, n8); }, 8.0 * n,
+         "one-shot copy 256-bit U2");
+    time([&] { copy_oneshot256<4><<<(n8 + 1023) / 1024, 256>>>(p, m, n8); }, 8.0 * n,
+         "one-shot copy 256-bit U4");
+    time([&] { probe_oneshot256<1><<<(n8 + 255) / 256, kThreads>>>(p, m, v, g, w, n8); },
+         28.0 * n, "one-shot 5-stream 256-bit U1");
+    time([&] { probe_oneshot256<2><<<(n8 + 511) / 512, kThreads>>>(p, m, v, g, w, n8); },
+         28.0 * n, "one-shot 5-stream 256-bit U2");
+    time([&] { probe_oneshot256<4><<<(n8 + 1023) / 1024, kThreads>>>(p, m, v, g, w, n8); },
+         28.0 * n, "one-shot 5-stream 256-bit U4");
     return 0;
 }
