@@ -352,7 +352,7 @@ void launch_k3(const ma_subgroup* groups, uint32_t count, int gdt, const ma::Ada
         const char* e = std::getenv("MA_K3_VARIANT");  // A/B only
         return e ? std::atoi(e) : 0;
     }();
-    constexpr int kVec = 4;
+    const int kVec = ma::k3_vec(gdt, variant);
     const int kTile = ma::k3_slots(gdt, variant) * ma::kK2Threads;
     const uint64_t cap = static_cast<uint64_t>(d.sms) * ma::k3_blocks_per_sm(gdt, variant);
     for (uint32_t first = 0; first < count; first += ma::kMaxSegs) {

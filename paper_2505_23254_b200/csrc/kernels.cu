@@ -971,6 +971,116 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_adam_bf16(SegTable tab, A
     }
 }
 
+// K3 with 8-element slots (A/B variants 4/5): one 16-byte access per thread
+// for each of p, m, v and a bf16 gradient slot (two for fp32 gradients),
+// half the memory instructions of the 4-element slots; the arithmetic and
+// its order are unchanged (adam_fast<8> / adam_elem per element).
+struct Slot8 {
+    uint4 p, m, v;
+    uint4 g[2];
+};
+
+__device__ __forceinline__ void unpack8(const uint4& q, float (&x)[8]) {
+    x[0] = widen_bf16(q.x & 0xFFFFu); x[1] = widen_bf16(q.x >> 16);
+    x[2] = widen_bf16(q.y & 0xFFFFu); x[3] = widen_bf16(q.y >> 16);
+    x[4] = widen_bf16(q.z & 0xFFFFu); x[5] = widen_bf16(q.z >> 16);
+    x[6] = widen_bf16(q.w & 0xFFFFu); x[7] = widen_bf16(q.w >> 16);
+}
+
+template <bool NUM>
+__device__ __forceinline__ uint4 pack8(const float (&x)[8]) {
+    if constexpr (NUM)
+        return make_uint4(narrow2_num<kBF16>(x[0], x[1]), narrow2_num<kBF16>(x[2], x[3]),
+                          narrow2_num<kBF16>(x[4], x[5]), narrow2_num<kBF16>(x[6], x[7]));
+    return make_uint4(narrow2<kBF16>(x[0], x[1]), narrow2<kBF16>(x[2], x[3]),
+                      narrow2<kBF16>(x[4], x[5]), narrow2<kBF16>(x[6], x[7]));
+}
+
+template <int GK, int U, int MINB>
+__global__ void __launch_bounds__(kK2Threads, MINB) k3_adam_bf16_v8(SegTable tab, AdamArgs a) {
+    StepScalars sc;
+    if (!resolve_step(a, sc)) return;
+    const AdamConsts c = a.c;
+    constexpr uint32_t kGB = GK == kF32 ? 4u : 2u;
+    const uint64_t t = blockIdx.x;
+    if (t < tab.total_tiles) {
+        const Seg& sg = tab.seg[seg_of_tile(tab, t)];
+        const uint64_t lt = t - sg.tile_begin;
+        const uint64_t j0 = lt * (U * kK2Threads) + threadIdx.x;
+        const uint64_t e0 = sg.head + 8 * j0;
+        uint16_t* P = reinterpret_cast<uint16_t*>(sg.p) + e0;
+        uint16_t* M = reinterpret_cast<uint16_t*>(sg.m) + e0;
+        uint16_t* V = reinterpret_cast<uint16_t*>(sg.v) + e0;
+        const uint8_t* G = static_cast<const uint8_t*>(sg.g) + e0 * kGB;
+        const uint64_t nv = sg.nvec;
+        const bool full = (lt + 1) * (U * kK2Threads) <= nv;
+        Slot8 q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (full || j0 + u * kK2Threads < nv) {
+                const int o = 8 * u * kK2Threads;
+                q[u].p = __ldcs(reinterpret_cast<const uint4*>(P + o));
+                q[u].m = __ldcs(reinterpret_cast<const uint4*>(M + o));
+                q[u].v = __ldcs(reinterpret_cast<const uint4*>(V + o));
+                q[u].g[0] = __ldcs(reinterpret_cast<const uint4*>(G + o * kGB));
+                if constexpr (GK == kF32) q[u].g[1] = __ldcs(reinterpret_cast<const uint4*>(G + o * kGB) + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (full || j0 + u * kK2Threads < nv) {
+                const int o = 8 * u * kK2Threads;
+                float g[8], p[8], m[8], v[8];
+                if constexpr (GK == kF32) {
+                    const uint32_t w[8] = {q[u].g[0].x, q[u].g[0].y, q[u].g[0].z, q[u].g[0].w,
+                                           q[u].g[1].x, q[u].g[1].y, q[u].g[1].z, q[u].g[1].w};
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) g[k] = __uint_as_float(w[k]);
+                } else {
+                    const uint32_t w[4] = {q[u].g[0].x, q[u].g[0].y, q[u].g[0].z, q[u].g[0].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        g[2 * k] = widen<GK>(w[k] & 0xFFFFu);
+                        g[2 * k + 1] = widen<GK>(w[k] >> 16);
+                    }
+                }
+                unpack8(q[u].p, p);
+                unpack8(q[u].m, m);
+                unpack8(q[u].v, v);
+                if (sc.fast && adam_fast<8>(p, m, v, g, c, sc)) {
+                    __stcs(reinterpret_cast<uint4*>(P + o), pack8<true>(p));
+                    __stcs(reinterpret_cast<uint4*>(M + o), pack8<true>(m));
+                    __stcs(reinterpret_cast<uint4*>(V + o), pack8<true>(v));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) adam_elem(p[k], m[k], v[k], g[k], c, sc);
+                    __stcs(reinterpret_cast<uint4*>(P + o), pack8<false>(p));
+                    __stcs(reinterpret_cast<uint4*>(M + o), pack8<false>(m));
+                    __stcs(reinterpret_cast<uint4*>(V + o), pack8<false>(v));
+                }
+            }
+        }
+        return;
+    }
+    const uint64_t q0 = t - tab.total_tiles;
+    const uint64_t nq = gridDim.x - tab.total_tiles;
+    for (uint32_t k = 0; k < tab.count; ++k) {
+        const Seg& sg = tab.seg[k];
+        if (sg.vector_ok) {
+            if (q0 != k % nq) continue;
+            const uint64_t tail_begin = sg.head + sg.nvec * 8;
+            const uint64_t extra = sg.head + (sg.n - tail_begin);
+            for (uint64_t q = threadIdx.x; q < extra; q += blockDim.x) {
+                bf16_state_scalar<GK>(sg, q < sg.head ? q : tail_begin + (q - sg.head), c, sc);
+            }
+        } else {
+            for (uint64_t e = q0 * blockDim.x + threadIdx.x; e < sg.n; e += nq * blockDim.x) {
+                bf16_state_scalar<GK>(sg, e, c, sc);
+            }
+        }
+    }
+}
+
 // ============================================================== step finish
 // LossScaler::on_overflow / on_clean_step (optimizer.hpp:24-34) and the
 // update counter (simulator.cpp:438-444,491); re-arms the flag.
@@ -1577,11 +1687,14 @@ void launch_k2_allgather(int gk, int wk, const SegTable& tab, const AdamArgs& a,
 
 // K3 A/B (MA_K3_VARIANT): 0 = 4 slots held to 4 CTA/SM (64 regs,
 // production for bf16 gradients, 0.94), 1 = 4 slots unbounded (80 regs,
-// 3 CTA/SM, 0.90), 2 = 2 slots at 4 CTA/SM (0.84), 3 = 8 slots (0.89).
+// 3 CTA/SM, 0.90), 2 = 2 slots at 4 CTA/SM (0.84), 3 = 8 slots (0.89),
+// 4 = 8-element slots at 4 CTA/SM (0.90, spills), 5 = 8-element unbounded (0.80).
 int k3_slots(int gk, int variant) {
     if (gk != kBF16) return kK3Slots;
-    return variant == 2 ? 2 : variant == 3 ? 8 : kK3Slots;
+    return variant == 2 ? 2 : variant == 3 ? 8 : (variant == 4 || variant == 5) ? 2 : kK3Slots;
 }
+
+int k3_vec(int gk, int variant) { return gk == kBF16 && (variant == 4 || variant == 5) ? 8 : 4; }
 
 template <typename F>
 void k3_dispatch(int gk, int variant, F&& f) {
@@ -1591,6 +1704,8 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 1: return f(k3_adam_bf16<kBF16, 4, 1>);
         case 2: return f(k3_adam_bf16<kBF16, 2, 4>);
         case 3: return f(k3_adam_bf16<kBF16, 8, 1>);
+        case 4: return f(k3_adam_bf16_v8<kBF16, 2, 4>);
+        case 5: return f(k3_adam_bf16_v8<kBF16, 2, 1>);
         default: return f(k3_adam_bf16<kBF16, 4, 4>);
     }
 }

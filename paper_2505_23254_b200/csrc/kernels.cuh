@@ -113,6 +113,8 @@ void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs&
 // kK3Slots x 256 slots of 4 elements per CTA, trailing CTAs for remainders.
 constexpr int kK3Slots = 4;
 int k3_slots(int gk, int variant);
+// elements per vector (slot) of the K3 variant: 4, or 8 for A/B variants 4/5
+int k3_vec(int gk, int variant);
 int k3_blocks_per_sm(int gk, int variant);
 void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st);
