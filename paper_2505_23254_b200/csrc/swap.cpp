@@ -533,17 +533,26 @@ Op* Engine::submit(const std::string& key, char* buf, std::uint64_t buf_bytes, b
                 fail(MA_ERR_SIZE_VIOLATION, "read destination for '" + key + "' must cover " +
                                                 std::to_string(op->loc.padded) + " padded bytes");
         }
+        // Bytes moved: the tensor's padded LOGICAL length.  A key rewritten
+        // smaller keeps its larger extents (reuse, like the reference), but
+        // only the granules the payload occupies are transferred — the
+        // caller's buffer need not cover the old extents.  The payload maps
+        // onto the extents in order.
+        const std::uint64_t move = std::min(align_up(op->loc.logical, kGranule), op->loc.padded);
+        op->bytes = move;
         // each extent in `workers` granule-aligned chunks, one task each
         std::uint64_t at_buf = 0;
         for (const Extent& e : op->loc.extents) {
-            const std::uint64_t chunk = align_up((e.length + cfg_.workers - 1) / cfg_.workers, kGranule);
-            for (std::uint64_t at = 0; at < e.length; at += chunk) {
+            if (at_buf >= move) break;
+            const std::uint64_t len = std::min(e.length, move - at_buf);
+            const std::uint64_t chunk = align_up((len + cfg_.workers - 1) / cfg_.workers, kGranule);
+            for (std::uint64_t at = 0; at < len; at += chunk) {
                 Task t;
                 t.fd = fds_[e.device];
                 t.device = e.device;
                 t.offset = e.offset + at;
                 t.buf = buf + at_buf + at;
-                t.length = std::min(chunk, e.length - at);
+                t.length = std::min(chunk, len - at);
                 t.write = write;
                 t.op = op.get();
                 tasks.push_back(t);
@@ -596,10 +605,10 @@ std::uint64_t Engine::wait(Op* op) {
     if (!op->error.empty()) fail(MA_ERR_IO_ERROR, op->error);
     stats_.submitted_ios += op->tasks;
     if (op->write) {
-        stats_.bytes_written += op->loc.padded;
+        stats_.bytes_written += op->bytes;
         stats_.write_requests += 1;
     } else {
-        stats_.bytes_read += op->loc.padded;
+        stats_.bytes_read += op->bytes;
         stats_.read_requests += 1;
     }
     return op->loc.logical;

@@ -117,6 +117,7 @@ struct Op {
     std::condition_variable cv;
     std::uint64_t pending = 0;
     std::uint64_t tasks = 0;
+    std::uint64_t bytes = 0;  // transferred (padded logical length)
     std::string error;
 };
 

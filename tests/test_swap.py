@@ -156,3 +156,58 @@ def test_manifest_restart(tmp_path):
     with pytest.raises(MemAscendError) as ei:
         mab.DirectIoEngine(devs, manifest_path=man)
     assert ei.value.code == "bad-config"
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_async_shadow_map_stress(backend, tmp_path):
+    """Many async operations in flight from several threads (the swapped
+    pipeline's pattern) against a shadow map, every backend."""
+    import threading
+
+    devs = mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 3, 96 << 20)
+    keys = 24
+    shadow = [None] * keys
+    locks = [threading.Lock() for _ in range(keys)]
+    errors = []
+    with mab.DirectIoEngine(devs, workers=3, queue_depth=16, backend=backend) as e:
+        def worker(seed):
+            rng = np.random.default_rng(seed)
+            try:
+                for _ in range(40):
+                    batch = sorted(set(int(k) for k in rng.integers(0, keys, 4)))
+                    held = [locks[k] for k in batch]
+                    for lk in held:
+                        lk.acquire()
+                    try:
+                        ops = []
+                        for k in batch:
+                            if shadow[k] is None or rng.random() < 0.5:
+                                n = int(rng.integers(1, 1 << 18))
+                                buf = mab.aligned_host_buffer((n + 4095) // 4096 * 4096)
+                                buf[:n] = rng.integers(0, 256, n, dtype=np.uint8)
+                                ops.append((k, "w", e.write_tensor_async(f"s{k}", buf, n), buf, n))
+                            else:
+                                n = len(shadow[k])
+                                # a shrunk key keeps its old extents: size by the location
+                                buf = mab.aligned_host_buffer(e.location(f"s{k}")["padded"])
+                                ops.append((k, "r", e.read_tensor_async(f"s{k}", buf), buf, n))
+                        for k, kind, op, buf, n in ops:
+                            got = op.wait()
+                            if kind == "w":
+                                shadow[k] = buf[:n].copy()
+                            elif got != n or not np.array_equal(buf[:n], shadow[k]):
+                                errors.append((k, got, n))
+                    finally:
+                        for lk in held:
+                            lk.release()
+            except Exception as ex:  # noqa: BLE001
+                errors.append(repr(ex))
+
+        threads = [threading.Thread(target=worker, args=(900 + t,)) for t in range(6)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        st = e.stats()
+    assert not errors, errors[:3]
+    assert st["write_requests"] >= keys and st["read_requests"] > 0
