@@ -656,6 +656,7 @@ void Engine::run_sync(const Task& t) {
                                              static_cast<off_t>(t.offset + done))
                                   : ::pread(t.fd, t.buf + done, t.length - done,
                                             static_cast<off_t>(t.offset + done));
+        if (n < 0 && errno == EINTR) continue;
         if (n <= 0)
             fail(MA_ERR_IO_ERROR, std::string(t.write ? "short write" : "short read") +
                                       " on device " + std::to_string(t.device) + " at offset " +
@@ -683,8 +684,25 @@ void Engine::run_aio(const Task& t) {
     std::vector<aiocb*> list;
     for (auto& cb : cbs) list.push_back(&cb);
     if (::lio_listio(LIO_WAIT, list.data(), static_cast<int>(list.size()), nullptr) != 0 &&
-        errno != EIO)
-        fail(MA_ERR_IO_ERROR, std::string("lio_listio failed: ") + std::strerror(errno));
+        errno != EIO && errno != EINTR) {
+        // EAGAIN: none or some queued; never leave queued requests behind
+        const int e = errno;
+        for (auto& cb : cbs) {
+            while (::aio_error(&cb) == EINPROGRESS) {
+                const aiocb* one[1] = {&cb};
+                ::aio_suspend(one, 1, nullptr);
+            }
+            ::aio_return(&cb);
+        }
+        fail(MA_ERR_IO_ERROR, std::string("lio_listio failed: ") + std::strerror(e));
+    }
+    // a signal can end LIO_WAIT early: wait for every request to finish
+    for (auto& cb : cbs) {
+        while (::aio_error(&cb) == EINPROGRESS) {
+            const aiocb* one[1] = {&cb};
+            ::aio_suspend(one, 1, nullptr);
+        }
+    }
     for (auto& cb : cbs) {
         const int e = ::aio_error(&cb);
         const ssize_t n = ::aio_return(&cb);
@@ -779,7 +797,9 @@ void Engine::worker_uring() {
             Piece* p = static_cast<Piece*>(u);
             --inflight;
             const Task& t = p->rec->t;
-            if (res < 0) {
+            if (res == -EINTR || res == -EAGAIN) {
+                ready.push_front(p);  // transient: resubmit as is
+            } else if (res < 0) {
                 close_piece(p, std::string("io_uring ") + (t.write ? "write" : "read") +
                                    " failed on device " + std::to_string(t.device) +
                                    " at offset " + std::to_string(p->off) + ": " +
