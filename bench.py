@@ -569,6 +569,51 @@ def storage_peak(store_dir, io_workers, io_depth, key_bytes=1 << 30, keys=4):
     return out
 
 
+def timed_swapped_steps(args, one_step, store, stream, dev, world, local_rank):
+    """W warm-up steps, then K timed steps between barriers (CUDA events on
+    the compute stream, max over ranks); returns (ms per step, swap-store
+    bytes moved per step, clocks, backend)."""
+    import torch
+    import torch.distributed as dist
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    io0 = store.stats() if store else {}
+    with ClockSampler(local_rank) as clk:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    io1 = store.stats() if store else {}
+    ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    io_bytes = ((io1.get("bytes_read", 0) - io0.get("bytes_read", 0)) +
+                (io1.get("bytes_written", 0) - io0.get("bytes_written", 0))) / args.steps
+    return float(ms.item()), io_bytes, clk.summary(), (store.backend if store else None)
+
+
+def storage_report(args, io_bytes, ms, bytes_per_swapped_param):
+    """Swap-device rate of the step against the device's measured mixed
+    read/write rate (equal bytes read and written concurrently bound it)."""
+    pk = storage_peak(args.swap_dir, args.io_workers, args.io_depth)
+    gbs = io_bytes / (ms / 1e3) / 1e9
+    return {"bound": "swap-device", "achieved": gbs, "unit": "GB/s", "peak": pk["mixed"],
+            "frac": gbs / pk["mixed"], "bytes_per_step": io_bytes,
+            "bytes_per_swapped_param": bytes_per_swapped_param,
+            "peak_read_gbs": pk["read"], "peak_write_gbs": pk["write"],
+            "peak_source": "measured O_DIRECT through the engine, same settings: 4 x 1 GiB keys, "
+                           "2 rewritten while 2 are read"}
+
+
 def ours_swapped(args, n, rank, world, local_rank):
     """configs[4]: Llama-3-70B-shaped state sharded 8 ways (8.82 B params per
     GPU).  fp32 master/m/v of `--swap-gb` worth of 100 M sub-groups live in
@@ -641,7 +686,6 @@ def ours_swapped(args, n, rank, world, local_rank):
     mab.gen_pseudo_grads(g, w, step=0, base=base, seed=1, scale=65536.0)
     st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "bf16", device=dev)
     stream = torch.cuda.current_stream(dev)
-    io0 = {}
 
     def one_step():
         st.check(g)
@@ -651,41 +695,15 @@ def ours_swapped(args, n, rank, world, local_rank):
         st.finish()
 
     try:
-        for _ in range(args.warmup):
-            one_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        io0 = store.stats() if store else {}
-        with ClockSampler(local_rank) as clk:
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(args.steps):
-                one_step()
-            b.record(stream)
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-        io1 = store.stats() if store else {}
-        ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        ms = float(ms.item())
-        backend = store.backend if store else None
+        ms, io_bytes, clocks, backend = timed_swapped_steps(args, one_step, store, stream, dev,
+                                                            world, local_rank)
         if store:
             store.close()
     finally:
         shutil.rmtree(sdir, ignore_errors=True)
     if rank != 0:
         return
-    pk = storage_peak(args.swap_dir, args.io_workers, args.io_depth)
-    io_bytes = ((io1.get("bytes_read", 0) - io0.get("bytes_read", 0)) +
-                (io1.get("bytes_written", 0) - io0.get("bytes_written", 0))) / args.steps
     n_sw = n - n_host
-    storage_gbs = io_bytes / (ms / 1e3) / 1e9
-    # equal bytes read and written concurrently: the measured mixed rate bounds it
-    storage_peak_gbs = pk["mixed"]
     line = {
         "metric": METRIC, "value": n * world / (ms / 1e3), "unit": "params/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -695,17 +713,12 @@ def ours_swapped(args, n, rank, world, local_rank):
                        dram_params=n_host, swapped_groups=len(swapped), groups=G,
                        host_slots=hslots, dev_slots=args.slots, io_backend=backend,
                        io_workers=args.io_workers, io_depth=args.io_depth),
-        "storage": {"bound": "swap-device", "achieved": storage_gbs, "unit": "GB/s",
-                    "peak": storage_peak_gbs, "frac": storage_gbs / storage_peak_gbs,
-                    "bytes_per_step": io_bytes, "bytes_per_swapped_param": 24,
-                    "peak_read_gbs": pk["read"], "peak_write_gbs": pk["write"],
-                    "peak_source": "measured O_DIRECT through the engine, same settings: 4 x 1 GiB "
-                                   "keys, 2 rewritten while 2 are read"},
+        "storage": storage_report(args, io_bytes, ms, 24),
         "host_link": {"achieved": 24 * n / (ms / 1e3) / 1e9, "unit": "GB/s",
                       "bytes_per_param": 24},
         "init_seconds": t_init,
         "gpu_launches": (1 + G + 1) * args.steps,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:
         res = reference_swapped_run(args, 2, 1, os.cpu_count() or 1)
@@ -783,38 +796,14 @@ def ours_swapped_bf16(args, n, rank, world, local_rank):
         st.finish()
 
     try:
-        for _ in range(args.warmup):
-            one_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        io0 = store.stats() if store else {}
-        with ClockSampler(local_rank) as clk:
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(args.steps):
-                one_step()
-            b.record(stream)
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-        io1 = store.stats() if store else {}
-        ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        ms = float(ms.item())
-        backend = store.backend if store else None
+        ms, io_bytes, clocks, backend = timed_swapped_steps(args, one_step, store, stream, dev,
+                                                            world, local_rank)
         if store:
             store.close()
     finally:
         shutil.rmtree(sdir, ignore_errors=True)
     if rank != 0:
         return
-    pk = storage_peak(args.swap_dir, args.io_workers, args.io_depth)
-    io_bytes = ((io1.get("bytes_read", 0) - io0.get("bytes_read", 0)) +
-                (io1.get("bytes_written", 0) - io0.get("bytes_written", 0))) / args.steps
-    storage_gbs = io_bytes / (ms / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": n * world / (ms / 1e3), "unit": "params/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -827,17 +816,12 @@ def ours_swapped_bf16(args, n, rank, world, local_rank):
                        swapped_groups=len(swapped), groups=G, host_slots=hslots,
                        dev_slots=args.slots, io_backend=backend, io_workers=args.io_workers,
                        io_depth=args.io_depth),
-        "storage": {"bound": "swap-device", "achieved": storage_gbs, "unit": "GB/s",
-                    "peak": pk["mixed"], "frac": storage_gbs / pk["mixed"],
-                    "bytes_per_step": io_bytes, "bytes_per_swapped_param": 8,
-                    "peak_read_gbs": pk["read"], "peak_write_gbs": pk["write"],
-                    "peak_source": "measured O_DIRECT through the engine, same settings: 4 x 1 GiB "
-                                   "keys, 2 rewritten while 2 are read"},
+        "storage": storage_report(args, io_bytes, ms, 8),
         "host_link": {"achieved": 8 * n / (ms / 1e3) / 1e9, "unit": "GB/s",
                       "bytes_per_param": 8},
         "init_seconds": t_init,
         "gpu_launches": (1 + G + 1) * args.steps,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
 
