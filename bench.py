@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--host-slots", type=int, default=6, help="cfg5 registered host slots")
     ap.add_argument("--io-workers", type=int, default=4, help="cfg5 swap-store workers")
     ap.add_argument("--io-depth", type=int, default=32, help="cfg5 requests in flight per worker")
+    ap.add_argument("--zero-fused", action="store_true",
+                    help="the whole ZeRO step over peer memory: K4 reduce-scatter+check of "
+                         "full-length gradients, K2 update + weight all-gather (per-rank "
+                         "partition --params, default 1e9)")
     ap.add_argument("--precision", choices=["mixed", "pure_bf16"], default="mixed",
                     help="cfg5 optimizer state: fp32 master/m/v (K2) or bf16 m/v + bf16 "
                          "weights (OptimPrecision::pure_bf16, K3)")
@@ -569,6 +573,76 @@ def storage_peak(store_dir, io_workers, io_depth, key_bytes=1 << 30, keys=4):
     return out
 
 
+def ours_zero_fused(args, n, rank, world, local_rank):
+    """Data-parallel ZeRO step with no collective call (tests/test_zero_step.py
+    checks it bit for bit): every rank holds full-length bf16 gradients and
+    the full working weights; per step K4 reduce-scatters the gradients with
+    the overflow check in its epilogue (peers read over NVLink through CUDA
+    IPC, the skip decision OR-ed by its last CTA), K2 updates this rank's
+    partition and stores the new weights into every rank's buffer, the
+    scaler advances.  Weak scaling: `n` params per rank.  Per rank and param:
+    world x 2 B gradient reads (world-1 of them remote) + 2 B write (K4),
+    28 B in HBM + (world-1) x 2 B remote weight stores (K2)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_23254_b200 as mab
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    total = n * world
+    G = torch.empty(total, dtype=torch.bfloat16, device=dev)
+    W = torch.empty(total, dtype=torch.bfloat16, device=dev)
+    base = rank * n
+    p = torch.empty(n, dtype=torch.float32, device=dev)
+    m = torch.zeros(n, dtype=torch.float32, device=dev)
+    v = torch.zeros(n, dtype=torch.float32, device=dev)
+    gp = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    mab.gen_seeded_weights(None, W, n=total, seed=1)
+    mab.gen_seeded_weights(p, W[base:base + n], base=base, seed=1)
+    # this rank's micro-batch gradients: the generator seeded per rank
+    mab.gen_pseudo_grads(G, W, step=0, seed=1 + rank, scale=65536.0)
+    gather = (mab.api.torch_all_gather_bytes() if world > 1 else (lambda b: [b]))
+    rs = mab.api.GradReduceScatter(world, rank, G, gather)
+    ag = mab.api.GradReduceScatter(world, rank, W, gather)
+    st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "bf16", device=dev)
+    sub = min(SUBGROUP, n)
+    w = W[base:base + n]
+    groups = mab.Stepper.subgroups(
+        [(p[o:o + sub], m[o:o + sub], v[o:o + sub], gp[o:o + sub], w[o:o + sub])
+         for o in range(0, n, sub)])
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step():
+        st.reduce_scatter(rs, base, n, gp, post_scale=1.0 / world)
+        st.apply_allgather(groups, ag)
+        st.finish()
+
+    ms, _, clocks, _ = timed_swapped_steps(args, one_step, None, stream, dev, world, local_rank)
+    skipped = bool(st.state()["last_overflow"])
+    timed_out = rs.timed_out() or ag.timed_out()
+    rs.close()
+    ag.close()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": n * world / (ms / 1e3), "unit": "params/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference generators seeded_weight/pseudo_gradient, per-rank seeds)",
+        "config": dict(workload_config(args, n, world),
+                       workload=f"zero-fused-{n}-per-rank",
+                       parallelism=f"zero x{world}: K4 reduce-scatter+check, K2 update+all-gather "
+                                   "over peer memory (no collective call)"),
+        "hbm_bytes_per_param": {"k4": world * 2 + 2, "k2": 28},
+        "remote_bytes_per_param": {"k4_reads": (world - 1) * 2, "k2_stores": (world - 1) * 2},
+        "last_step_skipped": skipped, "peer_timeout": timed_out,
+        "gpu_launches": 5 * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def timed_swapped_steps(args, one_step, store, stream, dev, world, local_rank):
     """W warm-up steps, then K timed steps between barriers (CUDA events on
     the compute stream, max over ranks); returns (ms per step, swap-store
@@ -850,7 +924,9 @@ def main():
         else:
             dist.init_process_group(backend)
     try:
-        if args.config == "cfg4":
+        if args.zero_fused:
+            ours_zero_fused(args, args.params or 1_000_000_000, rank, world, local_rank)
+        elif args.config == "cfg4":
             ours_streamed(args, n, rank, world, local_rank)
         elif args.config == "cfg5" and args.precision == "pure_bf16":
             ours_swapped_bf16(args, n, rank, world, local_rank)

@@ -71,3 +71,15 @@ def test_our_arm_two_ranks_one_gpu_p2p_exchange():
              "--flag-exchange", "p2p"],
             nproc=2, env={"MA_BENCH_BACKEND": "gloo", "MA_BENCH_DEVICE": "0"})
     assert j["n_gpus"] == 2 and j["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nproc", [1, 2])
+def test_zero_fused_line(nproc):
+    """--zero-fused: the ZeRO step over peer memory (K4 + K2-AG), every rank
+    as a process on one GPU for nproc 2."""
+    env = {"MA_BENCH_BACKEND": "gloo", "MA_BENCH_DEVICE": "0"} if nproc > 1 else None
+    j = run(["--zero-fused", "--params", "50000000", "--steps", "3", "--warmup", "3"],
+            nproc=nproc, env=env)
+    assert REQUIRED - {"e2e"} <= set(j) and j["n_gpus"] == nproc and j["value"] > 0
+    assert not j["peer_timeout"] and j["remote_bytes_per_param"]["k2_stores"] == 2 * (nproc - 1)
