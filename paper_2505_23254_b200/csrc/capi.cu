@@ -1076,7 +1076,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
             for (int t = 0; t < T; ++t)
                 if (!plan.host(k, t))
                     fail(MA_ERR_INVALID_ARGUMENT, "host-resident group without its state tensors");
-        n_swapped += keys ? 1 : 0;
+        n_swapped += keys && plan.n(k) ? 1 : 0;
     }
     if (n_swapped) {
         if (!h_staging || host_slots < 2)
@@ -1179,7 +1179,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
     // reads: swapped groups in order, each into a free host slot
     std::vector<uint32_t> swapped;
     for (uint32_t k = 0; k < plan.count; ++k)
-        if (plan.key(k, 0)) swapped.push_back(k);
+        if (plan.key(k, 0) && plan.n(k)) swapped.push_back(k);  // empty groups move nothing
     struct Pending {
         uint32_t hslot = 0;
         std::vector<ma::swp::Op*> ops;
@@ -1228,6 +1228,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
         std::vector<bool> dused(dev_slots, false);
         uint64_t chunk_no = 0;
         for (uint32_t k = 0; k < plan.count; ++k) {
+            if (plan.n(k) == 0) continue;
             const bool keyed = plan.key(k, 0) != nullptr;
             // keep the read-ahead full: block only for this group's own slot
             while (next_read < swapped.size()) {
