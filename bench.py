@@ -350,8 +350,11 @@ def ours(args, n, rank, world, local_rank):
     # ---- e2e: gradients from pinned host memory through the public API
     e2e = None
     if args.e2e_steps > 0:
-        g_host = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
-        g_host.view(torch.int16).copy_(g.view(torch.int16), non_blocking=False)
+        # the gradient flat buffer in alignment-free registered host memory
+        # (§4.3; torch's pin_memory would round 16.06 GB up to 32 GiB)
+        g_host = torch.from_numpy(mab.aligned_host_buffer(n * 2, register=True).view(np.int16))
+        g_host.copy_(g.view(torch.int16), non_blocking=False)
+        g_host = g_host.view(torch.bfloat16)
         res_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
 
         def e2e_step():
