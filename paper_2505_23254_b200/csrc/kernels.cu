@@ -1266,8 +1266,10 @@ __device__ __forceinline__ bool rs_scalar(const RsArgs& a, uint64_t e) {
     }
 }
 
-template <int SK, int DK>
-__global__ void __launch_bounds__(256, 3) k4_reduce_check(RsArgs a) {
+// ONE = 1: the single-source specialisation (world 1, or a scaled copy with
+// the check): no second-source registers, so 6 CTAs fit per SM instead of 3.
+template <int SK, int DK, int ONE = 0>
+__global__ void __launch_bounds__(256, ONE ? 6 : 3) k4_reduce_check(RsArgs a) {
     constexpr int U = rs_units(SK);
     constexpr uint32_t kSrcBytes = SK == kF32 ? 4 : 2, kDstBytes = DK == kF32 ? 4 : 2;
     const unsigned lane = threadIdx.x & 31u;
@@ -1284,6 +1286,20 @@ __global__ void __launch_bounds__(256, 3) k4_reduce_check(RsArgs a) {
             // roundings as starting from src0 and adding src1
             const uint8_t* b0 = static_cast<const uint8_t*>(a.src[0]) + a.head * kSrcBytes;
             const uint8_t* b1 = static_cast<const uint8_t*>(a.src[a.nsrc > 1 ? 1 : 0]) + a.head * kSrcBytes;
+            if constexpr (ONE != 0) {
+                RsRaw<SK> x[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
+                    if (full || j < a.nvec) x[u] = rs_raw<SK>(b0, j);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) acc[u][k] = rs_elem<SK>(x[u], k);
+                }
+                r = 1;
+            } else {
             RsRaw<SK> x[U], y[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -1302,8 +1318,9 @@ __global__ void __launch_bounds__(256, 3) k4_reduce_check(RsArgs a) {
                 }
             }
             r = a.nsrc > 1 ? 2 : 1;
+            }
         }
-        for (; r + 1 < a.nsrc; r += 2) {
+        for (; ONE == 0 && r + 1 < a.nsrc; r += 2) {
             const uint8_t* b0 = static_cast<const uint8_t*>(a.src[r]) + a.head * kSrcBytes;
             const uint8_t* b1 = static_cast<const uint8_t*>(a.src[r + 1]) + a.head * kSrcBytes;
             RsRaw<SK> x[U], y[U];
@@ -1323,7 +1340,7 @@ __global__ void __launch_bounds__(256, 3) k4_reduce_check(RsArgs a) {
                 }
             }
         }
-        if (r < a.nsrc) {
+        if (ONE == 0 && r < a.nsrc) {
             const uint8_t* b0 = static_cast<const uint8_t*>(a.src[r]) + a.head * kSrcBytes;
             RsRaw<SK> x[U];
 #pragma unroll
@@ -1362,10 +1379,22 @@ __global__ void __launch_bounds__(256, 3) k4_reduce_check(RsArgs a) {
     if (a.xchg) exchange_epilogue(a.xchg, a.epoch, a.flag, lane);
 }
 
+// MA_K4_SINGLE=0 (A/B only) keeps single-source launches on the general kernel
+bool k4_single() {
+    static const bool on = [] {
+        const char* e = std::getenv("MA_K4_SINGLE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void launch_reduce_check(int sk, int dk, const RsArgs& a, unsigned grid, cudaStream_t st) {
 #define MA_RS(S, D)                                                 \
     if (sk == S && dk == D) {                                       \
-        k4_reduce_check<S, D><<<grid, 256, 0, st>>>(a);             \
+        if (a.nsrc == 1 && k4_single())                             \
+            k4_reduce_check<S, D, 1><<<grid, 256, 0, st>>>(a);      \
+        else                                                        \
+            k4_reduce_check<S, D><<<grid, 256, 0, st>>>(a);         \
         return;                                                     \
     }
     MA_RS(kF32, kF32) MA_RS(kF32, kBF16) MA_RS(kF32, kF16)
