@@ -1635,7 +1635,7 @@ void launch_reduce(ma_stepper* s, const void* const* srcs, int nsrc, int sdt, ui
             break;
         }
     }
-    const uint64_t tile = static_cast<uint64_t>(ma::rs_units(sdt)) * 256;
+    const uint64_t tile = static_cast<uint64_t>(ma::rs_units_for(sdt, a.nsrc)) * 256;
     a.tiles = (a.nvec + tile - 1) / tile;
     const uint64_t rem = n - a.nvec * 8;
     const uint64_t cap = static_cast<uint64_t>(d.sms) * 8;

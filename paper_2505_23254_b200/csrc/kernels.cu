@@ -1268,9 +1268,11 @@ __device__ __forceinline__ bool rs_scalar(const RsArgs& a, uint64_t e) {
 
 // ONE = 1: the single-source specialisation (world 1, or a scaled copy with
 // the check): no second-source registers, so 6 CTAs fit per SM instead of 3.
-template <int SK, int DK, int ONE = 0>
-__global__ void __launch_bounds__(256, ONE ? 6 : 3) k4_reduce_check(RsArgs a) {
-    constexpr int U = rs_units(SK);
+// HALF = 1: half the units per thread (many sources: more CTAs instead of
+// more loads per thread; the host sizes tiles with rs_units_for)
+template <int SK, int DK, int ONE = 0, int HALF = 0>
+__global__ void __launch_bounds__(256, ONE ? 6 : HALF ? 5 : 3) k4_reduce_check(RsArgs a) {
+    constexpr int U = HALF ? (rs_units(SK) > 1 ? rs_units(SK) / 2 : 1) : rs_units(SK);
     constexpr uint32_t kSrcBytes = SK == kF32 ? 4 : 2, kDstBytes = DK == kF32 ? 4 : 2;
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t top = scan_word(DK).top;
@@ -1388,11 +1390,30 @@ bool k4_single() {
     return on;
 }
 
+// Half the units per thread (and 5 CTAs/SM instead of 3) from
+// MA_K4_HALF_MIN sources on (default 2: 2 sources 0.935 -> 0.971 of the copy
+// peak, 4 sources 0.88 -> 1.01, 8 sources 0.93 -> 1.02; A/B:
+// MA_K4_HALF_MIN=0 disables it)
+bool rs_half(int sk, uint32_t nsrc) {
+    static const uint32_t from = [] {
+        const char* e = std::getenv("MA_K4_HALF_MIN");
+        const int v = e ? std::atoi(e) : 2;
+        return v <= 0 ? 0xFFFFFFFFu : static_cast<uint32_t>(v);
+    }();
+    return nsrc >= from && nsrc >= 2 && sk != kF32;
+}
+
+int rs_units_for(int sk, uint32_t nsrc) {
+    return rs_half(sk, nsrc) ? rs_units(sk) / 2 : rs_units(sk);
+}
+
 void launch_reduce_check(int sk, int dk, const RsArgs& a, unsigned grid, cudaStream_t st) {
 #define MA_RS(S, D)                                                 \
     if (sk == S && dk == D) {                                       \
         if (a.nsrc == 1 && k4_single())                             \
             k4_reduce_check<S, D, 1><<<grid, 256, 0, st>>>(a);      \
+        else if (rs_half(S, a.nsrc))                                \
+            k4_reduce_check<S, D, 0, 1><<<grid, 256, 0, st>>>(a);   \
         else                                                        \
             k4_reduce_check<S, D><<<grid, 256, 0, st>>>(a);         \
         return;                                                     \

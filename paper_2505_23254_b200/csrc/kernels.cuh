@@ -139,6 +139,8 @@ struct RsArgs {
     unsigned long long epoch;
 };
 void launch_reduce_check(int sk, int dk, const RsArgs& a, unsigned grid, cudaStream_t st);
+// units per thread the launch for (source kind, source count) uses (host tile size)
+int rs_units_for(int sk, uint32_t nsrc);
 // all ranks meet at `epoch` (one warp; peers' slots over NVLink); a timeout
 // sets *flag (when non-null) so the step is skipped
 void launch_peer_barrier(const XchgDev* x, unsigned long long epoch, uint32_t* flag,
