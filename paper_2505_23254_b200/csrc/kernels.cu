@@ -1738,10 +1738,12 @@ void launch_k2_allgather(int gk, int wk, const SegTable& tab, const AdamArgs& a,
 // K3 A/B (MA_K3_VARIANT): 0 = 4 slots held to 4 CTA/SM (64 regs,
 // production for bf16 gradients, 0.94), 1 = 4 slots unbounded (80 regs,
 // 3 CTA/SM, 0.90), 2 = 2 slots at 4 CTA/SM (0.84), 3 = 8 slots (0.89),
-// 4 = 8-element slots at 4 CTA/SM (0.90, spills), 5 = 8-element unbounded (0.80).
+// 4 = 8-element slots at 4 CTA/SM (0.90, spills), 5 = 8-element unbounded (0.80),
+// 6 = 2 slots at 5 CTA/SM (0.86), 7 = 3 slots at 4 CTA/SM (0.91), 8 = 4 slots at 5 CTA/SM (0.88).
 int k3_slots(int gk, int variant) {
     if (gk != kBF16) return kK3Slots;
-    return variant == 2 ? 2 : variant == 3 ? 8 : (variant == 4 || variant == 5) ? 2 : kK3Slots;
+    return variant == 2 ? 2 : variant == 3 ? 8 : (variant == 4 || variant == 5) ? 2
+           : variant == 6 ? 2 : variant == 7 ? 3 : variant == 8 ? 4 : kK3Slots;
 }
 
 int k3_vec(int gk, int variant) { return gk == kBF16 && (variant == 4 || variant == 5) ? 8 : 4; }
@@ -1756,6 +1758,9 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 3: return f(k3_adam_bf16<kBF16, 8, 1>);
         case 4: return f(k3_adam_bf16_v8<kBF16, 2, 4>);
         case 5: return f(k3_adam_bf16_v8<kBF16, 2, 1>);
+        case 6: return f(k3_adam_bf16<kBF16, 2, 5>);
+        case 7: return f(k3_adam_bf16<kBF16, 3, 4>);
+        case 8: return f(k3_adam_bf16<kBF16, 4, 5>);
         default: return f(k3_adam_bf16<kBF16, 4, 4>);
     }
 }
