@@ -908,10 +908,30 @@ int ma_stepper_ingest_async(ma_stepper* s, const void* src, int src_dtype, void*
         if (n == 0) return;
         if (!src || !dst) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
         const DeviceInfo d = device_info();
-        const unsigned grid = static_cast<unsigned>(
-            std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(d.sms) * 8));
-        ma::launch_ingest(src_dtype, s->g_dtype, src, dst, n, &s->d_st->scale, &s->d_st->flag,
-                          grid, as_stream(stream));
+        ma::IngestArgs a{};
+        a.src = src;
+        a.dst = dst;
+        a.n = n;
+        a.d_scale = &s->d_st->scale;
+        a.flag = &s->d_st->flag;
+        const uint32_t es = elem_bytes(src_dtype), ed = elem_bytes(s->g_dtype);
+        for (uint64_t h = 0; n >= 8 && h < 8; ++h) {  // co-align src and dst on 16 bytes
+            if ((reinterpret_cast<uintptr_t>(src) + h * es) % 16 == 0 &&
+                (reinterpret_cast<uintptr_t>(dst) + h * ed) % 16 == 0) {
+                a.head = h;
+                a.nvec = (n - h) / 8;
+                break;
+            }
+        }
+        const uint64_t tile = static_cast<uint64_t>(ma::ingest_units(src_dtype)) * 256;
+        a.tiles = (a.nvec + tile - 1) / tile;
+        const uint64_t rem = n - a.nvec * 8;
+        const uint64_t cap = static_cast<uint64_t>(d.sms) * 8;
+        const uint64_t trailing =
+            rem ? std::max<uint64_t>(1, std::min<uint64_t>(cap, (rem + 255) / 256)) : 0;
+        const uint64_t grid = std::max<uint64_t>(1, a.tiles + trailing);
+        if (grid > 0x7FFFFFFFull) fail(MA_ERR_INVALID_ARGUMENT, "buffer too large for one launch");
+        ma::launch_ingest(src_dtype, s->g_dtype, a, static_cast<unsigned>(grid), as_stream(stream));
         CK(cudaGetLastError());
         s->last = as_stream(stream);
     });

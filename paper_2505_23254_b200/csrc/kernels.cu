@@ -1138,42 +1138,6 @@ __global__ void k_gen_grads(void* __restrict__ g, const uint16_t* __restrict__ w
 // flat gradient buffer that simulator.cpp:401-405 performs
 // (flat[i] = g * scale), with K1's exponent test applied to the stored value
 // in the same pass — the optimizer step then needs no separate K1 read.
-template <int SK, int DK>
-__global__ void __launch_bounds__(256) k_ingest(const void* __restrict__ src, void* __restrict__ dst,
-                                                uint64_t n, const float* d_scale, uint32_t* flag) {
-    const float sc = *d_scale;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    bool bad = false;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += stride) {
-        const float x = SK == kF32 ? reinterpret_cast<const float*>(src)[i]
-                                   : widen<SK>(reinterpret_cast<const uint16_t*>(src)[i]);
-        const float gs = __fmul_rn(x, sc);
-        if constexpr (DK == kF32) {
-            reinterpret_cast<float*>(dst)[i] = gs;
-            bad |= elem_non_finite(__float_as_uint(gs), kF32);
-        } else {
-            const uint16_t h = narrow<DK>(gs);
-            reinterpret_cast<uint16_t*>(dst)[i] = h;
-            bad |= elem_non_finite(h, DK);
-        }
-    }
-    if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31u) == 0) *flag = 1u;
-}
-
-void launch_ingest(int sk, int dk, const void* src, void* dst, uint64_t n, const float* d_scale,
-                   uint32_t* flag, unsigned grid, cudaStream_t st) {
-#define MA_ING(S, D)                                                               \
-    if (sk == S && dk == D) {                                                      \
-        k_ingest<S, D><<<grid, 256, 0, st>>>(src, dst, n, d_scale, flag);          \
-        return;                                                                    \
-    }
-    MA_ING(kF32, kF32) MA_ING(kF32, kBF16) MA_ING(kF32, kF16)
-    MA_ING(kBF16, kF32) MA_ING(kBF16, kBF16) MA_ING(kBF16, kF16)
-    MA_ING(kF16, kF32) MA_ING(kF16, kBF16) MA_ING(kF16, kF16)
-#undef MA_ING
-}
-
 // ============================================================== K4
 // Reduce-scatter epilogue check (the order and NaN rule
 // are those of oracle ora_reduce_check).  Sources are this rank's partition
@@ -1249,6 +1213,73 @@ __device__ __forceinline__ uint32_t rs_store8(void* base, uint64_t j, const floa
         return ((w[0] & sw.mask) + sw.inc) | ((w[1] & sw.mask) + sw.inc) |
                ((w[2] & sw.mask) + sw.inc) | ((w[3] & sw.mask) + sw.inc);
     }
+}
+
+// Producer-side check: dst = cast(src * scale) with the
+// overflow test on the stored values.  One tile of U x 256 eight-element
+// units per CTA, 16-byte accesses (src and dst co-aligned at element
+// `head`), trailing CTAs for the scalar head/tail.  Per element exactly the
+// arithmetic of the reference store (simulator.cpp:401-405): fp32 multiply,
+// then the cast.
+template <int SK, int DK, int U>
+__global__ void __launch_bounds__(256) k_ingest(IngestArgs a) {
+    const float sc = *a.d_scale;
+    constexpr uint32_t kSB = SK == kF32 ? 4 : 2, kDB = DK == kF32 ? 4 : 2;
+    const uint32_t top = scan_word(DK).top;
+    uint32_t acc_bits = 0;
+    bool bad = false;
+    if (blockIdx.x < a.tiles) {
+        const uint64_t j0 = static_cast<uint64_t>(blockIdx.x) * U * blockDim.x + threadIdx.x;
+        const uint8_t* sb = static_cast<const uint8_t*>(a.src) + a.head * kSB;
+        uint8_t* db = static_cast<uint8_t*>(a.dst) + a.head * kDB;
+        RsRaw<SK> x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
+            if (j < a.nvec) x[u] = rs_raw<SK>(sb, j);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
+            if (j >= a.nvec) continue;
+            float y[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[k] = __fmul_rn(rs_elem<SK>(x[u], k), sc);
+            acc_bits |= rs_store8<DK>(db, j, y);
+        }
+    } else {
+        const uint64_t q0 = blockIdx.x - a.tiles, nq = gridDim.x - a.tiles;
+        const uint64_t tail_begin = a.head + a.nvec * 8;
+        const uint64_t extra = a.head + (a.n - tail_begin);
+        for (uint64_t k = q0 * blockDim.x + threadIdx.x; k < extra; k += nq * blockDim.x) {
+            const uint64_t i = k < a.head ? k : tail_begin + (k - a.head);
+            const float gs = __fmul_rn(rs_load1<SK>(a.src, i), sc);
+            if constexpr (DK == kF32) {
+                reinterpret_cast<float*>(a.dst)[i] = gs;
+                bad |= elem_non_finite(__float_as_uint(gs), kF32);
+            } else {
+                const uint16_t h = narrow<DK>(gs);
+                reinterpret_cast<uint16_t*>(a.dst)[i] = h;
+                bad |= elem_non_finite(h, DK);
+            }
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, bad || (acc_bits & top) != 0u) && (threadIdx.x & 31u) == 0)
+        *a.flag = 1u;
+}
+
+int ingest_units(int sk) { return sk == kF32 ? 2 : 4; }
+
+void launch_ingest(int sk, int dk, const IngestArgs& a, unsigned grid, cudaStream_t st) {
+#define MA_ING(S, D)                                                                   \
+    if (sk == S && dk == D) {                                                          \
+        k_ingest<S, D, (S == kF32 ? 2 : 4)><<<grid, 256, 0, st>>>(a);                 \
+        return;                                                                        \
+    }
+    MA_ING(kF32, kF32) MA_ING(kF32, kBF16) MA_ING(kF32, kF16)
+    MA_ING(kBF16, kF32) MA_ING(kBF16, kBF16) MA_ING(kBF16, kF16)
+    MA_ING(kF16, kF32) MA_ING(kF16, kBF16) MA_ING(kF16, kF16)
+#undef MA_ING
 }
 
 template <int SK, int DK>

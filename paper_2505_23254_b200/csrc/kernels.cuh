@@ -152,8 +152,17 @@ void launch_gen_grads(int gk, int wk, void* g, const uint16_t* w, uint64_t n, ui
                       uint64_t seed, uint64_t step, const float* d_scale, float scale,
                       unsigned grid, cudaStream_t st);
 void launch_plant(void* buf, int dtype, uint64_t index, uint32_t bits, cudaStream_t st);
-void launch_ingest(int sk, int dk, const void* src, void* dst, uint64_t n, const float* d_scale,
-                   uint32_t* flag, unsigned grid, cudaStream_t st);
+// producer-side check: one tile of ingest_units(sk) x 256 eight-element
+// units per CTA over [head, head + 8 * nvec), trailing CTAs for the rest
+struct IngestArgs {
+    const void* src;
+    void* dst;
+    uint64_t n, head, nvec, tiles;
+    const float* d_scale;
+    uint32_t* flag;
+};
+int ingest_units(int sk);
+void launch_ingest(int sk, int dk, const IngestArgs& a, unsigned grid, cudaStream_t st);
 void launch_cast_sweep(int kind, int log2, uint64_t* out, uint64_t nblocks);
 void launch_mask_sweep(int kind, unsigned long long* mismatches, unsigned grid);
 void launch_fast_sweep(int mode, const float* divs, uint64_t count, uint64_t seed,

@@ -60,6 +60,17 @@ def main():
         out["k4"].append({"nsrc": k, "ms": ms, "gbs": byts / ms / 1e6,
                           "frac": byts / ms / 1e6 / peak, "bytes_per_elem": 2 * k + 2})
         print(out["k4"][-1], flush=True)
+    # producer-side check (k_ingest): dst = cast(src * scale) + the check
+    out["ingest"] = []
+    for skind, sdt in (("f32", torch.float32), ("bf16", torch.bfloat16)):
+        src = srcs[0].to(sdt)
+        ms = timed(lambda: st.ingest(src, dst), args.reps)
+        byts = (src.element_size() + 2) * n
+        out["ingest"].append({"src": skind, "ms": ms, "gbs": byts / ms / 1e6,
+                              "frac": byts / ms / 1e6 / peak,
+                              "bytes_per_elem": src.element_size() + 2})
+        print(out["ingest"][-1], flush=True)
+        del src
     del srcs, dst
     torch.cuda.empty_cache()
 
