@@ -75,7 +75,7 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_update_fused_with_weight_allgather(world):
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")

@@ -128,7 +128,7 @@ def oracle_run(world):
     return dict(p=p, m=m, v=v, w=w, overflow=overflow, scale=scales)
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_fused_zero_step_over_peer_memory(world):
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")
