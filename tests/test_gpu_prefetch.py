@@ -153,3 +153,31 @@ def test_cpp_device_pool_and_prefetcher(tmp_path):
     p = subprocess.run([exe, str(tmp_path / "store")], capture_output=True, text=True,
                        timeout=120)
     assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stdout + p.stderr
+
+
+@pytest.mark.parametrize("mode", ["hbm", "swapped"])
+def test_cpp_step_driver_workload_golden(golden, tmp_path, mode):
+    """include/memascend/step_driver.hpp from C++: the reference's workload
+    case through StepDriver (HBM-resident and swapped) ends on the golden
+    per-step digests of the unmodified reference."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2505_23254_b200", "lib")
+    exe = str(tmp_path / "step_driver_check")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"),
+                    "-I", "/usr/local/cuda/include",
+                    os.path.join(root, "tests", "cpp", "step_driver_check.cpp"), "-o", exe,
+                    "-L", lib, "-lmemascend", "-lmemascend_b200", "-L", "/usr/local/cuda/lib64",
+                    "-lcudart", f"-Wl,-rpath,{lib}", "-Wl,-rpath,/usr/local/cuda/lib64",
+                    "-pthread"], check=True)
+    p = subprocess.run([exe, mode, str(tmp_path / "store")], capture_output=True, text=True,
+                       timeout=120)
+    assert p.returncode == 0, p.stdout + p.stderr
+    got = dict(line.split() for line in p.stdout.split("\n") if line.strip())
+    c = next(x for x in golden("workload.json")["cases"] if x["name"] == "cfg_bf16_n100003")
+    last = c["per_step"][-1]
+    for k in "pmvw":
+        assert got[k] == last[f"{k}_fnv"], (k, got[k])
+    assert float(got["scale"]) == c["final_scale"] and int(got["updates"]) == c["updates"]
