@@ -92,3 +92,24 @@ def test_no_device_fails_loudly(so_path):
     dp = C.c_void_p()
     assert lib.ma_dpool_create(nb, nc, 1, C.byref(dp)) == 101
     assert b"no CPU fallback" in lib.ma_last_error()
+
+
+def test_every_public_header_compiles_on_its_own(tmp_path):
+    """Each drop-in / B200 header is self-contained (include order free),
+    as the reference's headers are."""
+    inc = os.path.join(ROOT, "include")
+    hdrs = sorted(f for f in os.listdir(os.path.join(inc, "memascend")) if f.endswith(".hpp"))
+    assert {"overflow.hpp", "optimizer.hpp", "pinned.hpp", "pool.hpp", "direct_io.hpp",
+            "device_pool.hpp", "step_driver.hpp"} <= set(hdrs)
+    for h in hdrs + ["../memascend_b200.h"]:
+        src = tmp_path / "one.cpp"
+        src.write_text(f'#include "memascend/{h}"\nint main() {{ return 0; }}\n')
+        p = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", inc, str(src)],
+                           capture_output=True, text=True)
+        assert p.returncode == 0, (h, p.stderr[-2000:])
+    # the C header is C, too
+    src = tmp_path / "one.c"
+    src.write_text('#include "memascend_b200.h"\nint main(void) { return 0; }\n')
+    p = subprocess.run(["gcc", "-std=c11", "-fsyntax-only", "-I", inc, str(src)],
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr[-2000:]
