@@ -6,7 +6,7 @@
 //   g++ -std=c++20 -O2 -Iinclude tools/bench_pool.cpp -o bench_pool \
 //       -Lpaper_2505_23254_b200/lib -lmemascend -lmemascend_b200 \
 //       -Wl,-rpath,$PWD/paper_2505_23254_b200/lib
-//   ./bench_pool <preset|model.json> [inflight=2] [max_backing_gib=8]
+//   ./bench_pool <preset|model.json> [inflight=1] [max_backing_gib=3]
 //
 // Rows per mode (monolithic, adaptive): capacity_bytes, and either a live
 // replay of the trainer's prefetch/hold pattern (backing, peak live,
@@ -37,8 +37,8 @@ int main(int argc, char** argv) {
         return 2;
     }
     const std::string ref = argv[1];
-    const std::uint64_t inflight = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 2;
-    const double max_gib = argc > 3 ? std::atof(argv[3]) : 8.0;
+    const std::uint64_t inflight = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 1;  // CLI defaults
+    const double max_gib = argc > 3 ? std::atof(argv[3]) : 3.0;
     try {
         ModelSpec spec;
         bool is_preset = false;
