@@ -11,7 +11,10 @@
 // pipeline of proj/src/simulator.cpp:367-425 ending in HBM: submit() keys in
 // consumption order, acquire() makes a CUDA stream wait for a tensor's copy
 // and returns its device address, release() returns the slot once that
-// stream's work so far is done.
+// stream's work so far is done.  As with the reference's blocking pool, the
+// pipeline is only as deep as the pool: a consumer must release a block's
+// tensors before it acquires tensors more than `inflight_blocks` blocks
+// ahead, otherwise acquire() waits for a slot that is never returned.
 #pragma once
 
 #include <cstdint>
