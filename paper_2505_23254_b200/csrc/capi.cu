@@ -982,76 +982,6 @@ int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups, u
     });
 }
 
-int ma_stepper_apply_streamed(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
-                              float* d_staging, uint64_t slot_elems, uint32_t slots,
-                              void* stream, void* h2d_stream, void* d2h_stream,
-                              int* skipped) {
-    NvtxRange nvtx_range("ma_stepper_apply_streamed");
-    return guarded([&] {
-        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
-        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        if (!d_staging || slot_elems == 0 || slots < 2 || slots > 16)
-            fail(MA_ERR_INVALID_ARGUMENT, "staging needs 2..16 slots of slot_elems > 0");
-        if (slot_elems % 4) fail(MA_ERR_ALIGNMENT, "slot_elems must be a multiple of 4");
-        cudaStream_t cs = as_stream(stream);
-        cudaStream_t hs = as_stream(h2d_stream);
-        cudaStream_t ds = as_stream(d2h_stream);
-        // The decision decides whether any state moves at all: a skipped step
-        // transfers nothing (test_simulator.cpp:111-125 "skip steps move only
-        // the forward reads").  One 4-byte readback per step.
-        uint32_t flag = 0;
-        CK(cudaMemcpyAsync(&flag, &s->d_st->flag, 4, cudaMemcpyDeviceToHost, cs));
-        CK(cudaStreamSynchronize(cs));
-        if (skipped) *skipped = flag ? 1 : 0;
-        s->last = cs;
-        if (flag) return;
-        stepper_grow_bc(s, s->issued + 1);
-        ma::AdamArgs a{};
-        a.c = s->c;
-        a.skip = &s->d_st->flag;
-        a.st = s->d_st;
-        a.bc_table = s->d_bc;
-        // event ids: [0] entry fence, then per slot {h2d, k2, d2h}
-        cudaEvent_t entry = s->event(0);
-        CK(cudaEventRecord(entry, cs));
-        CK(cudaStreamWaitEvent(hs, entry, 0));
-        auto ev = [&](uint32_t slot, int kind) { return s->event(1 + 3 * slot + kind); };
-        std::vector<bool> used(slots, false);
-        uint64_t chunk_no = 0;
-        for (uint32_t k = 0; k < count; ++k) {
-            const ma_subgroup& gsub = groups[k];
-            for (uint64_t off = 0; off < gsub.n; off += slot_elems, ++chunk_no) {
-                const uint64_t len = std::min(slot_elems, gsub.n - off);
-                const uint32_t slot = static_cast<uint32_t>(chunk_no % slots);
-                float* sp = d_staging + static_cast<uint64_t>(slot) * 3 * slot_elems;
-                float* sm = sp + slot_elems;
-                float* sv = sm + slot_elems;
-                if (used[slot]) CK(cudaStreamWaitEvent(hs, ev(slot, 2), 0));  // slot drained
-                CK(cudaMemcpyAsync(sp, gsub.p + off, len * 4, cudaMemcpyHostToDevice, hs));
-                CK(cudaMemcpyAsync(sm, gsub.m + off, len * 4, cudaMemcpyHostToDevice, hs));
-                CK(cudaMemcpyAsync(sv, gsub.v + off, len * 4, cudaMemcpyHostToDevice, hs));
-                CK(cudaEventRecord(ev(slot, 0), hs));
-                CK(cudaStreamWaitEvent(cs, ev(slot, 0), 0));
-                const uint64_t ges = elem_bytes(s->g_dtype);
-                ma_subgroup part{sp, sm, sv, static_cast<const uint8_t*>(gsub.g) + off * ges,
-                                 gsub.w ? static_cast<uint8_t*>(gsub.w) + off * 2 : nullptr, len};
-                launch_k2(&part, 1, s->g_dtype, s->w_dtype, a, cs);
-                CK(cudaEventRecord(ev(slot, 1), cs));
-                CK(cudaStreamWaitEvent(ds, ev(slot, 1), 0));
-                CK(cudaMemcpyAsync(gsub.p + off, sp, len * 4, cudaMemcpyDeviceToHost, ds));
-                CK(cudaMemcpyAsync(gsub.m + off, sm, len * 4, cudaMemcpyDeviceToHost, ds));
-                CK(cudaMemcpyAsync(gsub.v + off, sv, len * 4, cudaMemcpyDeviceToHost, ds));
-                CK(cudaEventRecord(ev(slot, 2), ds));
-                used[slot] = true;
-            }
-        }
-        // the compute stream (finish, the caller's sync) orders after every write-back
-        for (uint32_t slot = 0; slot < slots; ++slot) {
-            if (used[slot]) CK(cudaStreamWaitEvent(cs, ev(slot, 2), 0));
-        }
-    });
-}
-
 }  // extern "C"
 
 namespace {
@@ -1075,12 +1005,13 @@ struct SwapPlan {
 void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_staging,
                  uint32_t host_slots, void* d_staging, uint32_t dev_slots, uint64_t slot_elems,
                  void* stream, void* h2d_stream, void* d2h_stream, int* skipped) {
-    if (!s || !e) fail(MA_ERR_INVALID_ARGUMENT, "null stepper or swap store");
+    if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
     if (!d_staging || slot_elems == 0 || dev_slots < 2 || dev_slots > 16)
         fail(MA_ERR_INVALID_ARGUMENT, "device staging needs 2..16 slots of slot_elems > 0");
-    if (slot_elems % 8) fail(MA_ERR_ALIGNMENT, "slot_elems must be a multiple of 8");
     const int T = plan.ntens;
     const uint64_t E = plan.esize;
+    if (slot_elems % (16 / E))  // 16-byte aligned device slot tensors
+        fail(MA_ERR_ALIGNMENT, "slot_elems must be a multiple of " + std::to_string(16 / E));
     const uint64_t tb = (slot_elems * E + ma::swp::kGranule - 1) / ma::swp::kGranule *
                         ma::swp::kGranule;  // one tensor in a host slot
     uint32_t n_swapped = 0;
@@ -1099,6 +1030,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
         n_swapped += keys && plan.n(k) ? 1 : 0;
     }
     if (n_swapped) {
+        if (!e) fail(MA_ERR_INVALID_ARGUMENT, "swapped groups need a swap store");
         if (!h_staging || host_slots < 2)
             fail(MA_ERR_INVALID_ARGUMENT, "swapped groups need >= 2 host slots");
         if (reinterpret_cast<uintptr_t>(h_staging) % ma::swp::kGranule)
@@ -1121,7 +1053,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
     stepper_grow_bc(s, s->issued + 1);
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    ma::swp::Engine& eng = *e->e;
+    ma::swp::Engine* engp = e ? e->e : nullptr;
     char* hbase = static_cast<char*>(h_staging);
     char* dbase = static_cast<char*>(d_staging);
     auto hslot_ptr = [&](uint32_t h, int t) { return hbase + (static_cast<uint64_t>(T) * h + t) * tb; };
@@ -1174,7 +1106,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
                 std::vector<ma::swp::Op*> ops(T, nullptr);
                 for (int t = 0; t < T; ++t) {
                     try {
-                        ops[t] = eng.submit_write(plan.key(wb.group, t), hslot_ptr(wb.hslot, t),
+                        ops[t] = engp->submit_write(plan.key(wb.group, t), hslot_ptr(wb.hslot, t),
                                                   tb, plan.n(wb.group) * E);
                     } catch (const ma::swp::Failure& f) {
                         if (!code) code = f.code, msg = f.msg;
@@ -1183,7 +1115,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
                 for (int t = 0; t < T; ++t) {
                     if (!ops[t]) continue;
                     try {
-                        eng.wait(ops[t]);
+                        engp->wait(ops[t]);
                     } catch (const ma::swp::Failure& f) {
                         if (!code) code = f.code, msg = f.msg;
                     }
@@ -1223,14 +1155,14 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
         pend[k].hslot = h;
         pend[k].ops.assign(T, nullptr);
         for (int t = 0; t < T; ++t)
-            pend[k].ops[t] = eng.submit_read(plan.key(k, t), hslot_ptr(h, t), tb);
+            pend[k].ops[t] = engp->submit_read(plan.key(k, t), hslot_ptr(h, t), tb);
     };
     auto drain_reads = [&] {  // error path: never leave I/O into the slots in flight
         for (auto& p : pend)
             for (auto*& op : p.ops)
                 if (op) {
                     try {
-                        eng.wait(op);
+                        engp->wait(op);
                     } catch (const ma::swp::Failure&) {
                     }
                     op = nullptr;
@@ -1263,7 +1195,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
                 for (auto*& op : pend[k].ops) {
                     ma::swp::Op* o = op;
                     op = nullptr;
-                    eng.wait(o);
+                    engp->wait(o);
                 }
             }
             const uint64_t n = plan.n(k);
@@ -1383,6 +1315,41 @@ int ma_stepper_apply_swapped_bf16(ma_stepper* s, ma_swap* e, const ma_swap_group
             launch_k3(&part, 1, gdt, stepper_args(s), st);
         };
         run_swapped(s, e, plan, h_staging, host_slots, d_staging, dev_slots, slot_elems, stream,
+                    h2d_stream, d2h_stream, skipped);
+    });
+}
+
+// configs[3]: every group's state in registered host memory — the swapped
+// pipeline with no store (no host slots, no I/O), slices of slot_elems.
+int ma_stepper_apply_streamed(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
+                              float* d_staging, uint64_t slot_elems, uint32_t slots,
+                              void* stream, void* h2d_stream, void* d2h_stream,
+                              int* skipped) {
+    NvtxRange nvtx_range("ma_stepper_apply_streamed");
+    return guarded([&] {
+        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
+        if (!d_staging || slot_elems == 0 || slots < 2 || slots > 16)
+            fail(MA_ERR_INVALID_ARGUMENT, "staging needs 2..16 slots of slot_elems > 0");
+        SwapPlan plan;
+        plan.count = count;
+        plan.ntens = 3;
+        plan.esize = 4;
+        plan.key = [](uint32_t, int) -> const char* { return nullptr; };
+        plan.host = [&](uint32_t k, int t) {
+            return reinterpret_cast<char*>(t == 0 ? groups[k].p : t == 1 ? groups[k].m : groups[k].v);
+        };
+        plan.n = [&](uint32_t k) { return groups[k].n; };
+        const int gdt = s ? s->g_dtype : 0, wdt = s ? s->w_dtype : 0;
+        const uint64_t ges = elem_bytes(gdt);
+        plan.launch = [&](uint32_t k, uint64_t off, uint64_t len, char* const* d, cudaStream_t st) {
+            const ma_subgroup& gr = groups[k];
+            ma_subgroup part{reinterpret_cast<float*>(d[0]), reinterpret_cast<float*>(d[1]),
+                             reinterpret_cast<float*>(d[2]),
+                             static_cast<const uint8_t*>(gr.g) + off * ges,
+                             gr.w ? static_cast<uint8_t*>(gr.w) + off * 2 : nullptr, len};
+            launch_k2(&part, 1, gdt, wdt, stepper_args(s), st);
+        };
+        run_swapped(s, nullptr, plan, nullptr, 0, d_staging, slots, slot_elems, stream,
                     h2d_stream, d2h_stream, skipped);
     });
 }
