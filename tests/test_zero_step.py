@@ -26,9 +26,11 @@ import torch
 from oracle import oracle as ora
 from paper_2505_23254_b200.shard import shard_range
 
-N_TOTAL, SUBGROUP, STEPS, SEED = 300_007, 40_000, 6, 5
+N_TOTAL, SUBGROUP, SEED = 300_007, 40_000, 5
+STEPS = int(os.environ.get("MA_ZERO_SOAK_STEPS", "6"))  # soak runs: many steps
 HYP = dict(lr=1e-3, weight_decay=0.01)
 POISON = {(2, 1): 0x7FC0, (4, 0): 0xFF80}  # (step, rank) -> bf16 NaN / -inf
+POISON.update({(s, s % 3): 0x7F80 for s in range(11, 100_000, 37)})  # soak: more skips
 pytestmark = pytest.mark.gpu
 
 
