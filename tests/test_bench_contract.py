@@ -83,3 +83,16 @@ def test_zero_fused_line(nproc):
             nproc=nproc, env=env)
     assert REQUIRED - {"e2e"} <= set(j) and j["n_gpus"] == nproc and j["value"] > 0
     assert not j["peer_timeout"] and j["remote_bytes_per_param"]["k2_stores"] == 2 * (nproc - 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["mixed", "pure_bf16"])
+def test_cfg5_line(precision, tmp_path):
+    """configs[4] at a small size: a swap store under tmp, part of the groups
+    swapped, the storage and host-link objects present."""
+    j = run(["--config", "cfg5", "--precision", precision, "--params", "300000000",
+             "--swap-gb", "0.5", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+             "--swap-dir", str(tmp_path)])
+    assert j["value"] > 0 and j["config"]["swapped_groups"] >= 1
+    assert j["storage"]["bytes_per_step"] > 0 and 0 < j["storage"]["frac"] < 5
+    assert j["storage"]["bytes_per_swapped_param"] == (24 if precision == "mixed" else 8)
