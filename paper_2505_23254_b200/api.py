@@ -301,7 +301,8 @@ class Stepper:
             d2h_stream = self._d2h
         skipped = C.c_int()
         check(capi.lib().ma_stepper_apply_swapped(
-            self._h, store.handle, arr, len(arr), _raw(host_staging)[0], host_slots,
+            self._h, store.handle if store is not None else None, arr, len(arr),
+            _raw(host_staging)[0], host_slots,
             dev_staging.data_ptr(), dev_slots, slot_elems, _stream_ptr(stream),
             _stream_ptr(h2d_stream), _stream_ptr(d2h_stream), C.byref(skipped)))
         return bool(skipped.value)
@@ -333,7 +334,8 @@ class Stepper:
             d2h_stream = self._d2h
         skipped = C.c_int()
         check(capi.lib().ma_stepper_apply_swapped_bf16(
-            self._h, store.handle, arr, len(arr), _raw(host_staging)[0], host_slots,
+            self._h, store.handle if store is not None else None, arr, len(arr),
+            _raw(host_staging)[0], host_slots,
             dev_staging.data_ptr(), dev_slots, slot_elems, _stream_ptr(stream),
             _stream_ptr(h2d_stream), _stream_ptr(d2h_stream), C.byref(skipped)))
         return bool(skipped.value)

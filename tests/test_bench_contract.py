@@ -91,7 +91,7 @@ def test_cfg5_line(precision, tmp_path):
     """configs[4] at a small size: a swap store under tmp, part of the groups
     swapped, the storage and host-link objects present."""
     j = run(["--config", "cfg5", "--precision", precision, "--params", "300000000",
-             "--swap-gb", "0.5", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+             "--swap-gb", "1.3", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
              "--swap-dir", str(tmp_path)])
     assert j["value"] > 0 and j["config"]["swapped_groups"] >= 1
     assert j["storage"]["bytes_per_step"] > 0 and 0 < j["storage"]["frac"] < 5
