@@ -6,6 +6,10 @@
 // backing region comes from the registering PinnedAllocator, so checked-out
 // slots are DMA-ready for the streamed optimizer.
 #include <algorithm>
+#include <chrono>
+#include <unordered_map>
+#include <mutex>
+#include <condition_variable>
 #include <cctype>
 #include <fstream>
 #include <map>
@@ -320,126 +324,145 @@ std::uint64_t pool_capacity(const std::vector<TensorDescriptor>& inventory, Pool
     return layout_for(inventory, mode, inflight_blocks).payload;
 }
 
+struct Pool::State {
+    std::vector<std::vector<std::uint32_t>> free;          // per class, LIFO
+    std::unordered_map<std::string, std::uint32_t> known;  // inventory key -> class
+    std::unordered_map<std::string, BufferHandle> out;     // checked-out handles
+    PinnedRegion backing;
+    PinnedAllocator* allocator = nullptr;
+    mutable std::mutex mu;
+    std::condition_variable returned;
+    PoolStats stats;
+
+    std::uint32_t class_for(const std::vector<ClassInfo>& classes, const std::string& key,
+                            std::uint64_t payload) const {
+        if (auto it = known.find(key); it != known.end()) return it->second;
+        // unknown key: the tightest class that holds the payload
+        std::uint32_t best = UINT32_MAX;
+        for (std::uint32_t c = 0; c < classes.size(); ++c) {
+            if (classes[c].slot_payload_bytes >= payload &&
+                (best == UINT32_MAX || classes[c].slot_payload_bytes < classes[best].slot_payload_bytes))
+                best = c;
+        }
+        if (best == UINT32_MAX)
+            raise(ErrorCode::size_violation,
+                  "payload of " + std::to_string(payload) + " bytes fits no slot class");
+        return best;
+    }
+
+    const BufferHandle& held(const BufferHandle& h, const char* what) const {
+        auto it = out.find(h.key);
+        if (it == out.end())
+            raise(ErrorCode::lifecycle, std::string(what) + " on a handle that is not checked out");
+        return it->second;
+    }
+};
+
 Pool::Pool(const std::vector<TensorDescriptor>& inventory, const PoolConfig& config,
            PinnedAllocator& allocator)
-    : config_(config), allocator_(allocator) {
+    : st_(std::make_unique<State>()), config_(config) {
     Layout L = layout_for(inventory, config.mode, config.inflight_blocks);
     classes_ = std::move(L.classes);
-    runtime_.resize(classes_.size());
-    for (std::size_t c = 0; c < classes_.size(); ++c) {
-        auto& fs = runtime_[c].free_slots;
-        for (std::uint64_t s = classes_[c].slot_count; s > 0; --s) fs.push_back(static_cast<std::uint32_t>(s - 1));
-    }
+    st_->allocator = &allocator;
+    st_->free.resize(classes_.size());
+    for (std::size_t c = 0; c < classes_.size(); ++c)
+        for (std::uint64_t k = classes_[c].slot_count; k > 0; --k)
+            st_->free[c].push_back(static_cast<std::uint32_t>(k - 1));
     for (const auto& t : inventory) {
-        if (config.mode == PoolMode::monolithic) {
-            tensor_class_[t.name] = 0;
-            continue;
+        std::uint32_t c = 0;
+        if (config.mode == PoolMode::adaptive) {
+            const std::uint64_t b = tensor_bytes(t);
+            while (c < classes_.size() && classes_[c].slot_payload_bytes != b) ++c;
+            if (c == classes_.size()) continue;
         }
-        const std::uint64_t b = tensor_bytes(t);
-        for (std::uint32_t c = 0; c < classes_.size(); ++c) {
-            if (classes_[c].slot_payload_bytes == b) {
-                tensor_class_[t.name] = c;
-                break;
-            }
-        }
+        st_->known.emplace(t.name, c);
     }
-    backing_ = allocator_.allocate(std::max<std::uint64_t>(L.backing, 1), config.backing_policy,
-                                   config.lock_pages);
-    stats_.capacity_bytes = L.payload;
-    stats_.backing_bytes = L.backing;
+    st_->backing = allocator.allocate(std::max<std::uint64_t>(L.backing, 1), config.backing_policy,
+                                      config.lock_pages);
+    st_->stats.capacity_bytes = L.payload;
+    st_->stats.backing_bytes = L.backing;
 }
 
-std::uint32_t Pool::class_for(const std::string& key, std::uint64_t payload_bytes) const {
-    if (auto it = tensor_class_.find(key); it != tensor_class_.end()) return it->second;
-    // unknown key: the tightest class that holds the payload
-    std::uint32_t best = UINT32_MAX;
-    for (std::uint32_t c = 0; c < classes_.size(); ++c) {
-        if (classes_[c].slot_payload_bytes >= payload_bytes &&
-            (best == UINT32_MAX || classes_[c].slot_payload_bytes < classes_[best].slot_payload_bytes))
-            best = c;
-    }
-    if (best == UINT32_MAX)
-        raise(ErrorCode::size_violation,
-              "payload of " + std::to_string(payload_bytes) + " bytes fits no slot class");
-    return best;
-}
+Pool::~Pool() = default;
 
 BufferHandle Pool::checkout(const std::string& key, std::uint64_t payload_bytes) {
     if (payload_bytes == 0) raise(ErrorCode::invalid_argument, "zero-byte checkout for '" + key + "'");
-    std::unique_lock<std::mutex> lock(mu_);
-    if (ledger_.count(key)) raise(ErrorCode::already_checked_out, "'" + key + "' is already checked out");
-    const std::uint32_t c = class_for(key, payload_bytes);
+    State& S = *st_;
+    std::unique_lock<std::mutex> lock(S.mu);
+    if (S.out.count(key)) raise(ErrorCode::already_checked_out, "'" + key + "' is already checked out");
+    const std::uint32_t c = S.class_for(classes_, key, payload_bytes);
     const ClassInfo& info = classes_[c];
     if (payload_bytes > info.slot_payload_bytes)
         raise(ErrorCode::size_violation, "payload of " + std::to_string(payload_bytes) +
                                              " bytes exceeds slot size " +
                                              std::to_string(info.slot_payload_bytes) + " ('" + key + "')");
-    auto& fs = runtime_[c].free_slots;
+    auto& fs = S.free[c];
     if (fs.empty()) {
         if (!config_.blocking_checkout)
             raise(ErrorCode::pool_exhausted,
                   "class " + info.class_id + " has no free buffers for '" + key + "'");
         const auto t0 = std::chrono::steady_clock::now();
-        cv_.wait(lock, [&] { return !fs.empty(); });
-        stats_.blocked_time += std::chrono::steady_clock::now() - t0;
+        S.returned.wait(lock, [&] { return !fs.empty(); });
+        S.stats.blocked_time += std::chrono::steady_clock::now() - t0;
     }
     const std::uint32_t slot = fs.back();
     fs.pop_back();
     BufferHandle h{key, info.base_offset + std::uint64_t{slot} * info.slot_stride, payload_bytes, c, slot,
                    true};
-    ledger_[key] = h;
-    stats_.checkout_count += 1;
-    stats_.live_bytes += payload_bytes;
-    stats_.peak_live_bytes = std::max(stats_.peak_live_bytes, stats_.live_bytes);
+    S.out[key] = h;
+    S.stats.checkout_count += 1;
+    S.stats.live_bytes += payload_bytes;
+    S.stats.peak_live_bytes = std::max(S.stats.peak_live_bytes, S.stats.live_bytes);
     return h;
 }
 
 void Pool::checkin(const BufferHandle& handle) {
-    std::lock_guard<std::mutex> g(mu_);
-    auto it = ledger_.find(handle.key);
-    if (it == ledger_.end() || it->second.slot_index != handle.slot_index ||
+    State& S = *st_;
+    std::lock_guard<std::mutex> g(S.mu);
+    auto it = S.out.find(handle.key);
+    if (it == S.out.end() || it->second.slot_index != handle.slot_index ||
         it->second.class_index != handle.class_index)
         raise(ErrorCode::lifecycle, "checkin of a handle the pool does not hold ('" + handle.key + "')");
-    runtime_[handle.class_index].free_slots.push_back(handle.slot_index);
-    stats_.live_bytes -= it->second.length;
-    stats_.checkin_count += 1;
-    ledger_.erase(it);
-    cv_.notify_all();
+    S.free[handle.class_index].push_back(handle.slot_index);
+    S.stats.live_bytes -= it->second.length;
+    S.stats.checkin_count += 1;
+    S.out.erase(it);
+    S.returned.notify_all();
 }
 
 std::span<std::byte> Pool::span(const BufferHandle& handle) {
-    std::lock_guard<std::mutex> g(mu_);
-    if (!ledger_.count(handle.key)) raise(ErrorCode::lifecycle, "span() on a handle that is not checked out");
-    return backing_.bytes().subspan(handle.offset, handle.length);
+    std::lock_guard<std::mutex> g(st_->mu);
+    st_->held(handle, "span()");
+    return st_->backing.bytes().subspan(handle.offset, handle.length);
 }
 
 std::span<std::byte> Pool::padded_span(const BufferHandle& handle) {
-    std::lock_guard<std::mutex> g(mu_);
-    if (!ledger_.count(handle.key))
-        raise(ErrorCode::lifecycle, "padded_span() on a handle that is not checked out");
-    return backing_.bytes().subspan(handle.offset, (handle.length + kGranule - 1) / kGranule * kGranule);
+    std::lock_guard<std::mutex> g(st_->mu);
+    st_->held(handle, "padded_span()");
+    return st_->backing.bytes().subspan(handle.offset,
+                                        (handle.length + kGranule - 1) / kGranule * kGranule);
 }
 
 void* Pool::device_span(const BufferHandle& handle) {
-    std::lock_guard<std::mutex> g(mu_);
-    if (!ledger_.count(handle.key))
-        raise(ErrorCode::lifecycle, "device_span() on a handle that is not checked out");
-    if (!backing_.locked()) raise(ErrorCode::capability, "pool backing is not registered with the GPU");
+    std::lock_guard<std::mutex> g(st_->mu);
+    st_->held(handle, "device_span()");
+    if (!st_->backing.locked())
+        raise(ErrorCode::capability, "pool backing is not registered with the GPU");
     // registered memory is addressed by the GPU through the same UVA pointer
-    return backing_.data() + handle.offset;
+    return st_->backing.data() + handle.offset;
 }
 
 PoolStats Pool::stats() const {
-    std::lock_guard<std::mutex> g(mu_);
-    return stats_;
+    std::lock_guard<std::mutex> g(st_->mu);
+    return st_->stats;
 }
 
 std::vector<std::pair<std::uint64_t, std::uint64_t>> Pool::live_extents() const {
-    std::lock_guard<std::mutex> g(mu_);
-    std::vector<std::pair<std::uint64_t, std::uint64_t>> out;
-    out.reserve(ledger_.size());
-    for (const auto& kv : ledger_) out.emplace_back(kv.second.offset, kv.second.length);
-    return out;
+    std::lock_guard<std::mutex> g(st_->mu);
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> v;
+    v.reserve(st_->out.size());
+    for (const auto& kv : st_->out) v.emplace_back(kv.second.offset, kv.second.length);
+    return v;
 }
 
 double fragmentation(std::uint64_t capacity_bytes, std::uint64_t peak_live_bytes) {
