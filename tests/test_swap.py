@@ -211,3 +211,16 @@ def test_async_shadow_map_stress(backend, tmp_path):
         st = e.stats()
     assert not errors, errors[:3]
     assert st["write_requests"] >= keys and st["read_requests"] > 0
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_buffered_mode_round_trip(backend, tmp_path):
+    """cache_bypass=False opens the devices without O_DIRECT (the reference's
+    EngineConfig::cache_bypass); same contract otherwise."""
+    devs = mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 2, 16 << 20)
+    with mab.DirectIoEngine(devs, backend=backend, cache_bypass=False) as e:
+        src = payload(3 << 20, 5)
+        e.write_tensor("b", src, (3 << 20) - 17)
+        out = mab.aligned_host_buffer(3 << 20)
+        assert e.read_tensor("b", out) == (3 << 20) - 17
+        assert (out[:(3 << 20) - 17] == src[:(3 << 20) - 17]).all()
