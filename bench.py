@@ -434,6 +434,11 @@ def ours(args, n, rank, world, local_rank):
         threads = os.cpu_count() or 1
         cb = cpu_reference_run(min(args.cpu_sample, n), 3, 1, threads)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        # the reference's path at 1 worker too (the reference's
+        # simulator calls adam_step_fp32 with its default workers = 1)
+        one = cpu_reference_run(min(args.cpu_sample, n), 1, 0, 1)
+        line["cpu_baseline"]["single_thread"] = {"value": one["value"], "unit": "params/s",
+                                                 "cores": 1}
         line["host"] = {"cpu": cpu_model(), "nproc": threads}
     print(json.dumps(line), flush=True)
 
