@@ -181,3 +181,45 @@ def test_cpp_step_driver_workload_golden(golden, tmp_path, mode):
     for k in "pmvw":
         assert got[k] == last[f"{k}_fnv"], (k, got[k])
     assert float(got["scale"]) == c["final_scale"] and int(got["updates"]) == c["updates"]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_prefetch_random_stream(tmp_path, seed):
+    """200 tensors of random sizes in three classes; the consumer keeps a
+    sliding window of held tensors (smaller than every class's slot count),
+    reducing each on its stream before releasing it without a sync."""
+    rng = np.random.default_rng(seed)
+    classes = [(1 << 20, 4), (256 << 10, 6), (37 << 10, 8)]
+    window = 3
+    names, data = [], {}
+    devs = mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 2, 128 << 20)
+    store = mab.DirectIoEngine(devs, workers=3, queue_depth=16)
+    for k in range(200):
+        cap = classes[int(rng.integers(0, 3))][0]
+        nb = int(rng.integers(cap // 2 + 1, cap + 1))  # tightest class = the drawn one
+        buf = mab.aligned_host_buffer((nb + 4095) // 4096 * 4096)
+        buf[:] = rng.integers(0, 256, buf.size, dtype=np.uint8)
+        store.write_tensor(f"t{k}", buf, nb)
+        names.append(f"t{k}")
+        data[f"t{k}"] = int(buf[:nb].astype(np.int64).sum())
+    pool = mab.DevicePool(classes)
+    pf = mab.WeightPrefetcher(store, pool, int(rng.integers(1, 5)), 1 << 20)
+    for nm in names:
+        pf.submit(nm)
+    stream = torch.cuda.current_stream()
+    held, sums = [], {}
+    for nm in names:
+        t = pf.acquire(nm)
+        sums[nm] = t.to(torch.int64).sum()
+        held.append(nm)
+        if len(held) > window:
+            pf.release(held.pop(0), stream)
+    for nm in held:
+        pf.release(nm, stream)
+    torch.cuda.synchronize()
+    assert all(int(sums[nm]) == data[nm] for nm in names)
+    st = pool.stats()
+    assert st["checkout_count"] == st["checkin_count"] == len(names) and st["live_bytes"] == 0
+    pf.close()
+    pool.close()
+    store.close()
