@@ -210,3 +210,75 @@ def test_swapped_pure_bf16_skip_moves_nothing(golden, tmp_path):
     assert a["w"] == b["w"] and a["scale"] == b["scale"] == 65536.0 / 2
     groups = (t["n"] + 20013) // 20014
     assert b["moved"] == [0 if s == 3 else 2 * groups for s in range(c["steps"])]
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_swapped_random_groups_equal_hbm_path(tmp_path, seed):
+    """Random group boundaries (including 1..9-element groups), random tiers
+    and slot counts: the swapped pipeline equals the HBM-resident K2 path
+    bit for bit over 3 steps with a planted NaN at step 1."""
+    rng = np.random.default_rng(seed)
+    cuts = sorted(set(int(x) for x in rng.integers(1, 60_000, 12)) | {3, 7, 16})
+    bounds = [0] + cuts + [60_011]
+    spans = [(a, b - a) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    n = bounds[-1]
+    g = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    w_ref = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    w_sw = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    p_ref = torch.empty(n, dtype=torch.float32, device=DEV)
+    mab.gen_seeded_weights(p_ref, w_ref, seed=seed)
+    w_sw.copy_(w_ref)
+    m_ref = torch.zeros(n, device=DEV)
+    v_ref = torch.zeros(n, device=DEV)
+    p0 = p_ref.cpu().numpy()
+    hyper = mab.AdamHyper(weight_decay=0.01)
+    st_ref = mab.Stepper(hyper, 65536.0, 2000, "bf16", "bf16")
+    st_sw = mab.Stepper(hyper, 65536.0, 2000, "bf16", "bf16")
+    slot = max(((max(ln for _, ln in spans) + 7) // 8) * 8, 8)
+    hslots, dslots = int(rng.integers(2, 5)), int(rng.integers(2, 4))
+    devs = mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 2, 32 << 20)
+    store = mab.DirectIoEngine(devs, backend="auto")
+    buf = mab.aligned_host_buffer(align4k(slot * 4))
+    ref_groups, sw_groups, host = [], [], {}
+    for k, (o, ln) in enumerate(spans):
+        ref_groups.append((p_ref[o:o + ln], m_ref[o:o + ln], v_ref[o:o + ln], g[o:o + ln],
+                           w_ref[o:o + ln]))
+        if rng.random() < 0.6:
+            for name, arr in (("master", p0[o:o + ln]), ("m", np.zeros(ln, np.float32)),
+                              ("v", np.zeros(ln, np.float32))):
+                buf.view(np.float32)[:ln] = arr
+                store.write_tensor(f"{name}.g{k}", buf, ln * 4)
+            sw_groups.append(((f"master.g{k}", f"m.g{k}", f"v.g{k}"), g[o:o + ln],
+                              w_sw[o:o + ln]))
+        else:
+            t = [torch.tensor(p0[o:o + ln]).pin_memory(), torch.zeros(ln).pin_memory(),
+                 torch.zeros(ln).pin_memory()]
+            host[k] = t
+            sw_groups.append((tuple(t), g[o:o + ln], w_sw[o:o + ln]))
+    hstage = mab.aligned_host_buffer(hslots * 3 * align4k(slot * 4), register=True)
+    dstage = torch.empty(3 * dslots * slot, dtype=torch.float32, device=DEV)
+    for s in range(3):
+        mab.gen_pseudo_grads(g, w_ref, step=s, seed=seed, d_scale=st_ref.scale_t)
+        if s == 1:
+            mab.plant_bits(g, int(rng.integers(0, n)), 0x7FC0)
+        st_ref.check(g)
+        st_ref.apply(ref_groups)
+        st_ref.finish()
+        st_sw.check(g)
+        st_sw.apply_swapped(store, sw_groups, hstage, hslots, dstage, dslots, slot)
+        st_sw.finish()
+        torch.cuda.synchronize()
+    rb = mab.aligned_host_buffer(align4k(slot * 4))
+    for k, (o, ln) in enumerate(spans):
+        for idx, name, ref in ((0, "master", p_ref), (1, "m", m_ref), (2, "v", v_ref)):
+            if k in host:
+                got = host[k][idx].numpy()
+            else:
+                store.read_tensor(f"{name}.g{k}", rb)
+                got = rb.view(np.float32)[:ln]
+            assert np.array_equal(got.view(np.uint32),
+                                  ref[o:o + ln].cpu().numpy().view(np.uint32)), (k, name)
+    assert torch.equal(w_sw.view(torch.int16), w_ref.view(torch.int16))
+    assert st_sw.state()["scale"] == st_ref.state()["scale"] == 32768.0
+    store.close()
+    mab.host_unregister(hstage)
