@@ -190,31 +190,64 @@ static inline float load_grad(const void* g, int kind, uint64_t i) {
     return widen(((const uint16_t*)g)[i], kind);
 }
 
+/* x86 SSE NaN results (Intel SDM Vol. 1 §4.8.3.5, Table 4-7), made explicit
+ * so they do not depend on the operand order THIS compiler picks: a NaN
+ * operand propagates quieted (bit 22 set) — the first source operand if it
+ * is a NaN, else the second — and an invalid operation on non-NaN operands
+ * gives the default NaN 0xFFC00000.  `a` is the first source operand of the
+ * instruction in the reference's compiled adam_range (objdump of optimizer.o
+ * built with the reference flags; see ORD_* below). */
+static inline int isnan_bits(uint32_t u) { return (u & 0x7FFFFFFFu) > 0x7F800000u; }
+static inline float x86r(float r, float a, float b) {
+    if (r == r) return r;
+    if (isnan_bits(f2u(a))) return u2f(f2u(a) | 0x00400000u);
+    if (isnan_bits(f2u(b))) return u2f(f2u(b) | 0x00400000u);
+    return u2f(0xFFC00000u);
+}
+static inline float x86_sqrt(float x) {
+    const float r = sqrtf(x);
+    if (r == r) return r;
+    return isnan_bits(f2u(x)) ? u2f(f2u(x) | 0x00400000u) : u2f(0xFFC00000u);
+}
+
+/* The two instantiations of adam_range order their commutative operands
+ * differently (optimizer.cpp:35-39 as compiled by g++ -O3):
+ *   ORD_FP32 (Fp32Access):  m*b1, (1-b1)*g, b2*v, (1-b2)*gg, vb + va, q*lr, lrwd*p
+ *   ORD_BF16 (Bf16Access):  m*b1, g*(1-b1), v*b2, gg*(1-b2), va + vb, q*lr, lrwd*p */
+enum { ORD_FP32 = 0, ORD_BF16 = 1 };
+
 /* One element, operation order of proj/src/optimizer.cpp:31-39. */
-static inline void adam_elem(float* pp, float* mp, float* vp, float gs, const ora_hyper* h,
-                             float loss_scale, float bc1, float bc2) {
-    const float g = gs / loss_scale;
+static inline void adam_elem_ord(float* pp, float* mp, float* vp, float gs, const ora_hyper* h,
+                                 float loss_scale, float bc1, float bc2, int ord) {
+    const float g = x86r(gs / loss_scale, gs, loss_scale);
     float p = *pp, m = *mp, v = *vp;
     const float one_m_b1 = 1.0f - h->beta1;
     const float one_m_b2 = 1.0f - h->beta2;
-    const float m_a = h->beta1 * m;
-    const float m_b = one_m_b1 * g;
-    m = m_a + m_b;
-    const float gg = g * g;
-    const float v_a = h->beta2 * v;
-    const float v_b = one_m_b2 * gg;
-    v = v_a + v_b;
-    const float mh = m / bc1;
-    const float vh = v / bc2;
-    const float den = sqrtf(vh) + h->eps;
-    const float step = h->lr * (mh / den);
+    const float m_a = x86r(m * h->beta1, m, h->beta1);
+    const float m_b = ord == ORD_FP32 ? x86r(one_m_b1 * g, one_m_b1, g) : x86r(g * one_m_b1, g, one_m_b1);
+    m = x86r(m_a + m_b, m_a, m_b);
+    const float gg = x86r(g * g, g, g);
+    const float v_a = ord == ORD_FP32 ? x86r(h->beta2 * v, h->beta2, v) : x86r(v * h->beta2, v, h->beta2);
+    const float v_b = ord == ORD_FP32 ? x86r(one_m_b2 * gg, one_m_b2, gg) : x86r(gg * one_m_b2, gg, one_m_b2);
+    v = ord == ORD_FP32 ? x86r(v_b + v_a, v_b, v_a) : x86r(v_a + v_b, v_a, v_b);
+    const float mh = x86r(m / bc1, m, bc1);
+    const float vh = x86r(v / bc2, v, bc2);
+    const float sq = x86_sqrt(vh);
+    const float den = x86r(sq + h->eps, sq, h->eps);
+    const float q = x86r(mh / den, mh, den);
+    const float step = x86r(q * h->lr, q, h->lr);
     const float lrwd = h->lr * h->weight_decay;
-    const float decay = lrwd * p;
-    p = p - step;
-    p = p - decay;
+    const float decay = x86r(lrwd * p, lrwd, p);
+    p = x86r(p - step, p, step);
+    p = x86r(p - decay, p, decay);
     *pp = p;
     *mp = m;
     *vp = v;
+}
+
+static inline void adam_elem(float* pp, float* mp, float* vp, float gs, const ora_hyper* h,
+                             float loss_scale, float bc1, float bc2) {
+    adam_elem_ord(pp, mp, vp, gs, h, loss_scale, bc1, bc2, ORD_FP32);
 }
 
 /* optimizer.cpp:26-44 (adam_range), 46-69 (t == 0 check), 103-109
@@ -241,7 +274,7 @@ int ora_adam_step_bf16(uint16_t* p, uint16_t* m, uint16_t* v, const float* g, ui
         float pf = ora_bf16_to_float(p[i]);
         float mf = ora_bf16_to_float(m[i]);
         float vf = ora_bf16_to_float(v[i]);
-        adam_elem(&pf, &mf, &vf, g[i], h, loss_scale, bc1, bc2);
+        adam_elem_ord(&pf, &mf, &vf, g[i], h, loss_scale, bc1, bc2, ORD_BF16);
         p[i] = ora_bf16_from_float(pf);
         m[i] = ora_bf16_from_float(mf);
         v[i] = ora_bf16_from_float(vf);
@@ -370,7 +403,7 @@ int ora_train(const ora_train_cfg* c, ora_train_out* out) {
                     float pf = ora_bf16_to_float(w[i]);
                     float mf = ora_bf16_to_float(m16[i]);
                     float vf = ora_bf16_to_float(v16[i]);
-                    adam_elem(&pf, &mf, &vf, gs, &c->hyper, scale_now, bc1, bc2);
+                    adam_elem_ord(&pf, &mf, &vf, gs, &c->hyper, scale_now, bc1, bc2, ORD_BF16);
                     w[i] = ora_bf16_from_float(pf);
                     m16[i] = ora_bf16_from_float(mf);
                     v16[i] = ora_bf16_from_float(vf);

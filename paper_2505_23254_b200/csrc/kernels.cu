@@ -478,6 +478,24 @@ __device__ __forceinline__ void load_slot(const Seg& sg, uint64_t e, Slot4& s) {
     }
 }
 
+// The exact path of one 4-element slot, kept OUT OF LINE: a slot lands here
+// only when an element leaves the fast path's guarded ranges (zero or tiny
+// moments, non-finite values, a non-power-of-two loss scale), and inlined
+// into every slot of a tile it multiplied the kernels' code (15k SASS lines
+// for K3) and competed with the fast path for registers.
+struct Exact4 {
+    float4 p, m, v;
+};
+template <int ORD>
+__device__ __noinline__ Exact4 adam_exact4(float4 p, float4 m, float4 v, float4 g,
+                                           const AdamConsts c, const StepScalars s) {
+    adam_elem<ORD>(p.x, m.x, v.x, g.x, c, s);
+    adam_elem<ORD>(p.y, m.y, v.y, g.y, c, s);
+    adam_elem<ORD>(p.z, m.z, v.z, g.z, c, s);
+    adam_elem<ORD>(p.w, m.w, v.w, g.w, c, s);
+    return Exact4{p, m, v};
+}
+
 // MATH: 0 = production (hoisted-guard fast path, exact fallback), 1 = probe
 // (approximate div/sqrt, never production), 2 = exact intrinsics only (A/B)
 template <int GK, int WK, int MATH = 0, int AG = 0>
@@ -523,11 +541,10 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
             }
             return;
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) adam_elem(p[k], m[k], v[k], g[k], c, sc);
-        s.p = make_float4(p[0], p[1], p[2], p[3]);
-        s.m = make_float4(m[0], m[1], m[2], m[3]);
-        s.v = make_float4(v[0], v[1], v[2], v[3]);
+        const Exact4 r = adam_exact4<kOrdFp32>(s.p, s.m, s.v, make_float4(g0, g1, g2, g3), c, sc);
+        s.p = r.p;
+        s.m = r.m;
+        s.v = r.v;
     }
     __stcs(reinterpret_cast<float4*>(sg.p + e), s.p);
     __stcs(reinterpret_cast<float4*>(sg.m + e), s.m);
@@ -845,7 +862,7 @@ __device__ __forceinline__ void bf16_state_scalar(const Seg& sg, uint64_t e, con
     uint16_t* M = reinterpret_cast<uint16_t*>(sg.m);
     uint16_t* V = reinterpret_cast<uint16_t*>(sg.v);
     float p = widen_bf16(P[e]), m = widen_bf16(M[e]), v = widen_bf16(V[e]);
-    adam_elem(p, m, v, load_grad1<GK>(sg.g, e), c, s);
+    adam_elem<kOrdBf16>(p, m, v, load_grad1<GK>(sg.g, e), c, s);
     P[e] = narrow<kBF16>(p);
     M[e] = narrow<kBF16>(m);
     V[e] = narrow<kBF16>(v);
@@ -910,8 +927,13 @@ __device__ __forceinline__ void bf16_state_update(uint16_t* P, uint16_t* M, uint
         __stcs(reinterpret_cast<uint2*>(V), pack4<true>(v));
         return;
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) adam_elem(p[k], m[k], v[k], g[k], c, s);
+    const Exact4 r = adam_exact4<kOrdBf16>(make_float4(p[0], p[1], p[2], p[3]),
+                                           make_float4(m[0], m[1], m[2], m[3]),
+                                           make_float4(v[0], v[1], v[2], v[3]),
+                                           make_float4(g[0], g[1], g[2], g[3]), c, s);
+    p[0] = r.p.x; p[1] = r.p.y; p[2] = r.p.z; p[3] = r.p.w;
+    m[0] = r.m.x; m[1] = r.m.y; m[2] = r.m.z; m[3] = r.m.w;
+    v[0] = r.v.x; v[1] = r.v.y; v[2] = r.v.z; v[3] = r.v.w;
     __stcs(reinterpret_cast<uint2*>(P), pack4<false>(p));
     __stcs(reinterpret_cast<uint2*>(M), pack4<false>(m));
     __stcs(reinterpret_cast<uint2*>(V), pack4<false>(v));
@@ -1053,7 +1075,7 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_adam_bf16_v8(SegTable tab
                     __stcs(reinterpret_cast<uint4*>(V + o), pack8<true>(v));
                 } else {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) adam_elem(p[k], m[k], v[k], g[k], c, sc);
+                    for (int k = 0; k < 8; ++k) adam_elem<kOrdBf16>(p[k], m[k], v[k], g[k], c, sc);
                     __stcs(reinterpret_cast<uint4*>(P + o), pack8<false>(p));
                     __stcs(reinterpret_cast<uint4*>(M + o), pack8<false>(m));
                     __stcs(reinterpret_cast<uint4*>(V + o), pack8<false>(v));
@@ -1245,7 +1267,19 @@ __global__ void __launch_bounds__(256) k_ingest(IngestArgs a) {
             float y[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) y[k] = __fmul_rn(rs_elem<SK>(x[u], k), sc);
-            acc_bits |= rs_store8<DK>(db, j, y);
+            const uint32_t unit = rs_store8<DK>(db, j, y);
+            if ((unit & top) != 0u) {
+                // a non-finite unit (rare): store it again with the x86 NaN
+                // of `g * scale` (simulator.cpp:404) — the gradient's payload,
+                // quieted — instead of the GPU's canonical NaN
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float xk = rs_elem<SK>(x[u], k);
+                    y[k] = x86(y[k], xk, sc);
+                }
+                rs_store8<DK>(db, j, y);
+            }
+            acc_bits |= unit;
         }
     } else {
         const uint64_t q0 = blockIdx.x - a.tiles, nq = gridDim.x - a.tiles;
@@ -1253,7 +1287,8 @@ __global__ void __launch_bounds__(256) k_ingest(IngestArgs a) {
         const uint64_t extra = a.head + (a.n - tail_begin);
         for (uint64_t k = q0 * blockDim.x + threadIdx.x; k < extra; k += nq * blockDim.x) {
             const uint64_t i = k < a.head ? k : tail_begin + (k - a.head);
-            const float gs = __fmul_rn(rs_load1<SK>(a.src, i), sc);
+            const float xs = rs_load1<SK>(a.src, i);
+            const float gs = x86(__fmul_rn(xs, sc), xs, sc);
             if constexpr (DK == kF32) {
                 reinterpret_cast<float*>(a.dst)[i] = gs;
                 bad |= elem_non_finite(__float_as_uint(gs), kF32);

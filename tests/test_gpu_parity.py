@@ -187,8 +187,8 @@ def test_fast_path_general_division_random():
 def test_k2_fast_path_fallback_slots_bit_exact():
     """Slots whose new m/v leave the guarded ranges (zeros, tiny and huge
     moments, subnormal gradients) recompute exactly: K2 equals the oracle
-    element for element (NaN-producing inputs are excluded: x86 and the GPU
-    propagate different NaN payloads)."""
+    element for element.  (NaN-producing inputs, payloads included:
+    tests/test_gpu_nan.py.)"""
     n = 1 << 16
     rs = np.random.default_rng(5)
     g = (rs.standard_normal(n) * 1024).astype(f32)
