@@ -71,7 +71,8 @@ enum ma_status {
     MA_ERR_UNCALIBRATED = 16,
     MA_ERR_BAD_CONFIG = 17,
     MA_ERR_CUDA = 100,      /* a CUDA runtime call failed */
-    MA_ERR_NO_DEVICE = 101  /* no usable sm_100 device: there is no CPU fallback */
+    MA_ERR_NO_DEVICE = 101, /* no usable sm_100 device: there is no CPU fallback */
+    MA_ERR_NCCL = 102       /* an NCCL call failed (or libnccl.so.2 is not loadable) */
 };
 
 enum ma_dtype { MA_DT_F32 = 0, MA_DT_BF16 = 1, MA_DT_F16 = 2, MA_DT_NONE = 3 };
@@ -180,8 +181,13 @@ MA_API int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* 
  * (peer memory mapped with CUDA IPC), waits for all peers' slots of this
  * step, and leaves the OR in the local flag, so the following apply skips or
  * updates identically on every rank.  All ranks must call it the same number
- * of times.  A peer missing for ~15 s forces a skip and sets the error
- * reported by ma_xchg_error instead of hanging the GPU. */
+ * of times.  A peer that does not arrive within MA_PEER_TIMEOUT_S seconds
+ * (environment, default 300) is FATAL for the whole job, never a local skip:
+ * the waiting rank posts a poison value into every peer's slots and traps
+ * (its CUDA context reports cudaErrorLaunchFailure / MA_ERR_CUDA from then
+ * on), and every rank that reads the poison traps as well — ranks cannot
+ * diverge (one skipping while another updates).  ma_xchg_error reports 1
+ * only while the context is still usable (i.e. never after a trap). */
 #define MA_IPC_HANDLE_BYTES 64
 typedef struct ma_xchg ma_xchg;
 MA_API int ma_xchg_create(int world, int rank, ma_xchg** out, void* ipc_handle_out);
@@ -218,8 +224,10 @@ MA_API int ma_stepper_reduce_check_async(ma_stepper* s, const void* const* srcs,
  * complete), then K4 reading every peer over NVLink, whose last CTA is the
  * exit barrier (nobody overwrites gradients still being read) and the OR of
  * all ranks' flags — the stepper's flag is the global skip decision when the
- * call completes, with no separate collective.  A peer missing for ~2^35
- * cycles forces a skip and sets the error reported by ma_rs_error. */
+ * call completes, with no separate collective.  A peer missing for
+ * MA_PEER_TIMEOUT_S seconds stops the job (poison + trap on every rank, as
+ * for ma_stepper_check_xchg_async): no rank overwrites gradients a peer may
+ * still read, and no rank's decision differs from another's. */
 typedef struct ma_rs ma_rs;
 #define MA_RS_HANDLE_BYTES 192
 MA_API int ma_rs_create(int world, int rank, const void* grads, uint64_t n_total, int dtype,
@@ -282,6 +290,49 @@ MA_API int ma_stepper_state(ma_stepper* s, ma_step_state* out);
  * min(count, 65536) steps, oldest first. */
 MA_API int ma_stepper_history(ma_stepper* s, uint8_t* overflow, float* scale_after, uint64_t cap,
                        uint64_t* count);
+
+/* Resume a run (checkpoint/restart): the Adam step count
+ * (OptimizerState::step_t, optimizer.hpp:60-66) and the LossScaler's scale
+ * and clean_steps (optimizer.hpp:19-35) of a saved run.  Synchronous.  The
+ * next applied update uses t = updates + 1, exactly as the reference's
+ * adam_step (optimizer.cpp:120-124) continues from a restored step_t. */
+MA_API int ma_stepper_set_state(ma_stepper* s, float scale, uint32_t clean_steps,
+                                uint64_t updates);
+
+/* CUDA graph of a step chain: between graph_begin and graph_end every
+ * *_async call on `stream` (a non-default stream) is captured instead of
+ * executed — e.g. check -> ma_stepper_allreduce_flag_async -> apply ->
+ * finish; ma_graph_launch then replays the whole chain with one launch.
+ * Loss scale, skip flag and t live on the device, so one graph serves every
+ * later step; `reserve_steps` sizes the bias-correction table the graph
+ * holds (a launch beyond it fails with MA_ERR_LIFECYCLE: capture again).
+ * Calls that synchronise with the host (apply_streamed / apply_swapped,
+ * state, set_state) cannot be captured. */
+typedef struct ma_graph ma_graph;
+MA_API int ma_stepper_graph_begin(ma_stepper* s, uint64_t reserve_steps, void* stream);
+MA_API int ma_stepper_graph_end(ma_stepper* s, void* stream, ma_graph** out);
+MA_API int ma_graph_launch(ma_graph* g, void* stream);
+MA_API int ma_graph_destroy(ma_graph* g);
+
+/* ------------------------------------------------------------------ */
+/* NCCL communicator (SURVEY §8(b) `ma_init(device, ncclUniqueId*, rank,
+ * world)` / `ma_flag_allreduce_max`): the cross-rank OR of the skip flag as
+ * one ncclAllReduce(max) of the uint32 flag on the compute stream, so every
+ * rank makes the reference's single global decision (simulator.cpp:431-440).
+ * Rank 0 creates the id (ma_comm_unique_id), every rank receives it over any
+ * host channel and calls ma_comm_create on its own device (current CUDA
+ * device).  libnccl.so.2 is resolved at run time (the copy torch already
+ * loaded, else the system's); without it these return MA_ERR_NCCL. */
+#define MA_NCCL_ID_BYTES 128
+typedef struct ma_comm ma_comm;
+MA_API int ma_comm_unique_id(void* id_out);
+MA_API int ma_comm_create(const void* nccl_unique_id, int world, int rank, ma_comm** out);
+MA_API int ma_comm_destroy(ma_comm* c);
+MA_API int ma_comm_info(ma_comm* c, int* world, int* rank, int* nccl_version);
+/* In-place ncclAllReduce(max) of `count` device uint32 values on `stream`. */
+MA_API int ma_comm_allreduce_max_u32(ma_comm* c, uint32_t* d_buf, uint64_t count, void* stream);
+/* The step's skip decision across ranks: all-reduce(max) of *ma_stepper_flag(s). */
+MA_API int ma_stepper_allreduce_flag_async(ma_stepper* s, ma_comm* c, void* stream);
 
 /* ------------------------------------------------------------------ */
 /* Synthetic workload generators, bit-exact with simulator.hpp:23-42.

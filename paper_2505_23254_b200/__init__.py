@@ -10,6 +10,8 @@ from .capi import LIB_PATH, AdamHyper, MemAscendError, lib  # noqa: F401
 from .api import (  # noqa: F401
     DevicePool,
     DirectIoEngine,
+    NcclComm,
+    StepGraph,
     WeightPrefetcher,
     aligned_host_buffer,
     uring_available,
@@ -29,4 +31,5 @@ from .api import (  # noqa: F401
     overflow_check_async,
     plant_bits,
     pointer_kind,
+    torch_broadcast_bytes,
 )

@@ -47,6 +47,17 @@ def _info(x, kind=None):
     return a.ctypes.data, a.size, dt
 
 
+def _kind_ok(x, kind):
+    """x holds elements of `kind`: the matching torch dtype, or a raw-bits view
+    of the same width (int32 for f32, int16 for the 16-bit kinds)."""
+    if torch is None or not isinstance(x, torch.Tensor):
+        return True
+    code = _TORCH_DT.get(x.dtype)
+    if code is not None:
+        return code == capi.DTYPES[kind]
+    return x.element_size() == (4 if kind == "f32" else 2) and not x.is_floating_point()
+
+
 def _stream_ptr(stream):
     if stream is None:
         return torch.cuda.current_stream().cuda_stream if torch is not None else None
@@ -100,10 +111,17 @@ def adam_step_fp32(params, momentum, variance, grads, t: int, hyper: AdamHyper |
 def adam_step_fp32_async(params, momentum, variance, grads, t, hyper=None, loss_scale=1.0,
                          w_out=None, skip_flag=None, stream=None, grad_kind=None, w_kind=None):
     hyper = hyper or AdamHyper()
-    gp, n, gdt = _info(grads, grad_kind)
-    wp, _, wdt = _info(w_out, w_kind)
-    check(capi.lib().ma_adam_step_async(params.data_ptr(), momentum.data_ptr(),
-                                        variance.data_ptr(), gp, gdt, n, t, C.byref(hyper),
+    pp, n, _ = _info(params, "f32")
+    mp, nm, _ = _info(momentum, "f32")
+    vp, nv, _ = _info(variance, "f32")
+    gp, ng, gdt = _info(grads, grad_kind)
+    wp, nw, wdt = _info(w_out, w_kind)
+    for x in (params, momentum, variance):
+        if torch is not None and isinstance(x, torch.Tensor) and x.dtype != torch.float32:
+            raise MemAscendError(1, "adam_step: p/m/v must be float32")
+    if not (n == nm == nv == ng) or (w_out is not None and nw != n):
+        raise MemAscendError(1, "adam_step: parameter/state/grad lengths differ")
+    check(capi.lib().ma_adam_step_async(pp, mp, vp, gp, gdt, n, t, C.byref(hyper),
                                         loss_scale, wp, wdt,
                                         skip_flag.data_ptr() if skip_flag is not None else None,
                                         _stream_ptr(stream)))
@@ -225,23 +243,53 @@ class Stepper:
             _stream_ptr(stream), _stream_ptr(copy_stream)))
 
     @staticmethod
-    def subgroups(groups):
+    def subgroups(groups, g_dtype=None, w_dtype=None):
+        """ma_subgroup array of (p, m, v, g, w) tensors.  Every tensor must be
+        contiguous; p/m/v float32 of one length; g (and w, unless None) of that
+        length and — when given — of the stepper's gradient / working kinds."""
         arr = (capi.Subgroup * len(groups))()
         for k, (p, m, v, g, w) in enumerate(groups):
+            n = p.numel()
+            for name, x in (("p", p), ("m", m), ("v", v)):
+                _info(x, "f32")
+                if isinstance(x, torch.Tensor) and x.dtype != torch.float32:
+                    raise MemAscendError(1, f"sub-group {k}: {name} must be float32")
+                if x.numel() != n:
+                    raise MemAscendError(1, f"sub-group {k}: p/m/v lengths differ")
+            _, ng, _ = _info(g, g_dtype)
+            if ng != n:
+                raise MemAscendError(1, f"sub-group {k}: gradient length differs")
+            if g_dtype is not None and not _kind_ok(g, g_dtype):
+                raise MemAscendError(1, f"sub-group {k}: gradients are {g.dtype}, the stepper's "
+                                        f"gradient kind is {g_dtype}")
+            if w is not None:
+                _, nw, _ = _info(w, w_dtype if w_dtype not in (None, "none") else "bf16")
+                if nw != n:
+                    raise MemAscendError(1, f"sub-group {k}: working-weight length differs")
+                if w.element_size() != 2:
+                    raise MemAscendError(1, f"sub-group {k}: working weights must be 16-bit")
+            elif w_dtype not in (None, "none"):
+                raise MemAscendError(1, f"sub-group {k}: the stepper writes {w_dtype} working "
+                                        "weights but w is None")
             arr[k] = capi.Subgroup(p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
-                                   w.data_ptr() if w is not None else None, p.numel())
+                                   w.data_ptr() if w is not None else None, n)
         return arr
+
+    def _groups(self, groups):
+        if isinstance(groups, C.Array):
+            return groups
+        return self.subgroups(groups, self.g_dtype, self.w_dtype)
 
     def apply(self, groups, stream=None):
         """groups: list of (p, m, v, g, w) tensors, or a prebuilt subgroups() array."""
-        arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
+        arr = self._groups(groups)
         check(capi.lib().ma_stepper_apply_async(self._h, arr, len(arr), _stream_ptr(stream)))
 
     def apply_allgather(self, groups, ag: "GradReduceScatter", stream=None):
         """K2 fused with the weight all-gather: `ag` shares every rank's
         full-length working-weight buffer (a GradReduceScatter over it);
         groups' w are views of this rank's buffer."""
-        arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
+        arr = self._groups(groups)
         check(capi.lib().ma_stepper_apply_allgather_async(self._h, arr, len(arr), ag._h,
                                                           _stream_ptr(stream)))
 
@@ -258,7 +306,11 @@ class Stepper:
         """groups' p/m/v in registered host memory, g/w on the device; staging
         is a device fp32 tensor of 3 * slots * slot_elems.  Returns True when
         the step was skipped (no state moved)."""
-        arr = groups if isinstance(groups, C.Array) else self.subgroups(groups)
+        arr = self._groups(groups)
+        if staging.dtype != torch.float32 or not staging.is_contiguous() or \
+                staging.numel() < 3 * slots * slot_elems:
+            raise MemAscendError(1, "staging must be a contiguous float32 tensor of at least "
+                                    "3 * slots * slot_elems elements")
         if h2d_stream is None:
             self._h2d = getattr(self, "_h2d", None) or torch.cuda.Stream(device=staging.device)
             h2d_stream = self._h2d
@@ -280,16 +332,23 @@ class Stepper:
         buffer of host_slots x 3 x align4096(4 * slot_elems) bytes;
         dev_staging: device fp32 tensor of 3 * dev_slots * slot_elems.
         Returns True when the step was skipped (nothing read or written)."""
+        _check_staging(host_staging, host_slots, dev_staging, dev_slots, slot_elems, 3, 4)
         arr = (capi.SwapGroup * len(groups))()
         keep = []
         for k, (state, g, w) in enumerate(groups):
             n = g.numel()
+            if n > slot_elems:
+                raise MemAscendError(1, f"group {k}: {n} elements exceed slot_elems {slot_elems}")
+            if w is not None and w.numel() != n:
+                raise MemAscendError(1, f"group {k}: working-weight length differs")
             if isinstance(state[0], str):
                 keys = [x.encode() for x in state]
                 keep.append(keys)
                 arr[k] = capi.SwapGroup(keys[0], keys[1], keys[2], None, None, None,
                                         g.data_ptr(), w.data_ptr() if w is not None else None, n)
             else:
+                if any(_raw(x)[1] < 4 * n for x in state):
+                    raise MemAscendError(1, f"group {k}: host p/m/v shorter than the group")
                 p, m, v = (_raw(x)[0] for x in state)
                 arr[k] = capi.SwapGroup(None, None, None, p, m, v, g.data_ptr(),
                                         w.data_ptr() if w is not None else None, n)
@@ -315,9 +374,12 @@ class Stepper:
         memory, p the device bf16 weights.  host_staging: host_slots x 2 x
         align4096(2 * slot_elems) bytes; dev_staging: 2 * dev_slots *
         slot_elems bf16 (any 2-byte dtype)."""
+        _check_staging(host_staging, host_slots, dev_staging, dev_slots, slot_elems, 2, 2)
         arr = (capi.SwapGroupBf16 * len(groups))()
         keep = []
         for k, (state, p, g) in enumerate(groups):
+            if p.numel() > slot_elems or g.numel() != p.numel():
+                raise MemAscendError(1, f"group {k}: length exceeds slot_elems or g/p differ")
             if isinstance(state[0], str):
                 keys = [x.encode() for x in state]
                 keep.append(keys)
@@ -343,6 +405,31 @@ class Stepper:
     def finish(self, stream=None):
         check(capi.lib().ma_stepper_finish_async(self._h, _stream_ptr(stream)))
 
+    def allreduce_flag(self, comm: "NcclComm", stream=None):
+        """The step's cross-rank skip decision inside the library: one
+        ncclAllReduce(max) of the flag on the compute stream."""
+        check(capi.lib().ma_stepper_allreduce_flag_async(self._h, comm._h, _stream_ptr(stream)))
+
+    def set_state(self, scale: float, clean_steps: int, updates: int):
+        """Resume a saved run: LossScaler {scale, clean_steps} and the Adam
+        step count (OptimizerState::step_t); the next update uses t = updates + 1."""
+        check(capi.lib().ma_stepper_set_state(self._h, scale, clean_steps, updates))
+
+    def capture(self, fn, stream, reserve_steps: int = 1 << 20) -> "StepGraph":
+        """Record the *_async calls fn() makes on `stream` (a non-default
+        torch.cuda.Stream, which fn must use) into a CUDA graph; replay it
+        with StepGraph.launch().  Nothing executes during the capture."""
+        sp = _stream_ptr(stream)
+        check(capi.lib().ma_stepper_graph_begin(self._h, reserve_steps, sp))
+        try:
+            with torch.cuda.stream(stream):
+                fn()
+        finally:
+            g = C.c_void_p()
+            st = capi.lib().ma_stepper_graph_end(self._h, sp, C.byref(g))
+        check(st)
+        return StepGraph(g, self)
+
     def step(self, grads_list, groups, allreduce=None, stream=None):
         """One full step: check every grad buffer, optional cross-rank OR, update, scaler."""
         for g in grads_list:
@@ -366,6 +453,82 @@ class Stepper:
         check(capi.lib().ma_stepper_history(self._h, of.ctypes.data, sc.ctypes.data, cap,
                                             C.byref(cnt)))
         return of[:cnt.value].astype(bool), sc[:cnt.value]
+
+
+class StepGraph:
+    """A captured step chain (ma_graph): launch() replays it on a stream."""
+
+    def __init__(self, handle, stepper):
+        self._h, self._stepper = handle, stepper
+
+    def launch(self, stream=None):
+        check(capi.lib().ma_graph_launch(self._h, _stream_ptr(stream)))
+
+    def close(self):
+        if self._h:
+            capi.lib().ma_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NcclComm:
+    """NCCL communicator owned by the library (ma_comm_*).  Rank 0's unique id
+    is distributed by `broadcast(id_bytes_or_None) -> bytes` (any host
+    channel; `torch_broadcast_bytes()` uses torch.distributed)."""
+
+    def __init__(self, world: int, rank: int, broadcast):
+        uid = None
+        if rank == 0:
+            buf = (C.c_ubyte * capi.NCCL_ID_BYTES)()
+            check(capi.lib().ma_comm_unique_id(buf))
+            uid = bytes(buf)
+        uid = broadcast(uid)
+        assert len(uid) == capi.NCCL_ID_BYTES
+        h = C.c_void_p()
+        check(capi.lib().ma_comm_create((C.c_ubyte * capi.NCCL_ID_BYTES).from_buffer_copy(uid),
+                                        world, rank, C.byref(h)))
+        self._h = h
+        self.world, self.rank = world, rank
+
+    def info(self) -> dict:
+        w, r, v = C.c_int(), C.c_int(), C.c_int()
+        check(capi.lib().ma_comm_info(self._h, C.byref(w), C.byref(r), C.byref(v)))
+        return {"world": w.value, "rank": r.value, "nccl_version": v.value}
+
+    def allreduce_max_u32(self, t, stream=None):
+        """In-place all-reduce(max) of a device int32/uint32 tensor."""
+        if t.element_size() != 4 or not t.is_cuda or not t.is_contiguous():
+            raise MemAscendError(1, "allreduce_max_u32 needs a contiguous 4-byte device tensor")
+        check(capi.lib().ma_comm_allreduce_max_u32(self._h, t.data_ptr(), t.numel(),
+                                                   _stream_ptr(stream)))
+
+    def close(self):
+        if self._h:
+            capi.lib().ma_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def torch_broadcast_bytes(group=None, src=0):
+    """broadcast callable for NcclComm over torch.distributed (gloo or nccl)."""
+    import torch.distributed as dist
+
+    def bcast(b):
+        obj = [b]
+        dist.broadcast_object_list(obj, src=src, group=group)
+        return obj[0]
+
+    return bcast
 
 
 class FlagExchange:
@@ -594,8 +757,22 @@ class SwapOp:
             raise MemAscendError(4, "operation already waited on")
         out = C.c_uint64()
         h, self._h = self._h, None
-        check(capi.lib().ma_swap_wait(h, C.byref(out)))
+        try:
+            check(capi.lib().ma_swap_wait(h, C.byref(out)))
+        finally:
+            self._buf = None
         return out.value
+
+    def __del__(self):
+        # dropped without wait(): the store's workers may still read or write
+        # the buffer — finish the operation (and release the key) before the
+        # buffer reference goes away; its error, if any, is swallowed here
+        if getattr(self, "_h", None) is not None:
+            try:
+                capi.lib().ma_swap_wait(self._h, C.byref(C.c_uint64()))
+            except Exception:
+                pass
+            self._h = None
 
 
 class DevicePool:
@@ -690,6 +867,19 @@ def aligned_host_buffer(nbytes: int, register: bool = False) -> np.ndarray:
 
 
 # ----------------------------------------------------------------- host memory
+def _check_staging(host_staging, host_slots, dev_staging, dev_slots, slot_elems, ntens, esize):
+    """Sizes of the swapped pipeline's staging buffers (ma_stepper_apply_swapped*)."""
+    stride = (esize * slot_elems + 4095) // 4096 * 4096
+    if host_slots < 1 or dev_slots < 1 or slot_elems < 1:
+        raise MemAscendError(1, "host_slots, dev_slots and slot_elems must be >= 1")
+    if _raw(host_staging)[1] < host_slots * ntens * stride:
+        raise MemAscendError(1, f"host staging needs {host_slots * ntens * stride} bytes "
+                                f"({host_slots} slots x {ntens} x {stride})")
+    if not dev_staging.is_contiguous() or \
+            dev_staging.numel() * dev_staging.element_size() < dev_slots * ntens * slot_elems * esize:
+        raise MemAscendError(1, "device staging smaller than dev_slots x tensors x slot_elems")
+
+
 def _raw(x):
     """(pointer, bytes) of any tensor / array, whatever its dtype."""
     if torch is not None and isinstance(x, torch.Tensor):

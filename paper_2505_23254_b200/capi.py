@@ -22,13 +22,14 @@ ERROR_NAMES = {
     5: "unknown-region", 6: "pool-exhausted", 7: "size-violation", 8: "already-checked-out",
     9: "not-found", 10: "storage-full", 11: "device-error", 12: "capability", 13: "io-error",
     14: "alignment", 15: "busy", 16: "uncalibrated", 17: "bad-config",
-    100: "cuda-error", 101: "no-device",
+    100: "cuda-error", 101: "no-device", 102: "nccl-error",
 }
 
 DT_F32, DT_BF16, DT_F16, DT_NONE = 0, 1, 2, 3
 STEPPER_STATE_BYTES = 64
 IPC_HANDLE_BYTES = 64
 RS_HANDLE_BYTES = 192
+NCCL_ID_BYTES = 128
 DTYPES = {"f32": DT_F32, "bf16": DT_BF16, "f16": DT_F16, "none": DT_NONE}
 
 
@@ -145,6 +146,17 @@ SIGNATURES = [
     ("ma_stepper_finish_async", _I, [_VP, _VP]),
     ("ma_stepper_state", _I, [_VP, C.POINTER(StepState)]),
     ("ma_stepper_history", _I, [_VP, _VP, _VP, _U64, C.POINTER(_U64)]),
+    ("ma_stepper_set_state", _I, [_VP, _F, _U32, _U64]),
+    ("ma_stepper_graph_begin", _I, [_VP, _U64, _VP]),
+    ("ma_stepper_graph_end", _I, [_VP, _VP, C.POINTER(_VP)]),
+    ("ma_graph_launch", _I, [_VP, _VP]),
+    ("ma_graph_destroy", _I, [_VP]),
+    ("ma_comm_unique_id", _I, [_VP]),
+    ("ma_comm_create", _I, [_VP, _I, _I, C.POINTER(_VP)]),
+    ("ma_comm_destroy", _I, [_VP]),
+    ("ma_comm_info", _I, [_VP, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+    ("ma_comm_allreduce_max_u32", _I, [_VP, _VP, _U64, _VP]),
+    ("ma_stepper_allreduce_flag_async", _I, [_VP, _VP, _VP]),
     ("ma_gen_seeded_weights_async", _I, [_VP, _VP, _I, _U64, _U64, _U64, _VP]),
     ("ma_gen_pseudo_grads_async", _I, [_VP, _I, _VP, _I, _U64, _U64, _U64, _U64, _VP, _F, _VP]),
     ("ma_plant_bits_async", _I, [_VP, _I, _U64, _U32, _VP]),

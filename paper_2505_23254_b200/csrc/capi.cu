@@ -422,10 +422,14 @@ struct ma_stepper {
     ma::StepLog* d_log = nullptr;
     float2* d_bc = nullptr;
     uint64_t bc_cap = 0;
-    uint64_t issued = 0;  // finish calls enqueued
+    uint64_t issued = 0;  // finish calls enqueued since creation / the last set_state
+    uint64_t t_base = 0;  // updates at creation / the last set_state (resumed runs)
     cudaStream_t last = nullptr;
     int device = 0;
     bool owns_state = true;
+    bool capturing = false;        // between ma_stepper_graph_begin / _end
+    uint64_t capture_issued = 0;
+    std::vector<float2*> retired;  // superseded bias tables (graphs may hold them)
     std::vector<cudaEvent_t> events;
 
     cudaEvent_t event(uint64_t i) {
@@ -450,13 +454,14 @@ void stepper_grow_bc(ma_stepper* s, uint64_t need) {
     for (uint64_t t = 1; t <= cap; ++t) {
         bias_corrections(t, s->h.beta1, s->h.beta2, &host[t - 1].x, &host[t - 1].y);
     }
+    if (s->capturing)
+        fail(MA_ERR_LIFECYCLE, "bias-correction table exhausted during graph capture");
     float2* fresh = nullptr;
     CK(cudaMalloc(&fresh, cap * sizeof(float2)));
     CK(cudaMemcpy(fresh, host.data(), cap * sizeof(float2), cudaMemcpyHostToDevice));
-    if (s->d_bc) {
-        CK(cudaDeviceSynchronize());  // in-flight steps may still read the old table
-        CK(cudaFree(s->d_bc));
-    }
+    // in-flight steps and captured graphs may still read the old table: it
+    // is retired, not freed, until the stepper is destroyed
+    if (s->d_bc) s->retired.push_back(s->d_bc);
     s->d_bc = fresh;
     s->bc_cap = cap;
 }
@@ -703,6 +708,9 @@ int ma_stepper_create(const ma_adam_hyper* h, float init_scale, uint32_t growth_
             CK(cudaMemcpy(s->d_st, &init, sizeof init, cudaMemcpyHostToDevice));
             CK(cudaMemset(s->d_log, 0, sizeof(ma::StepLog) * ma::kHistory));
             stepper_grow_bc(s, 1024);
+            ma::launch_step_prepare(s->d_st, s->d_bc, s->c.eps, nullptr);
+            CK(cudaGetLastError());
+            CK(cudaDeviceSynchronize());
         } catch (...) {
             if (s->d_st && s->owns_state) cudaFree(s->d_st);
             if (s->d_log) cudaFree(s->d_log);
@@ -721,6 +729,7 @@ int ma_stepper_destroy(ma_stepper* s) {
         if (s->owns_state) cudaFree(s->d_st);
         cudaFree(s->d_log);
         cudaFree(s->d_bc);
+        for (float2* t : s->retired) cudaFree(t);
         delete s;
     });
 }
@@ -814,6 +823,21 @@ ma_xchg* xchg_new(int world, int rank, void* ipc_handle_out) {
     return x;
 }
 
+// How long a rank waits for its peers inside an exchange / barrier before
+// the whole job is stopped (poison + trap, kernels.cu xchg_post_wait):
+// MA_PEER_TIMEOUT_S seconds (fractional allowed), default 300.
+unsigned long long peer_timeout_ns() {
+    double secs = 300.0;
+    if (const char* e = std::getenv("MA_PEER_TIMEOUT_S")) {
+        char* end = nullptr;
+        const double v = std::strtod(e, &end);
+        if (end == e || !(v > 0.0) || v > 1e6)
+            fail(MA_ERR_INVALID_ARGUMENT, "MA_PEER_TIMEOUT_S must be a positive number of seconds");
+        secs = v;
+    }
+    return static_cast<unsigned long long>(secs * 1e9);
+}
+
 // all_handles: world records of `stride` bytes, the slot handle first in each
 void xchg_open_impl(ma_xchg* x, const void* all_handles, size_t stride) {
     if (x->ready) fail(MA_ERR_LIFECYCLE, "peer exchange already opened");
@@ -823,6 +847,7 @@ void xchg_open_impl(ma_xchg* x, const void* all_handles, size_t stride) {
     desc.my_slots = x->slots;
     desc.counter = x->local;
     desc.error = x->local + 1;
+    desc.timeout_ns = peer_timeout_ns();
     for (int r = 0; r < x->world; ++r) {
         if (r == x->rank) {
             desc.peer_slots[r] = x->slots;
@@ -947,7 +972,7 @@ int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t co
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        stepper_grow_bc(s, s->issued + 1);  // t <= finished steps + 1
+        stepper_grow_bc(s, s->t_base + s->issued + 2);  // t <= updates + 1, +1 prepared
         ma::AdamArgs a{};
         a.c = s->c;
         a.skip = &s->d_st->flag;
@@ -964,7 +989,7 @@ int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups, u
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        stepper_grow_bc(s, s->issued + 1);
+        stepper_grow_bc(s, s->t_base + s->issued + 2);
         ma::AdamArgs a{};
         a.c = s->c;
         a.skip = &s->d_st->flag;
@@ -1050,7 +1075,7 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
     if (skipped) *skipped = flag ? 1 : 0;
     s->last = cs;
     if (flag) return;
-    stepper_grow_bc(s, s->issued + 1);
+    stepper_grow_bc(s, s->t_base + s->issued + 2);
     int dev = 0;
     CK(cudaGetDevice(&dev));
     ma::swp::Engine* engp = e ? e->e : nullptr;
@@ -1358,7 +1383,8 @@ int ma_stepper_finish_async(ma_stepper* s, void* stream) {
     NvtxRange nvtx_range("ma_stepper_finish_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
-        ma::launch_step_finish(s->d_st, s->d_log, as_stream(stream));
+        stepper_grow_bc(s, s->t_base + s->issued + 2);  // the next update's scalars
+        ma::launch_step_finish(s->d_st, s->d_log, s->d_bc, s->c.eps, as_stream(stream));
         CK(cudaGetLastError());
         s->issued += 1;
         s->last = as_stream(stream);
@@ -1377,6 +1403,32 @@ int ma_stepper_state(ma_stepper* s, ma_step_state* out) {
         out->steps = st.steps;
         out->last_overflow = st.last_overflow;
         out->growth_interval = st.growth_interval;
+    });
+}
+
+// Resume: OptimizerState::step_t and LossScaler::{scale, clean_steps}
+// (optimizer.hpp:19-35,60-66) restored into the device-resident step state.
+int ma_stepper_set_state(ma_stepper* s, float scale, uint32_t clean_steps, uint64_t updates) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        if (s->capturing) fail(MA_ERR_LIFECYCLE, "set_state during graph capture");
+        if (!(scale > 0.0f)) fail(MA_ERR_INVALID_ARGUMENT, "loss scale must be > 0");
+        CK(cudaDeviceSynchronize());  // no step in flight reads the state
+        ma::StepDev st{};
+        CK(cudaMemcpy(&st, s->d_st, sizeof st, cudaMemcpyDeviceToHost));
+        if (clean_steps >= st.growth_interval)
+            fail(MA_ERR_INVALID_ARGUMENT, "clean_steps must be < growth_interval");
+        st.flag = 0;
+        st.scale = scale;
+        st.clean_steps = clean_steps;
+        st.updates = updates;
+        CK(cudaMemcpy(s->d_st, &st, sizeof st, cudaMemcpyHostToDevice));
+        s->t_base = updates;
+        s->issued = 0;
+        stepper_grow_bc(s, updates + 2);
+        ma::launch_step_prepare(s->d_st, s->d_bc, s->c.eps, nullptr);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
     });
 }
 
@@ -1789,7 +1841,7 @@ int ma_stepper_apply_allgather_async(ma_stepper* s, const ma_subgroup* groups, u
                                                   "rank's shared weight buffer");
         }
         const cudaStream_t st = as_stream(stream);
-        stepper_grow_bc(s, s->issued + 1);
+        stepper_grow_bc(s, s->t_base + s->issued + 2);
         ma::AdamArgs a{};
         a.c = s->c;
         a.skip = &s->d_st->flag;
@@ -1810,6 +1862,80 @@ int ma_stepper_apply_allgather_async(ma_stepper* s, const ma_subgroup* groups, u
         ma::launch_peer_barrier(ag->x->d_desc, ag->x->epoch, nullptr, st);
         CK(cudaGetLastError());
         s->last = st;
+    });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ CUDA graphs
+// A captured step chain (check -> [flag all-reduce] -> apply -> finish, any
+// sequence of *_async calls on one stream) replayed with one launch.  The
+// kernels read the loss scale, the skip flag and t on the device, so one
+// graph serves every later step; the only host-side state is the count of
+// finish calls (t's upper bound for the bias-correction table baked into the
+// graph, which begin() sizes for `reserve_steps` replays of one step).
+struct ma_graph {
+    ma_stepper* s = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t finishes = 0;  // finish calls per replay
+    uint64_t bc_cap = 0;    // capacity of the table the graph's kernels read
+};
+
+extern "C" {
+
+int ma_stepper_graph_begin(ma_stepper* s, uint64_t reserve_steps, void* stream) {
+    return guarded([&] {
+        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+        if (!stream) fail(MA_ERR_INVALID_ARGUMENT, "graph capture needs a non-default stream");
+        if (s->capturing) fail(MA_ERR_LIFECYCLE, "graph capture already in progress");
+        stepper_grow_bc(s, s->t_base + s->issued + reserve_steps + 2);
+        CK(cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal));
+        s->capturing = true;
+        s->capture_issued = s->issued;
+    });
+}
+
+int ma_stepper_graph_end(ma_stepper* s, void* stream, ma_graph** out) {
+    return guarded([&] {
+        if (!s || !out) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
+        if (!s->capturing) fail(MA_ERR_LIFECYCLE, "no graph capture in progress");
+        cudaGraph_t graph = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(as_stream(stream), &graph);
+        s->capturing = false;
+        const uint64_t finishes = s->issued - s->capture_issued;
+        s->issued = s->capture_issued;  // nothing executed yet
+        cuda_check(e, "cudaStreamEndCapture");
+        auto* g = new ma_graph();
+        g->s = s;
+        g->finishes = finishes;
+        g->bc_cap = s->bc_cap;
+        const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) {
+            delete g;
+            cuda_check(ie, "cudaGraphInstantiate");
+        }
+        *out = g;
+    });
+}
+
+int ma_graph_launch(ma_graph* g, void* stream) {
+    return guarded([&] {
+        if (!g) fail(MA_ERR_INVALID_ARGUMENT, "null graph");
+        ma_stepper* s = g->s;
+        if (s->t_base + s->issued + g->finishes + 1 > g->bc_cap)
+            fail(MA_ERR_LIFECYCLE, "graph's bias-correction table exhausted: capture again");
+        CK(cudaGraphLaunch(g->exec, as_stream(stream)));
+        s->issued += g->finishes;
+        s->last = as_stream(stream);
+    });
+}
+
+int ma_graph_destroy(ma_graph* g) {
+    return guarded([&] {
+        if (!g) return;
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        delete g;
     });
 }
 

@@ -37,34 +37,62 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 // flag into slot [epoch & 1][rank] of every peer (remote stores over
 // NVLink), then waits for all peers' entries of this epoch in its own slots
 // and replaces the local flag by the OR — the all-reduce(max) of the skip
-// decision without a separate collective launch.  A peer that never arrives
-// within ~2^35 cycles raises `error` and forces a skip instead of hanging.
+// decision without a separate collective launch.
+//
+// Failure is FATAL and shared, never a local decision: a rank whose peers do
+// not all arrive within timeout_ns (MA_PEER_TIMEOUT_S, default 300 s, wall
+// clock from %globaltimer) posts kXchgPoison into every peer's slots, sets
+// its error word and traps; a rank that reads a poisoned slot does the same.
+// No rank can therefore skip while another updates: a rank either completes
+// the exchange with every peer's value or dies, and a peer that completed
+// the exchange just before the poison landed dies at the next exchange —
+// the job stops loudly instead of continuing with diverged optimizer state.
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __noinline__ void xchg_abort(const XchgDev& x, unsigned lane) {
+    for (uint32_t r = lane; r < x.world; r += 32) {
+        st_release_sys(x.peer_slots[r] + x.rank, kXchgPoison);
+        st_release_sys(x.peer_slots[r] + x.world + x.rank, kXchgPoison);
+    }
+    if (lane == 0) atomicExch(x.error, 1u);
+    __threadfence_system();
+    __trap();
+}
+
 // One warp: publish (epoch << 1 | local) to every rank, wait for every
-// rank's value of this epoch; returns the OR of the flags (timed_out set if a
-// peer never arrived).
+// rank's value of this epoch; returns the OR of the flags.
 __device__ uint32_t xchg_post_wait(const XchgDev& x, unsigned long long epoch, uint32_t local,
-                                   unsigned lane, uint32_t* timed_out_out) {
+                                   unsigned lane) {
     const unsigned long long bank = epoch & 1ull;
     const unsigned long long val = (epoch << 1) | local;
     __threadfence_system();  // everything this rank wrote before is visible to the peers
     for (uint32_t r = lane; r < x.world; r += 32) {
         st_release_sys(x.peer_slots[r] + bank * x.world + x.rank, val);
     }
-    uint32_t any = 0, timed_out = 0;
-    const long long start = clock64();
-    for (uint32_t r = lane; r < x.world; r += 32) {
-        unsigned long long v;
+    uint32_t any = 0, failed = 0;
+    const unsigned long long start = global_ns();
+    for (uint32_t r = lane; r < x.world && !failed; r += 32) {
         for (;;) {
-            v = ld_acquire_sys(x.my_slots + bank * x.world + r);
-            if ((v >> 1) == epoch) break;
-            if (clock64() - start > (1ll << 35)) {
-                timed_out = 1;
+            const unsigned long long v = ld_acquire_sys(x.my_slots + bank * x.world + r);
+            if (v == kXchgPoison) {
+                failed = 1;
+                break;
+            }
+            if ((v >> 1) == epoch) {
+                any |= static_cast<uint32_t>(v & 1ull);
+                break;
+            }
+            if (global_ns() - start > x.timeout_ns) {
+                failed = 1;
                 break;
             }
         }
-        any |= static_cast<uint32_t>(v & 1ull);
     }
-    *timed_out_out = __any_sync(0xFFFFFFFFu, timed_out != 0u);
+    if (__any_sync(0xFFFFFFFFu, failed != 0u)) xchg_abort(x, lane);
     return __any_sync(0xFFFFFFFFu, any != 0u);
 }
 
@@ -81,11 +109,9 @@ __device__ void exchange_epilogue(const XchgDev* xp, unsigned long long epoch, u
     const XchgDev& x = *xp;
     __threadfence();
     const uint32_t local = *reinterpret_cast<volatile uint32_t*>(flag) != 0u;
-    uint32_t timed_out = 0;
-    const uint32_t any = xchg_post_wait(x, epoch, local, lane, &timed_out);
+    const uint32_t any = xchg_post_wait(x, epoch, local, lane);
     if (lane == 0) {
-        if (timed_out) atomicExch(x.error, 1u);
-        *flag = (any || timed_out) ? 1u : 0u;
+        *flag = any ? 1u : 0u;
         *x.counter = 0u;  // re-arm for the next launch (all CTAs have arrived)
         __threadfence();
     }
@@ -95,15 +121,10 @@ __device__ __forceinline__ void k1_exchange_epilogue(const K1Args& a, unsigned l
     exchange_epilogue(a.xchg, a.epoch, a.flag, lane);
 }
 
-// A peer missing at the barrier forces this step's skip (flag) and raises
-// the error word, like a timeout in the fused exchange.
+// Entry / exit barrier of the peer-memory collectives (same fatal rule).
 __global__ void k_peer_barrier(const XchgDev* xp, unsigned long long epoch, uint32_t* flag) {
-    uint32_t timed_out = 0;
-    xchg_post_wait(*xp, epoch, 0u, threadIdx.x & 31u, &timed_out);
-    if (threadIdx.x == 0 && timed_out) {
-        atomicExch(xp->error, 1u);
-        if (flag) *flag = 1u;
-    }
+    (void)flag;
+    xchg_post_wait(*xp, epoch, 0u, threadIdx.x & 31u);
 }
 
 // One-shot K1 (production): CTA b scans the U * 256 consecutive 16-byte
@@ -253,24 +274,39 @@ __global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
 
 
 // ============================================================== K2
-__device__ __forceinline__ bool resolve_step(const AdamArgs& a, StepScalars& s) {
-    if (a.skip != nullptr && *a.skip != 0u) return false;
-    if (a.st != nullptr) {
-        // device-resident scaler: t = applied updates + 1
-        const unsigned long long t = a.st->updates + 1ull;
-        const float2 bc = a.bc_table[t - 1ull];
-        s.scale = a.st->scale;
-        s.bc1 = bc.x;
-        s.bc2 = bc.y;
-    } else {
-        s.scale = a.scale;
-        s.bc1 = a.bc1;
-        s.bc2 = a.bc2;
-    }
+// Per-step scalars of an explicit step (scale, bc1, bc2 from the host).
+__device__ __forceinline__ void scalars_from(float scale, float bc1, float bc2, float eps,
+                                             StepScalars& s) {
+    s.scale = scale;
+    s.bc1 = bc1;
+    s.bc2 = bc2;
     s.scale_pow2 = exact_reciprocal(s.scale, &s.inv_scale);
-    s.fast = s.scale_pow2 && fast_step_ok(s.bc1, s.bc2, a.c.eps);
+    s.fast = s.scale_pow2 && fast_step_ok(s.bc1, s.bc2, eps);
     s.y1 = s.fast ? rcp_refined(s.bc1) : 0.0f;
     s.y2 = s.fast ? rcp_refined(s.bc2) : 0.0f;
+}
+
+__device__ __forceinline__ bool resolve_step(const AdamArgs& a, StepScalars& s) {
+    if (a.st != nullptr) {
+        // device-resident scaler: the flag, the scale and the precomputed
+        // scalars of t = updates + 1 in three independent loads (the skip
+        // flag of a stepper launch is always st->flag)
+        const uint4 h = *reinterpret_cast<const uint4*>(a.st);
+        const float4 q = *reinterpret_cast<const float4*>(&a.st->inv_scale);
+        const uint2 r = *reinterpret_cast<const uint2*>(&a.st->y2);
+        if (h.x != 0u) return false;
+        s.scale = __uint_as_float(h.z);
+        s.inv_scale = q.x;
+        s.bc1 = q.y;
+        s.bc2 = q.z;
+        s.y1 = q.w;
+        s.y2 = __uint_as_float(r.x);
+        s.scale_pow2 = (r.y & 1u) != 0u;
+        s.fast = (r.y & 2u) != 0u;
+        return true;
+    }
+    if (a.skip != nullptr && *a.skip != 0u) return false;
+    scalars_from(a.scale, a.bc1, a.bc2, a.c.eps, s);
     return true;
 }
 
@@ -1103,10 +1139,240 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_adam_bf16_v8(SegTable tab
     }
 }
 
+// -------------------------------------------------------------- K3 v2
+// Issue-slot economy for the pure-bf16 update (K3 moves half K2's bytes per
+// parameter, so at the same bandwidth it must retire twice the parameters
+// per second: it was instruction-bound at ~56 issued instructions per
+// parameter).  Changes against k3_adam_bf16, arithmetic unchanged:
+//  * 8-element slots: one 16-byte access per tensor and slot (7 memory
+//    instructions per 8 parameters instead of per 4);
+//  * bf16 widening straight from the packed words (shift / mask), narrowing
+//    by pair conversion (F2FP) — no unpacked intermediate arrays;
+//  * the admission guard as floating-point compares on |M|, V and |p|
+//    (ordered compares also reject NaN), accumulated in one predicate per
+//    slot: the same admitted set as fast_m_ok / fast_v_ok / fast_p_ok;
+//  * a slot that fails the guard takes the out-of-line exact path on its
+//    raw words (adam_exact8_bf16), so the fast path's registers hold nothing
+//    for it.
+template <int GK>
+struct K3Raw {
+    uint4 p, m, v;
+    uint4 g[GK == kF32 ? 2 : 1];
+};
+
+template <int GK>
+__device__ __forceinline__ float k3_grad(const K3Raw<GK>& r, int k) {
+    if constexpr (GK == kF32) {
+        const uint4& q = r.g[k >> 2];
+        return __uint_as_float((k & 3) == 0 ? q.x : (k & 3) == 1 ? q.y : (k & 3) == 2 ? q.z : q.w);
+    } else {
+        const uint4& q = r.g[0];
+        const uint32_t w = (k >> 1) == 0 ? q.x : (k >> 1) == 1 ? q.y : (k >> 1) == 2 ? q.z : q.w;
+        if constexpr (GK == kBF16) return (k & 1) ? __uint_as_float(w & 0xFFFF0000u) : __uint_as_float(w << 16);
+        return widen_f16((k & 1) ? (w >> 16) : (w & 0xFFFFu));
+    }
+}
+
+__device__ __forceinline__ float bf16_lane(const uint4& q, int k) {
+    const uint32_t w = (k >> 1) == 0 ? q.x : (k >> 1) == 1 ? q.y : (k >> 1) == 2 ? q.z : q.w;
+    return (k & 1) ? __uint_as_float(w & 0xFFFF0000u) : __uint_as_float(w << 16);
+}
+
+template <int GK>
+__device__ __noinline__ void adam_exact8_bf16(K3Raw<GK> r, uint4* out, const AdamConsts c,
+                                              const StepScalars s) {
+    float p[8], m[8], v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        p[k] = bf16_lane(r.p, k);
+        m[k] = bf16_lane(r.m, k);
+        v[k] = bf16_lane(r.v, k);
+        adam_elem<kOrdBf16>(p[k], m[k], v[k], k3_grad<GK>(r, k), c, s);
+    }
+    out[0] = make_uint4(narrow2<kBF16>(p[0], p[1]), narrow2<kBF16>(p[2], p[3]),
+                        narrow2<kBF16>(p[4], p[5]), narrow2<kBF16>(p[6], p[7]));
+    out[1] = make_uint4(narrow2<kBF16>(m[0], m[1]), narrow2<kBF16>(m[2], m[3]),
+                        narrow2<kBF16>(m[4], m[5]), narrow2<kBF16>(m[6], m[7]));
+    out[2] = make_uint4(narrow2<kBF16>(v[0], v[1]), narrow2<kBF16>(v[2], v[3]),
+                        narrow2<kBF16>(v[4], v[5]), narrow2<kBF16>(v[6], v[7]));
+}
+
+// One 8-element slot through the fast path; false when any element leaves
+// the guarded ranges (then nothing is produced).
+// NaN-propagating 3-input min / max (FMNMX3.NAN, sm_100): a NaN anywhere
+// makes the result NaN, which every ordered compare below rejects.
+__device__ __forceinline__ float min3n(float a, float b, float c) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float max3n(float a, float b, float c) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// GUARD: 0 = five compares per element, 1 = the same ranges tested once per
+// slot on NaN-propagating min / max reductions (FMNMX3.NAN).
+template <int GK, int GUARD = 0>
+__device__ __forceinline__ bool k3_fast8(const K3Raw<GK>& r, uint4& po, uint4& mo, uint4& vo,
+                                         const AdamConsts& c, const StepScalars& s) {
+    float P[8], M[8], V[8], AM[8], AP[8];
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const float p = bf16_lane(r.p, k), m = bf16_lane(r.m, k), v = bf16_lane(r.v, k);
+        const float g = __fmul_rn(k3_grad<GK>(r, k), s.inv_scale);
+        M[k] = __fadd_rn(__fmul_rn(c.beta1, m), __fmul_rn(c.one_minus_b1, g));
+        V[k] = __fadd_rn(__fmul_rn(c.beta2, v), __fmul_rn(c.one_minus_b2, __fmul_rn(g, g)));
+        const float am = fabsf(M[k]);
+        if constexpr (GUARD == 0) {
+            ok &= (am >= 0x1p-50f) & (am < 0x1p51f) & (V[k] >= 0x1p-96f) & (V[k] < 0x1p80f) &
+                  (fabsf(p) < __uint_as_float(0x7F800000u));
+        } else {
+            AM[k] = am;
+            AP[k] = fabsf(p);
+        }
+        const float mh = div_by(M[k], s.bc1, s.y1);
+        const float vh = div_by(V[k], s.bc2, s.y2);
+        const float den = __fadd_rn(sqrt_fast(vh), c.eps);
+        const float upd = __fmul_rn(c.lr, div_by(mh, den, rcp_refined(den)));
+        P[k] = __fsub_rn(__fsub_rn(p, upd), __fmul_rn(c.lr_wd, p));
+    }
+    po = make_uint4(narrow2_num<kBF16>(P[0], P[1]), narrow2_num<kBF16>(P[2], P[3]),
+                    narrow2_num<kBF16>(P[4], P[5]), narrow2_num<kBF16>(P[6], P[7]));
+    mo = make_uint4(narrow2_num<kBF16>(M[0], M[1]), narrow2_num<kBF16>(M[2], M[3]),
+                    narrow2_num<kBF16>(M[4], M[5]), narrow2_num<kBF16>(M[6], M[7]));
+    vo = make_uint4(narrow2_num<kBF16>(V[0], V[1]), narrow2_num<kBF16>(V[2], V[3]),
+                    narrow2_num<kBF16>(V[4], V[5]), narrow2_num<kBF16>(V[6], V[7]));
+    if constexpr (GUARD != 0) {
+        const float mn_m = min3n(min3n(AM[0], AM[1], AM[2]), min3n(AM[3], AM[4], AM[5]),
+                                 min3n(AM[6], AM[7], AM[7]));
+        const float mx_m = max3n(max3n(AM[0], AM[1], AM[2]), max3n(AM[3], AM[4], AM[5]),
+                                 max3n(AM[6], AM[7], AM[7]));
+        const float mn_v = min3n(min3n(V[0], V[1], V[2]), min3n(V[3], V[4], V[5]),
+                                 min3n(V[6], V[7], V[7]));
+        const float mx_v = max3n(max3n(V[0], V[1], V[2]), max3n(V[3], V[4], V[5]),
+                                 max3n(V[6], V[7], V[7]));
+        const float mx_p = max3n(max3n(AP[0], AP[1], AP[2]), max3n(AP[3], AP[4], AP[5]),
+                                 max3n(AP[6], AP[7], AP[7]));
+        ok = (mn_m >= 0x1p-50f) & (mx_m < 0x1p51f) & (mn_v >= 0x1p-96f) & (mx_v < 0x1p80f) &
+             (mx_p < __uint_as_float(0x7F800000u));
+    }
+    return ok;
+}
+
+// NOT an optimizer: the same loads / stores / grid with a trivial update
+// (A/B variant 16, MA_K3_VARIANT=16) — the access pattern's own ceiling.
+template <int GK>
+__device__ __forceinline__ void k3_probe8(const K3Raw<GK>& r, uint4& po, uint4& mo, uint4& vo) {
+    float P[8], M[8], V[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const float d = __fmul_rn(k3_grad<GK>(r, k), 1e-9f);
+        P[k] = __fadd_rn(bf16_lane(r.p, k), d);
+        M[k] = __fadd_rn(bf16_lane(r.m, k), d);
+        V[k] = __fadd_rn(bf16_lane(r.v, k), d);
+    }
+    po = make_uint4(narrow2_num<kBF16>(P[0], P[1]), narrow2_num<kBF16>(P[2], P[3]),
+                    narrow2_num<kBF16>(P[4], P[5]), narrow2_num<kBF16>(P[6], P[7]));
+    mo = make_uint4(narrow2_num<kBF16>(M[0], M[1]), narrow2_num<kBF16>(M[2], M[3]),
+                    narrow2_num<kBF16>(M[4], M[5]), narrow2_num<kBF16>(M[6], M[7]));
+    vo = make_uint4(narrow2_num<kBF16>(V[0], V[1]), narrow2_num<kBF16>(V[2], V[3]),
+                    narrow2_num<kBF16>(V[4], V[5]), narrow2_num<kBF16>(V[6], V[7]));
+}
+
+template <int GK, int U, int MINB, bool PROBE = false, int GUARD = 0>
+__global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs a) {
+    StepScalars sc;
+    if (!resolve_step(a, sc)) return;
+    const AdamConsts c = a.c;
+    constexpr uint32_t kGB = GK == kF32 ? 4u : 2u;
+    const uint64_t t = blockIdx.x;
+    if (t < tab.total_tiles) {
+        const Seg& sg = tab.seg[seg_of_tile(tab, t)];
+        const uint64_t lt = t - sg.tile_begin;
+        const uint64_t j0 = lt * (U * kK2Threads) + threadIdx.x;
+        const uint64_t e0 = sg.head + 8 * j0;
+        uint4* P = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sg.p) + e0);
+        uint4* M = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sg.m) + e0);
+        uint4* V = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sg.v) + e0);
+        const uint4* G = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(sg.g) + e0 * kGB);
+        const uint64_t nv = sg.nvec;
+        const bool full = (lt + 1) * (U * kK2Threads) <= nv;
+        constexpr int kS = kK2Threads;  // uint4 stride between a thread's slots
+        K3Raw<GK> q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (full || j0 + u * kK2Threads < nv) {
+                q[u].p = __ldcs(P + u * kS);
+                q[u].m = __ldcs(M + u * kS);
+                q[u].v = __ldcs(V + u * kS);
+                q[u].g[0] = __ldcs(G + u * kS * (kGB / 2));
+                if constexpr (GK == kF32) q[u].g[1] = __ldcs(G + u * kS * 2 + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (full || j0 + u * kK2Threads < nv) {
+                uint4 po, mo, vo;
+                if constexpr (PROBE) {
+                    k3_probe8<GK>(q[u], po, mo, vo);
+                } else if (!(sc.fast && k3_fast8<GK, GUARD>(q[u], po, mo, vo, c, sc))) {
+                    uint4 out[3];
+                    adam_exact8_bf16<GK>(q[u], out, c, sc);
+                    po = out[0];
+                    mo = out[1];
+                    vo = out[2];
+                }
+                __stcs(P + u * kS, po);
+                __stcs(M + u * kS, mo);
+                __stcs(V + u * kS, vo);
+            }
+        }
+        return;
+    }
+    const uint64_t q0 = t - tab.total_tiles;
+    const uint64_t nq = gridDim.x - tab.total_tiles;
+    for (uint32_t k = 0; k < tab.count; ++k) {
+        const Seg& sg = tab.seg[k];
+        if (sg.vector_ok) {
+            if (q0 != k % nq) continue;
+            const uint64_t tail_begin = sg.head + sg.nvec * 8;
+            const uint64_t extra = sg.head + (sg.n - tail_begin);
+            for (uint64_t i = threadIdx.x; i < extra; i += blockDim.x) {
+                bf16_state_scalar<GK>(sg, i < sg.head ? i : tail_begin + (i - sg.head), c, sc);
+            }
+        } else {
+            for (uint64_t e = q0 * blockDim.x + threadIdx.x; e < sg.n; e += nq * blockDim.x) {
+                bf16_state_scalar<GK>(sg, e, c, sc);
+            }
+        }
+    }
+}
+
 // ============================================================== step finish
+// The next update's scalars (t = updates + 1, current scale) into StepDev.
+__device__ void step_prepare(StepDev* st, const float2* bc_table, float eps) {
+    const float2 bc = bc_table[st->updates];
+    StepScalars s;
+    scalars_from(st->scale, bc.x, bc.y, eps, s);
+    st->inv_scale = s.scale_pow2 ? s.inv_scale : 0.0f;
+    st->bc1 = s.bc1;
+    st->bc2 = s.bc2;
+    st->y1 = s.y1;
+    st->y2 = s.y2;
+    st->mode = (s.scale_pow2 ? 1u : 0u) | (s.fast ? 2u : 0u);
+}
+
+__global__ void k_step_prepare(StepDev* st, const float2* bc_table, float eps) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) step_prepare(st, bc_table, eps);
+}
+
 // LossScaler::on_overflow / on_clean_step (optimizer.hpp:24-34) and the
-// update counter (simulator.cpp:438-444,491); re-arms the flag.
-__global__ void k_step_finish(StepDev* st, StepLog* log) {
+// update counter (simulator.cpp:438-444,491); re-arms the flag and prepares
+// the next update's scalars.
+__global__ void k_step_finish(StepDev* st, StepLog* log, const float2* bc_table, float eps) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const uint32_t of = st->flag != 0u;
     if (of) {
@@ -1124,6 +1390,7 @@ __global__ void k_step_finish(StepDev* st, StepLog* log) {
     st->steps += 1ull;
     st->last_overflow = of;
     st->flag = 0u;
+    step_prepare(st, bc_table, eps);
 }
 
 // ============================================================== generators
@@ -1801,23 +2068,40 @@ void launch_k2_allgather(int gk, int wk, const SegTable& tab, const AdamArgs& a,
 #undef MA_AG
 }
 
-// K3 A/B (MA_K3_VARIANT): 0 = 4 slots held to 4 CTA/SM (64 regs,
-// production for bf16 gradients, 0.94), 1 = 4 slots unbounded (80 regs,
-// 3 CTA/SM, 0.90), 2 = 2 slots at 4 CTA/SM (0.84), 3 = 8 slots (0.89),
-// 4 = 8-element slots at 4 CTA/SM (0.90, spills), 5 = 8-element unbounded (0.80),
-// 6 = 2 slots at 5 CTA/SM (0.86), 7 = 3 slots at 4 CTA/SM (0.91), 8 = 4 slots at 5 CTA/SM (0.88).
+// K3 A/B (MA_K3_VARIANT), fractions of the copy peak at 268 M
+// params, bf16 g.  0 (= 17) = production: k3_v2, two 8-element slots per
+// thread at 4 CTA/SM, the admission guard on NaN-propagating min / max
+// reductions (0.981).  Other k3_v2 shapes: 9 = per-element compare guard
+// (0.975), 10 = 9 at 3 CTA/SM (0.95), 11 = one slot at 4 (0.87), 12 = four
+// slots at 2 (0.96), 13 = two slots unbounded (0.80), 14 = one slot at 6
+// (0.87), 18 = 0 at 3 CTA/SM (0.95), 16 = access-pattern probe, no Adam
+// (1.01: the ceiling).  Round-1 kernels (k3_adam_bf16, 4-element slots):
+// 15 = 4 slots at 4 CTA/SM (the round-1 production, 0.94 before / 0.89 after
+// the x86-NaN exact path), 1 = 4 slots unbounded (0.90), 2 = 2 slots at 4
+// (0.84), 3 = 8 slots (0.89), 4/5 = 8-element slots at 4 / unbounded
+// (0.90 / 0.80), 6 = 2 slots at 5 (0.86), 7 = 3 slots at 4 (0.91), 8 = 4
+// slots at 5 (0.88).
 int k3_slots(int gk, int variant) {
-    if (gk != kBF16) return kK3Slots;
-    return variant == 2 ? 2 : variant == 3 ? 8 : (variant == 4 || variant == 5) ? 2
-           : variant == 6 ? 2 : variant == 7 ? 3 : variant == 8 ? 4 : kK3Slots;
+    if (gk != kBF16) return 2;  // k3_v2<GK, 2, 4>
+    switch (variant) {
+        case 0: case 2: case 4: case 5: case 6: case 9: case 10: case 13: return 2;
+        case 3: return 8;
+        case 7: return 3;
+        case 11: case 14: return 1;
+        case 1: case 8: case 12: case 15: return 4;
+        default: return 2;
+    }
 }
 
-int k3_vec(int gk, int variant) { return gk == kBF16 && (variant == 4 || variant == 5) ? 8 : 4; }
+int k3_vec(int gk, int variant) {
+    if (gk != kBF16) return 8;
+    return (variant >= 1 && variant <= 3) || (variant >= 6 && variant <= 8) || variant == 15 ? 4 : 8;
+}
 
 template <typename F>
 void k3_dispatch(int gk, int variant, F&& f) {
-    if (gk == kF32) return f(k3_adam_bf16<kF32>);
-    if (gk == kF16) return f(k3_adam_bf16<kF16>);
+    if (gk == kF32) return f(k3_v2<kF32, 2, 4, false, 1>);
+    if (gk == kF16) return f(k3_v2<kF16, 2, 4, false, 1>);
     switch (variant) {
         case 1: return f(k3_adam_bf16<kBF16, 4, 1>);
         case 2: return f(k3_adam_bf16<kBF16, 2, 4>);
@@ -1827,7 +2111,16 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 6: return f(k3_adam_bf16<kBF16, 2, 5>);
         case 7: return f(k3_adam_bf16<kBF16, 3, 4>);
         case 8: return f(k3_adam_bf16<kBF16, 4, 5>);
-        default: return f(k3_adam_bf16<kBF16, 4, 4>);
+        case 10: return f(k3_v2<kBF16, 2, 3>);
+        case 11: return f(k3_v2<kBF16, 1, 4>);
+        case 12: return f(k3_v2<kBF16, 4, 2>);
+        case 13: return f(k3_v2<kBF16, 2, 1>);
+        case 14: return f(k3_v2<kBF16, 1, 6>);
+        case 15: return f(k3_adam_bf16<kBF16, 4, 4>);
+        case 9: return f(k3_v2<kBF16, 2, 4>);
+        case 16: return f(k3_v2<kBF16, 2, 4, true>);
+        case 18: return f(k3_v2<kBF16, 2, 3, false, 1>);
+        default: return f(k3_v2<kBF16, 2, 4, false, 1>);
     }
 }
 
@@ -1844,8 +2137,13 @@ void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsi
     k3_dispatch(gk, variant, [&](auto fn) { fn<<<grid, kK2Threads, 0, st>>>(tab, a); });
 }
 
-void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s) {
-    k_step_finish<<<1, 32, 0, s>>>(st, log);
+void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, float eps,
+                        cudaStream_t s) {
+    k_step_finish<<<1, 32, 0, s>>>(st, log, bc_table, eps);
+}
+
+void launch_step_prepare(StepDev* st, const float2* bc_table, float eps, cudaStream_t s) {
+    k_step_prepare<<<1, 32, 0, s>>>(st, bc_table, eps);
 }
 
 void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,

@@ -25,10 +25,15 @@ struct XchgDev {
     unsigned long long* peer_slots[kMaxRanks];  // rank r's slot array, mapped here
     unsigned long long* my_slots;               // this rank's slot array [2][world]
     unsigned int* counter;                      // K1 CTAs finished (last CTA exchanges)
-    unsigned int* error;                        // set on a peer timeout
+    unsigned int* error;                        // set before a fatal timeout / poison trap
     uint32_t world;
     uint32_t rank;
+    unsigned long long timeout_ns;              // MA_PEER_TIMEOUT_S (default 300 s)
 };
+
+// Posted into every peer's slots by a rank that gives up on an exchange: a
+// value no epoch can take (epochs are < 2^63).  Whoever reads it traps too.
+constexpr unsigned long long kXchgPoison = ~0ull;
 
 struct K1Args {
     const uint4* body;      // 16-byte aligned vector body
@@ -145,7 +150,9 @@ int rs_units_for(int sk, uint32_t nsrc);
 // sets *flag (when non-null) so the step is skipped
 void launch_peer_barrier(const XchgDev* x, unsigned long long epoch, uint32_t* flag,
                          cudaStream_t st);
-void launch_step_finish(StepDev* st, StepLog* log, cudaStream_t s);
+void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, float eps,
+                        cudaStream_t s);
+void launch_step_prepare(StepDev* st, const float2* bc_table, float eps, cudaStream_t s);
 void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,
                         unsigned grid, cudaStream_t st);
 void launch_gen_grads(int gk, int wk, void* g, const uint16_t* w, uint64_t n, uint64_t base,

@@ -19,13 +19,18 @@ void check_status(int status) {
 }  // namespace
 
 StepDriver::StepDriver(const AdamHyper& hyper, const LossScaler& scaler, int grad_dtype,
-                       int working_dtype) {
-    if (scaler.clean_steps != 0)
-        raise(ErrorCode::invalid_argument,
-              "StepDriver starts a fresh LossScaler (clean_steps must be 0)");
+                       int working_dtype, std::uint64_t step_t) {
     const ma_adam_hyper h{hyper.lr, hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay};
-    check_status(ma_stepper_create(&h, scaler.scale, scaler.growth_interval, grad_dtype, working_dtype,
-                            nullptr, &h_));
+    check_status(ma_stepper_create(&h, scaler.scale, scaler.growth_interval, grad_dtype,
+                                   working_dtype, nullptr, &h_));
+    if (scaler.clean_steps != 0 || step_t != 0) {
+        const int st = ma_stepper_set_state(h_, scaler.scale, scaler.clean_steps, step_t);
+        if (st != MA_OK) {
+            ma_stepper_destroy(h_);
+            h_ = nullptr;
+            check_status(st);
+        }
+    }
 }
 
 StepDriver::~StepDriver() {
@@ -54,6 +59,46 @@ bool StepDriver::apply_swapped(DirectIoEngine& store, std::span<const ma_swap_gr
 }
 
 void StepDriver::finish(void* stream) { check_status(ma_stepper_finish_async(h_, stream)); }
+
+void StepDriver::exchange(Communicator& comm, void* stream) {
+    check_status(ma_stepper_allreduce_flag_async(h_, comm.handle(), stream));
+}
+
+void StepDriver::resume(const LossScaler& scaler, std::uint64_t step_t) {
+    check_status(ma_stepper_set_state(h_, scaler.scale, scaler.clean_steps, step_t));
+}
+
+void StepDriver::capture_begin(void* stream, std::uint64_t reserve_steps) {
+    check_status(ma_stepper_graph_begin(h_, reserve_steps, stream));
+}
+
+StepGraph StepDriver::capture_end(void* stream) {
+    ma_graph* g = nullptr;
+    check_status(ma_stepper_graph_end(h_, stream, &g));
+    return StepGraph(g);
+}
+
+StepGraph::~StepGraph() {
+    if (g_) ma_graph_destroy(g_);
+}
+
+void StepGraph::launch(void* stream) { check_status(ma_graph_launch(g_, stream)); }
+
+std::array<unsigned char, MA_NCCL_ID_BYTES> Communicator::unique_id() {
+    std::array<unsigned char, MA_NCCL_ID_BYTES> id{};
+    check_status(ma_comm_unique_id(id.data()));
+    return id;
+}
+
+Communicator::Communicator(int world, int rank,
+                           const std::array<unsigned char, MA_NCCL_ID_BYTES>& id)
+    : world_(world), rank_(rank) {
+    check_status(ma_comm_create(id.data(), world, rank, &h_));
+}
+
+Communicator::~Communicator() {
+    if (h_) ma_comm_destroy(h_);
+}
 
 LossScaler StepDriver::scaler() const {
     ma_step_state s{};

@@ -3,13 +3,21 @@
 // cfg_bf16_n100003 (tests/golden/workload.json) through memascend::StepDriver
 // — generators from the C ABI, K1 -> K2 -> scaler per step — once over
 // HBM-resident sub-groups and once with every sub-group's state in a
-// DirectIoEngine store (apply_swapped).  Prints the final FNV-1a digests of
-// p/m/v/w, the scale and t; the test compares them with the golden values.
+// DirectIoEngine store (apply_swapped).  Further modes, same golden digests:
+//   nccl    the cross-rank decision through the library's NCCL communicator
+//           (world 1: Communicator + StepDriver::exchange between K1 and K2);
+//   graph   check -> exchange -> apply -> finish captured once into a CUDA
+//           graph and replayed every step (gradients produced outside it);
+//   resume  three steps, then a NEW StepDriver built from the saved
+//           LossScaler and step_t continues the run (checkpoint/restart).
+// Prints the final FNV-1a digests of p/m/v/w, the scale and t; the test
+// compares them with the golden values.
 #include <cuda_runtime.h>
 
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -33,7 +41,8 @@ static float f(std::uint32_t u) {
 
 int main(int argc, char** argv) {
     if (argc < 3) return 2;
-    const bool swapped = std::string(argv[1]) == "swapped";
+    const std::string mode = argv[1];
+    const bool swapped = mode == "swapped";
     const std::string dir = argv[2];
     const std::uint64_t n = 100003, sub = 30000, seed = 1;
     AdamHyper h;
@@ -57,7 +66,10 @@ int main(int argc, char** argv) {
         cudaStreamCreate(&h2d);
         cudaStreamCreate(&d2h);
         if (ma_gen_seeded_weights_async(p, w, MA_DT_BF16, n, 0, seed, st)) return 3;
-        StepDriver drv(h, LossScaler{}, MA_DT_BF16, MA_DT_BF16);
+        auto drv_ptr = std::make_unique<StepDriver>(h, LossScaler{}, MA_DT_BF16, MA_DT_BF16);
+        std::unique_ptr<Communicator> comm;
+        if (mode == "nccl" || mode == "graph")
+            comm = std::make_unique<Communicator>(1, 0, Communicator::unique_id());
         std::vector<ma_subgroup> groups;
         for (std::uint64_t o = 0; o < n; o += sub) {
             const std::uint64_t k = std::min(sub, n - o);
@@ -95,18 +107,41 @@ int main(int argc, char** argv) {
             cudaMalloc(&dstage, 2 * 3 * slot * 4);
         }
         SwapStaging staging{hstage, 2, dstage, 2, slot, h2d, d2h};
+        std::unique_ptr<StepGraph> graph;
+        if (mode == "graph") {
+            StepDriver& d = *drv_ptr;
+            d.capture_begin(st, 16);
+            d.check(g, n, st);
+            d.exchange(*comm, st);
+            d.apply(groups, st);
+            d.finish(st);
+            graph = std::make_unique<StepGraph>(d.capture_end(st));
+        }
         for (std::uint64_t s = 0; s < 6; ++s) {
+            if (mode == "resume" && s == 3) {
+                // checkpoint: the scaler and t; p/m/v/w stay where they are
+                const LossScaler saved = drv_ptr->scaler();
+                const std::uint64_t step_t = drv_ptr->updates();
+                drv_ptr = std::make_unique<StepDriver>(h, saved, MA_DT_BF16, MA_DT_BF16, step_t);
+            }
+            StepDriver& drv = *drv_ptr;
             ma_gen_pseudo_grads_async(g, MA_DT_BF16, w, MA_DT_BF16, n, 0, seed, s,
                                       ma_stepper_scale(drv.handle()), 0.0f, st);
             if (s == 2) ma_plant_bits_async(g, MA_DT_BF16, 777, 32704, st);
             if (s == 4) ma_plant_bits_async(g, MA_DT_BF16, 100002, 32639, st);
+            if (graph) {
+                graph->launch(st);
+                continue;
+            }
             drv.check(g, n, st);
+            if (comm) drv.exchange(*comm, st);
             if (swapped)
                 drv.apply_swapped(*store, sg, staging, st);
             else
                 drv.apply(groups, st);
             drv.finish(st);
         }
+        StepDriver& drv = *drv_ptr;
         cudaStreamSynchronize(st);
         std::vector<float> hp(n), hm(n), hv(n);
         std::vector<uint16_t> hw(n);

@@ -155,7 +155,7 @@ def test_cpp_device_pool_and_prefetcher(tmp_path):
     assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stdout + p.stderr
 
 
-@pytest.mark.parametrize("mode", ["hbm", "swapped"])
+@pytest.mark.parametrize("mode", ["hbm", "swapped", "nccl", "graph", "resume"])
 def test_cpp_step_driver_workload_golden(golden, tmp_path, mode):
     """include/memascend/step_driver.hpp from C++: the reference's workload
     case through StepDriver (HBM-resident and swapped) ends on the golden
@@ -175,7 +175,10 @@ def test_cpp_step_driver_workload_golden(golden, tmp_path, mode):
     p = subprocess.run([exe, mode, str(tmp_path / "store")], capture_output=True, text=True,
                        timeout=120)
     assert p.returncode == 0, p.stdout + p.stderr
-    got = dict(line.split() for line in p.stdout.split("\n") if line.strip())
+    keys = {"p", "m", "v", "w", "scale", "updates"}
+    got = dict(line.split() for line in p.stdout.split("\n")
+               if len(line.split()) == 2 and line.split()[0] in keys)
+    assert keys <= set(got), p.stdout + p.stderr
     c = next(x for x in golden("workload.json")["cases"] if x["name"] == "cfg_bf16_n100003")
     last = c["per_step"][-1]
     for k in "pmvw":

@@ -1,0 +1,174 @@
+"""Step-driver runtime features on the B200, each against the oracle's
+composition of the reference (bit for bit):
+
+  * resume: LossScaler {scale, clean_steps} and OptimizerState::step_t
+    restored into a NEW stepper (optimizer.hpp:19-35,60-66,
+    optimizer.cpp:120-124) continue a run exactly — 5 steps, snapshot,
+    5 more == 10 steps, including a skipped step on each side of the cut and
+    a scale growth right after it;
+  * CUDA graph: check -> apply -> finish captured once and replayed every
+    step (the loss scale, flag and t stay on the device, so one graph serves
+    all steps), gradients produced outside the graph;
+  * NCCL in the library: a world-1 communicator's all-reduce(max) of the
+    flag between K1 and K2, eager and inside the graph.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a B200", allow_module_level=True)
+
+import paper_2505_23254_b200 as mab  # noqa: E402
+from oracle import oracle as ora  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+N, SUB, SEED = 100_003, 30_000, 1
+HYP = dict(weight_decay=0.01)
+FAULTS = [(2, 4242, 0x7FC0), (7, 99, 0xFF80)]
+
+
+class Run:
+    def __init__(self, growth=2000, init_scale=65536.0):
+        dev = torch.device("cuda", 0)
+        self.p = torch.empty(N, dtype=torch.float32, device=dev)
+        self.m = torch.zeros(N, dtype=torch.float32, device=dev)
+        self.v = torch.zeros(N, dtype=torch.float32, device=dev)
+        self.w = torch.empty(N, dtype=torch.bfloat16, device=dev)
+        self.g = torch.empty(N, dtype=torch.bfloat16, device=dev)
+        mab.gen_seeded_weights(self.p, self.w, seed=SEED)
+        self.growth = growth
+        self.st = mab.Stepper(mab.AdamHyper(**HYP), init_scale, growth, "bf16", "bf16")
+        self.groups = mab.Stepper.subgroups(
+            [(self.p[o:o + SUB], self.m[o:o + SUB], self.v[o:o + SUB], self.g[o:o + SUB],
+              self.w[o:o + SUB]) for o in range(0, N, SUB)], "bf16", "bf16")
+
+    def produce(self, s, stream=None):
+        mab.gen_pseudo_grads(self.g, self.w, step=s, seed=SEED, d_scale=self.st.scale_t,
+                             stream=stream)
+        for fs, idx, bits in FAULTS:
+            if fs == s:
+                mab.plant_bits(self.g, idx, bits, stream=stream)
+
+    def bits(self):
+        torch.cuda.synchronize()
+        return {k: getattr(self, k).view(torch.int32 if k in "pmv" else torch.int16).cpu().numpy()
+                for k in "pmvw"}
+
+
+def oracle(steps, growth=2000, init_scale=65536.0):
+    return ora.train(N, steps, SEED, g_kind="bf16", w_kind="bf16", hyp=ora.hyper(**HYP),
+                     scale=init_scale, growth=growth, faults=FAULTS)
+
+
+def same(run, ref):
+    b = run.bits()
+    for k in "pmv":
+        assert np.array_equal(b[k].view(np.uint32), ref[k].view(np.uint32)), k
+    assert np.array_equal(b["w"].view(np.uint16), ref["w"])
+
+
+def test_resume_equals_uninterrupted_run():
+    growth = 3  # the scale grows on the first step after the cut
+    ref = oracle(10, growth=growth)
+    a = Run(growth)
+    for s in range(5):
+        a.produce(s)
+        a.st.step([a.g], a.groups)
+    snap = a.st.state()
+    assert snap["updates"] == 4 and snap["clean_steps"] == 2  # step 2 was skipped
+    b = Run(growth)
+    b.p.copy_(a.p), b.m.copy_(a.m), b.v.copy_(a.v), b.w.copy_(a.w)
+    a.st.close()
+    b.st.set_state(snap["scale"], snap["clean_steps"], snap["updates"])
+    for s in range(5, 10):
+        b.produce(s)
+        b.st.step([b.g], b.groups)
+    same(b, ref)
+    st = b.st.state()
+    assert st["updates"] == 8 and st["scale"] == float(ref["scale_after"][-1])
+    of, sc = b.st.history()
+    assert of.tolist() == ref["overflow"][5:].astype(bool).tolist()
+    assert sc.tolist() == ref["scale_after"][5:].tolist()
+
+
+def test_set_state_validation():
+    r = Run()
+    with pytest.raises(mab.MemAscendError):
+        r.st.set_state(0.0, 0, 3)
+    with pytest.raises(mab.MemAscendError):
+        r.st.set_state(1024.0, 2000, 3)  # clean_steps must stay below growth_interval
+
+
+@pytest.mark.parametrize("with_comm", [False, True])
+def test_graph_replay_equals_eager(with_comm):
+    ref = oracle(10)
+    r = Run()
+    stream = torch.cuda.Stream()
+    comm = mab.NcclComm(1, 0, lambda b: b) if with_comm else None
+
+    def chain():
+        r.st.check(r.g, stream=stream)
+        if comm is not None:
+            r.st.allreduce_flag(comm, stream=stream)
+        r.st.apply(r.groups, stream=stream)
+        r.st.finish(stream=stream)
+
+    stream.wait_stream(torch.cuda.current_stream())
+    graph = r.st.capture(chain, stream, reserve_steps=64)
+    for s in range(10):
+        r.produce(s, stream=stream)
+        graph.launch(stream)
+    stream.synchronize()
+    same(r, ref)
+    of, sc = r.st.history()
+    assert of.tolist() == ref["overflow"].astype(bool).tolist()
+    assert sc.tolist() == ref["scale_after"].tolist()
+    assert r.st.state()["steps"] == 10
+    graph.close()
+    if comm is not None:
+        assert comm.info()["world"] == 1 and comm.info()["nccl_version"] > 0
+        comm.close()
+
+
+def test_graph_reserve_exhaustion_is_reported():
+    r = Run()
+    stream = torch.cuda.Stream()
+
+    def chain():
+        r.st.check(r.g, stream=stream)
+        r.st.apply(r.groups, stream=stream)
+        r.st.finish(stream=stream)
+
+    graph = r.st.capture(chain, stream, reserve_steps=3)
+    launched = 0
+    with pytest.raises(mab.MemAscendError) as e:
+        for s in range(100000):
+            graph.launch(stream)
+            launched += 1
+    assert e.value.code == "lifecycle" and launched >= 3
+    stream.synchronize()
+
+
+def test_nccl_flag_allreduce_eager():
+    ref = oracle(10)
+    r = Run()
+    comm = mab.NcclComm(1, 0, lambda b: b)
+    for s in range(10):
+        r.produce(s)
+        r.st.check(r.g)
+        r.st.allreduce_flag(comm)
+        r.st.apply(r.groups)
+        r.st.finish()
+    same(r, ref)
+    comm.close()
+
+
+def test_subgroup_validation():
+    r = Run()
+    with pytest.raises(mab.MemAscendError):  # f32 grads for a bf16 stepper
+        r.st.apply([(r.p, r.m, r.v, torch.zeros(N, device="cuda"), r.w)])
+    with pytest.raises(mab.MemAscendError):  # length mismatch
+        r.st.apply([(r.p, r.m, r.v[:-1], r.g, r.w)])
+    with pytest.raises(mab.MemAscendError):  # missing working weights
+        r.st.apply([(r.p, r.m, r.v, r.g, None)])
