@@ -49,7 +49,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg4", "cfg5"], default="cfg2")
+    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg3", "cfg4", "cfg5"], default="cfg2",
+                    help="BASELINE.json configs[n-1]; cfg3 = cfg2's partition per rank with "
+                         "the seeded inf/NaN injection plan, decisions checked against the "
+                         "committed oracle plan")
     ap.add_argument("--slots", type=int, default=3, help="cfg4 staging slots")
     ap.add_argument("--slot-params", type=int, default=1 << 24, help="cfg4 params per slot")
     ap.add_argument("--params", type=int, default=0, help="override params per GPU (debug)")
@@ -68,9 +71,13 @@ def parse():
                     help="cfg5 optimizer state: fp32 master/m/v (K2) or bf16 m/v + bf16 "
                          "weights (OptimPrecision::pure_bf16, K3)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--flag-exchange", choices=["nccl", "p2p"], default="nccl",
-                    help="N>1: all-reduce the skip flag with NCCL, or fuse the exchange into "
-                         "K1 over peer memory")
+    ap.add_argument("--flag-exchange", choices=["nccl", "torch", "p2p"], default="nccl",
+                    help="N>1: all-reduce the skip flag with the library's own NCCL "
+                         "communicator (ma_comm, default), with torch.distributed, or fuse "
+                         "the exchange into K1 over peer memory")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture check -> exchange -> apply -> finish into a CUDA graph once "
+                         "and replay it every step (one launch per step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=CFG1,
                     help="params in the CPU baseline's bounded sample")
@@ -237,6 +244,8 @@ def reference_arm(args, n_per_gpu, rank, world):
 
 def workload_config(args, n, world):
     name = ("llama3-8b-optimizer-state-hbm" if args.config == "cfg2" and not args.params
+            else "llama3-8b-optimizer-state-hbm-inf-nan-injection" if args.config == "cfg3"
+            and not args.params
             else "cfg1-64M-subgroup" if args.config == "cfg1" and not args.params
             else "qwen2.5-14b-shard-streamed-from-host" if args.config == "cfg4"
             and not args.params
@@ -255,11 +264,65 @@ def workload_config(args, n, world):
 
 
 # --------------------------------------------------------------- our arm
+class Exchange:
+    """The step's cross-rank skip decision (N > 1): the library's own NCCL
+    communicator (ma_comm: ncclAllReduce(max) of the flag on the compute
+    stream, capturable), torch.distributed's all-reduce, or the OR fused into
+    K1's last CTA over peer memory (ma_xchg)."""
+
+    def __init__(self, mode, world, rank):
+        import paper_2505_23254_b200 as mab
+
+        self.mode, self.world = mode, world
+        self.comm = self.xchg = None
+        if world > 1 and mode == "nccl":
+            self.comm = mab.NcclComm(world, rank, mab.torch_broadcast_bytes())
+        elif world > 1 and mode == "p2p":
+            self.xchg = mab.api.FlagExchange(world, rank, mab.api.torch_all_gather_bytes())
+
+    def after_check(self, st, stream):
+        import torch
+        import torch.distributed as dist
+
+        if self.comm is not None:
+            st.allreduce_flag(self.comm, stream=stream)
+        elif self.world > 1 and self.mode == "torch":
+            with torch.cuda.stream(stream):
+                dist.all_reduce(st.flag, op=dist.ReduceOp.MAX)
+
+    @property
+    def capturable(self):
+        # torch's all-reduce is not ours to capture; the p2p exchange takes its
+        # epoch from the host per launch, which a replayed graph would freeze
+        return self.world == 1 or self.mode == "nccl"
+
+    def describe(self):
+        if self.world == 1:
+            return "none (1 rank)"
+        return {"nccl": "ma_comm ncclAllReduce(max) of the flag (library NCCL)",
+                "torch": "torch.distributed all_reduce(max) of the flag",
+                "p2p": "fused into K1's last CTA over peer memory (CUDA IPC)"}[self.mode]
+
+    def close(self):
+        if self.comm is not None:
+            self.comm.close()
+        if self.xchg is not None:
+            self.xchg.close()
+
+
 def ours(args, n, rank, world, local_rank):
+    """configs[1] (and [0] / [2]): the state of `n` params per GPU in HBM.
+    A step = K1 over the step's gradients -> cross-rank OR of the flag ->
+    K2 over every sub-group -> device-side LossScaler, on one stream; with
+    --graph the chain is captured once and replayed (one launch per step).
+    configs[2] (--config cfg3) regenerates the gradients every step and plants
+    the seeded inf/NaN plan (outside the timed segments), and checks every
+    rank's decisions and loss scales against the committed plan."""
     import torch
     import torch.distributed as dist
 
     import paper_2505_23254_b200 as mab
+    from paper_2505_23254_b200.shard import FaultPlan
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -279,42 +342,68 @@ def ours(args, n, rank, world, local_rank):
     sub = min(SUBGROUP, n)
     groups = mab.Stepper.subgroups(
         [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub], w[o:o + sub])
-         for o in range(0, n, sub)])
-    stream = torch.cuda.current_stream(dev)
-    flush = None
+         for o in range(0, n, sub)], "bf16", "bf16")
+    stream = torch.cuda.Stream(device=dev)  # non-default: capturable
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    inject = args.config == "cfg3"
+    plan = FaultPlan(n * world, sub, seed=2505) if inject else None
+    flush = flush_read = None
     if n * BYTES_PER_PARAM < 4 * 126e6:  # small configs: flush L2 between steps
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        flush_read = torch.empty(1, dtype=torch.int64, device=dev)
+    xc = Exchange(args.flag_exchange, world, rank)
+    use_graph = args.graph and xc.capturable
 
-    # cross-rank OR of the skip flag: NCCL all-reduce(max) (default), or fused
-    # into K1's last CTA over peer memory (--flag-exchange p2p)
-    xchg = None
-    if world > 1 and args.flag_exchange == "p2p":
-        xchg = mab.api.FlagExchange(world, rank, mab.api.torch_all_gather_bytes())
+    def chain(with_events=None):
+        if with_events:
+            with_events[0].record(stream)
+        st.check(g, stream=stream, xchg=xc.xchg)
+        if with_events:
+            with_events[1].record(stream)
+        xc.after_check(st, stream)
+        if with_events:
+            with_events[2].record(stream)
+        st.apply(groups, stream=stream)
+        st.finish(stream=stream)
+        if with_events:
+            with_events[3].record(stream)
 
-    def allreduce(flag):
-        if world > 1 and xchg is None:
-            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+    graph = st.capture(chain, stream, reserve_steps=1 << 20) if use_graph else None
 
+    def prepare(s):
+        """Outside the timed segments: this step's gradients (+ the cfg3
+        plants) and the L2 flush (small configs: 256 MB written, then read
+        back so the write-back of its dirty lines also completes here)."""
+        with torch.cuda.stream(stream):
+            # the reference's per-step gradients (simulator.cpp:401-405: the
+            # generator over the current working weights, times the current
+            # device-resident loss scale)
+            mab.gen_pseudo_grads(g, w, step=s, base=base, seed=1, d_scale=st.scale_t,
+                                 stream=stream)
+            if inject:
+                for pl in plan.local(s, base, n):
+                    mab.plant_bits(g, pl.index - base, pl.bits, stream=stream)
+            if flush is not None:
+                flush.zero_()
+                torch.sum(flush.view(torch.int64), dim=0, keepdim=True, out=flush_read)
+
+    segmented = True  # the producer (and flush) run between the timed steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    seg = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
 
-    def one_step(rec=None):
-        if flush is not None:
-            flush.zero_()
-        if rec:
-            rec[0].record(stream)
-        st.check(g, xchg=xchg)
-        if rec:
-            rec[1].record(stream)
-        allreduce(st.flag)
-        if rec:
-            rec[2].record(stream)
-        st.apply(groups)
-        st.finish()
-        if rec:
-            rec[3].record(stream)
+    def one_step(s, k=None):
+        prepare(s)
+        if k is not None:
+            seg[k][0].record(stream)
+        if graph is not None:
+            graph.launch(stream)
+        else:
+            chain(ev[k] if k is not None else None)
+        if k is not None:
+            seg[k][1].record(stream)
 
-    for _ in range(args.warmup):
-        one_step()
+    for s in range(args.warmup):
+        one_step(s)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -324,7 +413,7 @@ def ours(args, n, rank, world, local_rank):
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for k in range(args.steps):
-            one_step(ev[k])
+            one_step(args.warmup + k, k)
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -332,13 +421,52 @@ def ours(args, n, rank, world, local_rank):
         torch.cuda.synchronize()
     clocks = clk.summary()
     elapsed_ms = t0.elapsed_time(t1)
-    if flush is not None:
-        # L2 was flushed before every step: time only the steps themselves
-        elapsed_ms = float(sum(e[0].elapsed_time(e[3]) for e in ev))
-    k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
-    k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+    if segmented:
+        # gradients produced (and L2 flushed) between steps: time the steps
+        elapsed_ms = float(sum(e[0].elapsed_time(e[1]) for e in seg))
+        region_ms = t0.elapsed_time(t1)
+    if graph is None:
+        k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+        k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+        kernel_timing = "CUDA events around K1 and K2 on the launching stream, timed region"
+    else:
+        # inside a graph replay the kernels cannot be bracketed: K1 / K2 are
+        # timed over the same number of eager steps right after the region
+        cal = [[torch.cuda.Event(enable_timing=True) for _ in range(4)]
+               for _ in range(args.steps)]
+        for k in range(args.steps):
+            prepare(args.warmup + args.steps + k)
+            chain(cal[k])
+        torch.cuda.synchronize()
+        k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in cal]))
+        k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in cal]))
+        kernel_timing = ("CUDA events around K1 and K2 over as many eager steps right after "
+                         "the graph-timed region")
+    total_steps = args.warmup + args.steps * (2 if graph is not None else 1)
     state = st.state()
-    assert state["steps"] == args.warmup + args.steps and state["last_overflow"] == 0
+    assert state["steps"] == total_steps, state
+    check = None
+    if inject:
+        fx = json.load(open(os.path.join(ROOT, "tests", "golden", "cfg3_plan.json")))
+        if total_steps > fx["steps"]:
+            raise SystemExit(f"cfg3: the committed plan covers {fx['steps']} steps")
+        of, sc = st.history()
+        want_of = fx["overflow"][:total_steps]
+        want_sc = np.array(fx["scale_after_bits"][:total_steps], np.uint32).view(np.float32)
+        ok = (of.astype(int).tolist() == want_of and
+              np.array_equal(sc.view(np.uint32), want_sc.view(np.uint32)))
+        res = torch.tensor([0 if ok else 1], dtype=torch.int32, device=dev)
+        if world > 1:
+            dist.all_reduce(res, op=dist.ReduceOp.MAX)
+        if res.item():
+            raise SystemExit(f"rank {rank}: cfg3 decisions / scales differ from "
+                             "tests/golden/cfg3_plan.json")
+        check = {"plan": "tests/golden/cfg3_plan.json (FaultPlan seed 2505 + the reference's "
+                         "LossScaler)", "steps_checked": total_steps, "skipped": int(of.sum()),
+                 "decisions_match": True, "scales_match": True, "ranks_agree": True,
+                 "planted_this_rank": sum(len(plan.local(s, base, n)) for s in range(total_steps))}
+    else:
+        assert state["last_overflow"] == 0
 
     # max over ranks
     t = torch.tensor([elapsed_ms, k1_ms, k2_ms], dtype=torch.float64, device=dev)
@@ -349,7 +477,7 @@ def ours(args, n, rank, world, local_rank):
 
     # ---- e2e: gradients from pinned host memory through the public API
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not inject:
         # the gradient flat buffer in alignment-free registered host memory
         # (§4.3; torch's pin_memory would round 16.06 GB up to 32 GiB)
         g_host = torch.from_numpy(mab.aligned_host_buffer(n * 2, register=True).view(np.int16))
@@ -358,13 +486,14 @@ def ours(args, n, rank, world, local_rank):
         res_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
 
         def e2e_step():
-            st.check_from_host(g_host, g)
-            if xchg is not None:
-                st.check(None, xchg=xchg)  # exchange-only K1 launch (no elements)
-            allreduce(st.flag)
-            st.apply(groups)
-            st.finish()
-            res_host.copy_(st.state_t[:16], non_blocking=True)  # flag/scale readback
+            st.check_from_host(g_host, g, stream=stream)
+            if xc.xchg is not None:
+                st.check(None, stream=stream, xchg=xc.xchg)  # exchange-only K1 launch
+            xc.after_check(st, stream)
+            st.apply(groups, stream=stream)
+            st.finish(stream=stream)
+            with torch.cuda.stream(stream):
+                res_host.copy_(st.state_t[:16], non_blocking=True)  # flag/scale readback
 
         e2e_step()
         torch.cuda.synchronize()
@@ -386,9 +515,12 @@ def ours(args, n, rank, world, local_rank):
                "h2d_bytes_per_step": n * 2, "d2h_bytes_per_step": 16,
                "ms_per_step": e2e_ms,
                "path": "pinned host bf16 grads -> chunked H2D overlapped with K1 "
-                       "(ma_stepper_check_host_async) -> K2 over HBM-resident state -> "
-                       "D2H of the step's flag/loss-scale"}
+                       "(ma_stepper_check_host_async) -> flag exchange -> K2 over HBM-resident "
+                       "state -> D2H of the step's flag/loss-scale"}
         del g_host
+    if graph is not None:
+        graph.close()
+    xc.close()
 
     if rank != 0:
         return
@@ -408,29 +540,39 @@ def ours(args, n, rank, world, local_rank):
                 break
             except Exception:
                 traffic = None
+    cfg = workload_config(args, n, world)
+    cfg.update(flag_exchange=xc.describe(), graph=graph is not None,
+               gradients="regenerated every step outside the timed segments (the reference's "
+                         "pseudo_gradient over the current weights x the device loss scale)")
+    if flush is not None:
+        cfg["l2"] = ("L2 flushed between steps (256 MB written then read back, outside the "
+                     "timed segments)")
     line = {
         "metric": METRIC,
         "value": n * world / (ms_per_step / 1e3),
         "unit": "params/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step,
+        "region_ms_incl_producer": region_ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (reference generators seeded_weight/pseudo_gradient)",
-        "config": workload_config(args, n, world),
+        "config": cfg,
         "hbm_gbs_per_gpu": alg_bytes / (ms_per_step / 1e3) / 1e9,
-        "roofline": {"bound": "hbm", "kernel": "k2_adam (K2 fused unscale+AdamW+cast)",
+        "roofline": {"bound": "hbm", "kernel": "k2_oneshot (K2 fused unscale+AdamW+cast)",
                      "achieved": k2_gbs, "peak": peak, "unit": "GB/s",
                      "frac": k2_gbs / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                      "bytes_per_param": BYTES_PER_PARAM, "params_per_launch": n,
-                     "k2_ms": k2_ms, "k1_ms": k1_ms,
+                     "k2_ms": k2_ms, "k1_ms": k1_ms, "kernel_timing": kernel_timing,
                      "k1_gbs": 2 * n / (k1_ms / 1e3) / 1e9,
                      "step_frac": alg_bytes / (ms_per_step / 1e3) / 1e9 / peak},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
         "e2e": e2e,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if check is not None:
+        line["cfg3_check"] = check
+    if world == 1 and not args.no_cpu_baseline and not inject:
         threads = os.cpu_count() or 1
         cb = cpu_reference_run(min(args.cpu_sample, n), 3, 1, threads)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -918,17 +1060,50 @@ def ours_swapped_bf16(args, n, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def launch_ranks(args):
+    """`bench.py --gpus N` without a launcher: re-execute under
+    torch.distributed.run with N ranks (one per GPU) on 127.0.0.1 and exit
+    with its status.  Guards: N must not exceed the visible GPUs (our arm;
+    the MA_BENCH_DEVICE test hook puts every rank on one device)."""
+    import socket
+
+    if args.impl == "ours" and "MA_BENCH_DEVICE" not in os.environ:
+        import torch
+
+        have = torch.cuda.device_count()
+        if args.gpus > have:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible",
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        launch_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr, flush=True)
+        sys.exit(2)
+    # the NCCL communicators log their init (incl. "nranks N") unless the
+    # caller chose otherwise
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
     # test hooks for the N>1 path on a single GPU (tests/ only): every rank on
     # MA_BENCH_DEVICE, collectives over MA_BENCH_BACKEND (gloo); default nccl
+    hook = "MA_BENCH_DEVICE" in os.environ
     local_rank = int(os.environ.get("MA_BENCH_DEVICE", local_rank))
     backend = os.environ.get("MA_BENCH_BACKEND", "nccl")
-    n = args.params or {"cfg2": LLAMA3_8B, "cfg1": CFG1, "cfg4": (QWEN25_14B + 7) // 8,
-                        "cfg5": (LLAMA3_70B + 7) // 8}[args.config]
+    n = args.params or {"cfg2": LLAMA3_8B, "cfg1": CFG1, "cfg3": LLAMA3_8B,
+                        "cfg4": (QWEN25_14B + 7) // 8, "cfg5": (LLAMA3_70B + 7) // 8}[args.config]
     if args.impl == "reference":
         reference_arm(args, n, rank, world)
         return
@@ -936,11 +1111,19 @@ def main():
         import torch
         import torch.distributed as dist
 
+        if not hook and world > torch.cuda.device_count():
+            print(f"bench.py: {world} ranks but {torch.cuda.device_count()} CUDA device(s)",
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
         torch.cuda.set_device(local_rank)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
+        if hook and args.flag_exchange == "nccl":
+            # NCCL cannot put two ranks on one GPU: the single-GPU test hook
+            # exchanges the flag through torch.distributed instead
+            args.flag_exchange = "torch"
     try:
         if args.zero_fused:
             ours_zero_fused(args, args.params or 1_000_000_000, rank, world, local_rank)

@@ -12,6 +12,7 @@
 #include "reference_trainer.hpp"
 
 #include <cinttypes>
+#include <array>
 #include <cstdio>
 #include <fstream>
 #include <nlohmann/json.hpp>
@@ -371,6 +372,33 @@ json workload() {
     return {{"cases", cases}};
 }
 
+// BASELINE configs[2] injection plan (paper_2505_23254_b200/shard.py
+// FaultPlan, seed 2505): each step draws k in {0, 1, 3} non-finite plants
+// (plus a max-finite control plant that never triggers), so the global skip
+// decision of step s is k > 0 — independent of the partition size.  The
+// scale sequence is the reference's own LossScaler (optimizer.hpp:19-35)
+// driven by those decisions; bench.py --config cfg3 checks its ranks
+// against this fixture.
+json cfg3_plan() {
+    const std::uint64_t seed = 2505, steps = 1024;
+    LossScaler sc;  // 65536, growth 2000
+    json of = json::array(), scales = json::array();
+    for (std::uint64_t s = 0; s < steps; ++s) {
+        std::uint64_t h = splitmix64(seed ^ splitmix64(s ^ 0xC0FFEEull));
+        h = splitmix64(h);
+        const std::uint64_t k = std::array<std::uint64_t, 3>{0, 1, 3}[h % 3];
+        if (k) {
+            sc.on_overflow();
+        } else {
+            sc.on_clean_step();
+        }
+        of.push_back(k ? 1 : 0);
+        scales.push_back(float_bits(sc.scale));
+    }
+    return {{"seed", seed}, {"steps", steps}, {"init_scale", 65536.0},
+            {"growth_interval", 2000}, {"overflow", of}, {"scale_after_bits", scales}};
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -382,5 +410,6 @@ int main(int argc, char** argv) {
     if (which == "all" || which == "halfprec") write(dir, "halfprec.json", halfprec());
     if (which == "all" || which == "trainer") write(dir, "trainer.json", trainer());
     if (which == "all" || which == "workload") write(dir, "workload.json", workload());
+    if (which == "all" || which == "cfg3") write(dir, "cfg3_plan.json", cfg3_plan());
     return 0;
 }

@@ -48,6 +48,76 @@ def test_reference_arm_line(nproc):
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0
 
 
+def run_plain(args, env=None, timeout=600):
+    """bench.py WITHOUT a launcher (the driver's `python bench.py --gpus N`)."""
+    e = dict(os.environ, **(env or {}))
+    e.pop("WORLD_SIZE", None)
+    return subprocess.run([sys.executable, "bench.py"] + args, cwd=ROOT, env=e,
+                          capture_output=True, text=True, timeout=timeout)
+
+
+def test_gpus_flag_launches_ranks_itself():
+    """`python bench.py --gpus 2` with no torchrun re-executes itself under
+    torch.distributed.run with two ranks; rank 0 alone prints, n_gpus: 2."""
+    p = run_plain(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1",
+                   "--cpu-sample", "1000000"])
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["impl"] == "reference"
+
+
+def test_gpus_beyond_visible_devices_fails_loudly():
+    import torch
+
+    want = torch.cuda.device_count() + 2  # >= 2: the launcher path
+    p = run_plain(["--gpus", str(want), "--steps", "1", "--warmup", "1"])
+    assert p.returncode != 0
+    assert "CUDA device" in p.stderr and not [ln for ln in p.stdout.splitlines()
+                                               if ln.startswith("{")]
+
+
+def test_world_size_mismatch_fails_loudly():
+    e = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--impl", "reference"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=300)
+    assert p.returncode != 0 and "WORLD_SIZE" in p.stderr
+
+
+@pytest.mark.gpu
+def test_gpus_flag_two_ranks_on_one_gpu_without_torchrun():
+    p = run_plain(["--gpus", "2", "--params", "100000000", "--steps", "3", "--warmup", "3",
+                   "--e2e-steps", "0"], env={"MA_BENCH_BACKEND": "gloo", "MA_BENCH_DEVICE": "0"})
+    assert p.returncode == 0, p.stderr[-3000:]
+    j = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][0])
+    assert j["n_gpus"] == 2 and j["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nproc", [1, 2])
+def test_cfg3_injection_line(nproc):
+    """configs[2]: the seeded inf/NaN plan over nproc ranks; bench.py itself
+    asserts every rank's decisions and scales against the committed plan."""
+    env = {"MA_BENCH_BACKEND": "gloo", "MA_BENCH_DEVICE": "0"} if nproc > 1 else None
+    j = run(["--config", "cfg3", "--params", "100000000", "--steps", "12", "--warmup", "3",
+             "--no-cpu-baseline"], nproc=nproc, env=env)
+    c = j["cfg3_check"]
+    assert c["decisions_match"] and c["scales_match"] and c["steps_checked"] == 15
+    assert 0 < c["skipped"] < 15 and j["n_gpus"] == nproc
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg3"])
+def test_graph_replay_line(cfg):
+    j = run(["--config", cfg, "--graph", "--params", "67108864", "--steps", "8", "--warmup", "3",
+             "--no-cpu-baseline", "--e2e-steps", "0"])
+    assert j["config"]["graph"] is True and j["value"] > 0
+    assert j["roofline"]["k2_ms"] > 0
+    if cfg == "cfg3":
+        assert j["cfg3_check"]["steps_checked"] == 3 + 8 + 8  # + the eager K1/K2 calibration
+
+
 @pytest.mark.gpu
 def test_our_arm_line_n1():
     j = run(["--params", "200000000", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",

@@ -191,3 +191,23 @@ def test_ranks_on_b200_peer_exchange_fused_in_k1(world):
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(free_port(), d, True, True, world), nprocs=world, join=True)
         _check_against_single_process(d, world)
+
+
+def test_cfg3_plan_fixture_pins_decisions_and_scales(golden):
+    """tests/golden/cfg3_plan.json (oracle/_ref golden_gen: the plan's draws
+    + the reference's own LossScaler) is what bench.py --config cfg3 checks
+    its ranks against: shard.FaultPlan's decision of every step equals it
+    for any partition size, and the oracle's scaler reproduces its scales."""
+    fx = golden("cfg3_plan.json")
+    for n_total, sub in ((1_000_003, 100_000), (8_030_261_248 * 8, 100_000_000), (77, 10)):
+        plan = FaultPlan(n_total, sub, seed=fx["seed"])
+        assert [int(plan.expected_skip(s)) for s in range(fx["steps"])] == fx["overflow"]
+    sc = ora.Scaler(fx["init_scale"], fx["growth_interval"], 0)
+    got = []
+    for of in fx["overflow"]:
+        if of:
+            ora.lib().ora_scaler_on_overflow(ora.C.byref(sc))
+        else:
+            ora.lib().ora_scaler_on_clean_step(ora.C.byref(sc))
+        got.append(int(np.float32(sc.scale).view(np.uint32)))
+    assert got == fx["scale_after_bits"]
