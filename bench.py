@@ -585,11 +585,53 @@ def ours(args, n, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def host_grads_e2e(args, st, g, n, world, rank, dev, stream, step_rest):
+    """The same step end to end through the public API: this step's bf16
+    gradients come from registered (pinned) host memory —
+    ma_stepper_check_host_async copies them in chunks with K1 overlapped —
+    then `step_rest()` (exchange, update, scaler) and a D2H of the step's
+    flag / loss scale.  Returns (ms per step, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_23254_b200 as mab
+
+    g_host = torch.from_numpy(mab.aligned_host_buffer(n * 2, register=True).view(np.int16))
+    g_host.copy_(g.view(torch.int16), non_blocking=False)
+    g_host = g_host.view(torch.bfloat16)
+    res_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
+
+    def e2e_step():
+        st.check_from_host(g_host, g, stream=stream)
+        step_rest()
+        with torch.cuda.stream(stream):
+            res_host.copy_(st.state_t[:16], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b) / args.e2e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    del g_host
+    return float(ms.item())
+
+
 def ours_streamed(args, n, rank, world, local_rank):
     """configs[3]: Qwen2.5-14B-shaped state sharded 8 ways (1.85 B params per
-    GPU); fp32 p/m/v live in the registered host pool, grads and working
-    weights in HBM; every 100 M sub-group is staged H2D -> K2 -> D2H through
-    `--slots` device slots.  Bound: the host link, 24 B/param (12 in, 12 out)."""
+    GPU); fp32 p/m/v live in the drop-in memascend::Pool (adaptive,
+    alignment-free, cudaHostRegister'd: include/memascend/state_pool.h, one
+    checked-out slot per sub-group tensor), grads and working weights in HBM;
+    every 100 M sub-group is staged H2D -> K2 -> D2H through `--slots`
+    device slots.  Bound: the host link, 24 B/param (12 in, 12 out)."""
     import torch
     import torch.distributed as dist
 
@@ -597,63 +639,73 @@ def ours_streamed(args, n, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    # the pool: alignment-free registered host memory (§4.3: no
-    # power-of-two rounding, which torch's pinned caching allocator applies)
-    host = []
-    for _ in range(3):
-        buf = mab.aligned_host_buffer(n * 4, register=True)
-        host.append(torch.from_numpy(buf.view(np.float32)))
-    p, m, v = host
-    m.zero_()
-    v.zero_()
-    pinned_exact = 3 * ((n * 4 + 4095) // 4096 * 4096)
-    pinned_pow2 = 3 * (1 << (n * 4 - 1).bit_length())
+    sub = min(SUBGROUP, n)
+    t_init = time.perf_counter()
+    pool = mab.StatePool(n, sub)
+    pstats = pool.stats()
+    pinned_pow2 = 3 * sum(1 << (min(sub, n - o) * 4 - 1).bit_length() for o in range(0, n, sub))
     g = torch.empty(n, dtype=torch.bfloat16, device=dev)
     w = torch.empty(n, dtype=torch.bfloat16, device=dev)
     base = rank * n
-    chunk = 1 << 28
-    tmp = torch.empty(min(n, chunk), dtype=torch.float32, device=dev)
-    for o in range(0, n, chunk):
-        k = min(chunk, n - o)
-        mab.gen_seeded_weights(tmp[:k], w[o:o + k], base=base + o, seed=1)
-        p[o:o + k].copy_(tmp[:k])
+    tmp = torch.empty(sub, dtype=torch.float32, device=dev)
+    groups = []
+    for k, o in enumerate(range(0, n, sub)):
+        ln = min(sub, n - o)
+        (ph, _), (mh, _), (vh, _) = (pool.tensor(k, i) for i in range(3))
+        mab.gen_seeded_weights(tmp[:ln], w[o:o + ln], base=base + o, seed=1)
+        ph.copy_(tmp[:ln])  # m and v slots are zero (the allocator's fill)
+        groups.append((ph, mh, vh, g[o:o + ln], w[o:o + ln]))
     del tmp
-    mab.gen_pseudo_grads(g, w, step=0, base=base, seed=1, scale=65536.0)
+    t_init = time.perf_counter() - t_init
     st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "bf16", device=dev)
-    sub = min(SUBGROUP, n)
-    groups = mab.Stepper.subgroups(
-        [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub], w[o:o + sub])
-         for o in range(0, n, sub)])
+    arr = mab.Stepper.subgroups(groups, "bf16", "bf16")
     slot = args.slot_params
     staging = torch.empty(3 * args.slots * slot, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    xc = Exchange(args.flag_exchange, world, rank)
 
-    def one_step():
-        st.check(g)
-        if world > 1:
-            dist.all_reduce(st.flag, op=dist.ReduceOp.MAX)
-        st.apply_streamed(groups, staging, slot, args.slots)
-        st.finish()
+    def rest():
+        xc.after_check(st, stream)
+        st.apply_streamed(arr, staging, slot, args.slots, stream=stream)
+        st.finish(stream=stream)
 
-    for _ in range(args.warmup):
-        one_step()
+    seg = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+
+    def one_step(s, k=None):
+        mab.gen_pseudo_grads(g, w, step=s, base=base, seed=1, d_scale=st.scale_t, stream=stream)
+        if k is not None:
+            seg[k][0].record(stream)
+        st.check(g, stream=stream, xchg=xc.xchg)
+        rest()
+        if k is not None:
+            seg[k][1].record(stream)
+
+    for s in range(args.warmup):
+        one_step(s)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     with ClockSampler(local_rank) as clk:
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.steps):
-            one_step()
-        b.record(stream)
+        for k in range(args.steps):
+            one_step(args.warmup + k, k)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
+    ms = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in seg) / args.steps],
+                      dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e_ms = host_grads_e2e(args, st, g, n, world, rank, dev, stream, rest)
+        e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "params/s",
+               "h2d_bytes_per_step": n * 2 + 12 * n, "d2h_bytes_per_step": 12 * n + 16,
+               "ms_per_step": e2e_ms,
+               "path": "pinned host bf16 grads -> chunked H2D overlapped with K1 -> flag "
+                       "exchange -> p/m/v slots of the registered memascend::Pool streamed "
+                       "H2D -> K2 -> D2H (ma_stepper_apply_streamed) -> D2H of flag/scale"}
 
     # measured host-link ceiling: concurrent pinned H2D + D2H of 1 GiB each
     hb = torch.empty(1 << 28, dtype=torch.float32, pin_memory=True)
@@ -678,7 +730,9 @@ def ours_streamed(args, n, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
         best = max(best, 2 * (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    xc.close()
     if rank != 0:
+        pool.close()
         return
     link = 24 * n / (ms / 1e3) / 1e9
     line = {
@@ -686,15 +740,23 @@ def ours_streamed(args, n, rank, world, local_rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generators seeded_weight/pseudo_gradient)",
-        "config": dict(workload_config(args, n, world), slots=args.slots, slot_params=slot),
-        "pinned_host_bytes": {"alignment_free": pinned_exact,
+        "config": dict(workload_config(args, n, world), slots=args.slots, slot_params=slot,
+                       flag_exchange=xc.describe(),
+                       state_pool="memascend::Pool (adaptive, alignment-free, registered), "
+                                  f"{pstats['classes']} slot classes, every master/m/v "
+                                  "sub-group tensor a checked-out slot"),
+        "pinned_host_bytes": {"pool_backing": pstats["backing_bytes"],
+                              "pool_payload": pstats["capacity_bytes"],
                               "torch_pin_memory_would_take": pinned_pow2},
-        "host_link": {"bound": "host-link", "achieved": link, "unit": "GB/s",
-                      "peak": best, "frac": link / best, "bytes_per_param": 24,
-                      "peak_source": "measured concurrent pinned H2D+D2H, 1 GiB each"},
+        "roofline": {"bound": "host-link", "achieved": link, "unit": "GB/s", "peak": best,
+                     "frac": link / best, "traffic": None, "bytes_per_param": 24,
+                     "peak_source": "measured concurrent pinned H2D+D2H, 1 GiB each"},
+        "init_seconds": t_init,
         "gpu_launches": (1 + ((n + slot - 1) // slot) + 1) * args.steps,
         "clocks": clk.summary(),
+        "e2e": e2e,
     }
+    pool.close()
     print(json.dumps(line), flush=True)
 
 
@@ -848,6 +910,16 @@ def storage_report(args, io_bytes, ms, bytes_per_swapped_param):
                            "2 rewritten while 2 are read"}
 
 
+def storage_roofline(sr):
+    """The swapped step's roofline: the swap device (bytes moved per step
+    from the store's own request counters) against its measured mixed
+    read/write rate through the same engine and settings."""
+    return {"bound": "swap-device", "achieved": sr["achieved"], "peak": sr["peak"],
+            "unit": "GB/s", "frac": sr["frac"], "traffic": sr["bytes_per_step"],
+            "bytes_per_swapped_param": sr["bytes_per_swapped_param"],
+            "peak_source": sr["peak_source"]}
+
+
 def ours_swapped(args, n, rank, world, local_rank):
     """configs[4]: Llama-3-70B-shaped state sharded 8 ways (8.82 B params per
     GPU).  fp32 master/m/v of `--swap-gb` worth of 100 M sub-groups live in
@@ -921,20 +993,36 @@ def ours_swapped(args, n, rank, world, local_rank):
     st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "bf16", device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    xc = Exchange(args.flag_exchange, world, rank)
+
+    def rest():
+        xc.after_check(st, stream)
+        st.apply_swapped(store, groups, hstage, hslots, dstage, args.slots, sub, stream=stream)
+        st.finish(stream=stream)
+
     def one_step():
-        st.check(g)
-        if world > 1:
-            dist.all_reduce(st.flag, op=dist.ReduceOp.MAX)
-        st.apply_swapped(store, groups, hstage, hslots, dstage, args.slots, sub)
-        st.finish()
+        st.check(g, stream=stream, xchg=xc.xchg)
+        rest()
 
     try:
         ms, io_bytes, clocks, backend = timed_swapped_steps(args, one_step, store, stream, dev,
                                                             world, local_rank)
+        e2e = None
+        if args.e2e_steps > 0:
+            e2e_ms = host_grads_e2e(args, st, g, n, world, rank, dev, stream, rest)
+            n_sw_ = n - n_host
+            e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "params/s",
+                   "h2d_bytes_per_step": n * 2 + 12 * n, "d2h_bytes_per_step": 12 * n + 16,
+                   "storage_bytes_per_step": 24 * n_sw_, "ms_per_step": e2e_ms,
+                   "path": "pinned host bf16 grads -> chunked H2D overlapped with K1 -> flag "
+                           "exchange -> swapped groups read from the O_DIRECT store into "
+                           "registered host slots, every group H2D -> K2 -> D2H, swapped groups "
+                           "written back (ma_stepper_apply_swapped) -> D2H of flag/scale"}
         if store:
             store.close()
     finally:
         shutil.rmtree(sdir, ignore_errors=True)
+        xc.close()
     if rank != 0:
         return
     n_sw = n - n_host
@@ -953,7 +1041,9 @@ def ours_swapped(args, n, rank, world, local_rank):
         "init_seconds": t_init,
         "gpu_launches": (1 + G + 1) * args.steps,
         "clocks": clocks,
+        "e2e": e2e,
     }
+    line["roofline"] = storage_roofline(line["storage"])
     if world == 1 and not args.no_cpu_baseline:
         res = reference_swapped_run(args, 2, 1, os.cpu_count() or 1)
         line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -1022,20 +1112,36 @@ def ours_swapped_bf16(args, n, rank, world, local_rank):
     dstage = torch.empty(2 * args.slots * sub, dtype=torch.int16, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    xc = Exchange(args.flag_exchange, world, rank)
+
+    def rest():
+        xc.after_check(st, stream)
+        st.apply_swapped_bf16(store, groups, hstage, hslots, dstage, args.slots, sub,
+                              stream=stream)
+        st.finish(stream=stream)
+
     def one_step():
-        st.check(g)
-        if world > 1:
-            dist.all_reduce(st.flag, op=dist.ReduceOp.MAX)
-        st.apply_swapped_bf16(store, groups, hstage, hslots, dstage, args.slots, sub)
-        st.finish()
+        st.check(g, stream=stream, xchg=xc.xchg)
+        rest()
 
     try:
         ms, io_bytes, clocks, backend = timed_swapped_steps(args, one_step, store, stream, dev,
                                                             world, local_rank)
+        e2e = None
+        if args.e2e_steps > 0:
+            e2e_ms = host_grads_e2e(args, st, g, n, world, rank, dev, stream, rest)
+            e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "params/s",
+                   "h2d_bytes_per_step": n * 2 + 4 * n, "d2h_bytes_per_step": 4 * n + 16,
+                   "ms_per_step": e2e_ms,
+                   "path": "pinned host bf16 grads -> chunked H2D overlapped with K1 -> flag "
+                           "exchange -> bf16 m/v streamed from the store / DRAM tier, K3 on "
+                           "HBM-resident bf16 weights (ma_stepper_apply_swapped_bf16) -> D2H "
+                           "of flag/scale"}
         if store:
             store.close()
     finally:
         shutil.rmtree(sdir, ignore_errors=True)
+        xc.close()
     if rank != 0:
         return
     line = {
@@ -1056,7 +1162,9 @@ def ours_swapped_bf16(args, n, rank, world, local_rank):
         "init_seconds": t_init,
         "gpu_launches": (1 + G + 1) * args.steps,
         "clocks": clocks,
+        "e2e": e2e,
     }
+    line["roofline"] = storage_roofline(line["storage"])
     print(json.dumps(line), flush=True)
 
 

@@ -11,6 +11,7 @@ from .api import (  # noqa: F401
     DevicePool,
     DirectIoEngine,
     NcclComm,
+    StatePool,
     StepGraph,
     WeightPrefetcher,
     aligned_host_buffer,

@@ -775,6 +775,69 @@ class SwapOp:
             self._h = None
 
 
+class StatePool:
+    """configs[3]'s host-resident optimizer state in the drop-in memascend::Pool
+    (include/memascend/state_pool.h over pool.hpp, libmemascend.so): an
+    adaptive, alignment-free, cudaHostRegister'd pool; every sub-group's
+    master / m / v is a checked-out slot, exposed as torch tensors over the
+    slot's host span (registered memory: ma_stepper_apply_streamed DMAs from
+    and to it directly)."""
+
+    _lib = None
+
+    @classmethod
+    def lib(cls):
+        if cls._lib is None:
+            import os
+
+            path = os.path.join(os.path.dirname(capi.LIB_PATH), "libmemascend.so")
+            L = C.CDLL(path)
+            L.memascend_last_error.restype = C.c_char_p
+            L.memascend_state_pool_create.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_void_p)]
+            L.memascend_state_pool_tensor.argtypes = [C.c_void_p, C.c_uint64, C.c_int,
+                                                      C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                                      C.POINTER(C.c_uint64)]
+            L.memascend_state_pool_stats.argtypes = [C.c_void_p] + [C.POINTER(C.c_uint64)] * 5
+            L.memascend_state_pool_destroy.argtypes = [C.c_void_p]
+            cls._lib = L
+        return cls._lib
+
+    def _check(self, st):
+        if st != 0:
+            raise MemAscendError(st, self.lib().memascend_last_error().decode(errors="replace"))
+
+    def __init__(self, n_params: int, subgroup: int):
+        h = C.c_void_p()
+        self._check(self.lib().memascend_state_pool_create(n_params, subgroup, C.byref(h)))
+        self._h = h
+        self.groups = (n_params + subgroup - 1) // subgroup
+
+    def tensor(self, group: int, which: int):
+        """(host float32 tensor over the slot, device pointer) of master (0), m (1) or v (2)."""
+        host, dev, n = C.c_void_p(), C.c_void_p(), C.c_uint64()
+        self._check(self.lib().memascend_state_pool_tensor(self._h, group, which, C.byref(host),
+                                                           C.byref(dev), C.byref(n)))
+        arr = np.ctypeslib.as_array((C.c_float * n.value).from_address(host.value))
+        return torch.from_numpy(arr), dev.value
+
+    def stats(self) -> dict:
+        v = [C.c_uint64() for _ in range(5)]
+        self._check(self.lib().memascend_state_pool_stats(self._h, *[C.byref(x) for x in v]))
+        return dict(zip(("capacity_bytes", "backing_bytes", "live_bytes", "checkouts",
+                         "classes"), (x.value for x in v)))
+
+    def close(self):
+        if self._h:
+            self.lib().memascend_state_pool_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DevicePool:
     """Exact-fit slot pool in HBM (ma_dpool): classes = [(payload_bytes,
     slot_count), ...], planned like pool.cpp:22-68 (4096-rounded strides)."""

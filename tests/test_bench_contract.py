@@ -162,7 +162,22 @@ def test_cfg5_line(precision, tmp_path):
     swapped, the storage and host-link objects present."""
     j = run(["--config", "cfg5", "--precision", precision, "--params", "300000000",
              "--swap-gb", "1.3", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
-             "--swap-dir", str(tmp_path)])
+             "--e2e-steps", "1", "--swap-dir", str(tmp_path)])
+    assert j["roofline"]["bound"] == "swap-device" and j["roofline"]["frac"] > 0
+    assert j["e2e"]["value"] > 0 and j["e2e"]["d2h_bytes_per_step"] > 0
     assert j["value"] > 0 and j["config"]["swapped_groups"] >= 1
     assert j["storage"]["bytes_per_step"] > 0 and 0 < j["storage"]["frac"] < 5
     assert j["storage"]["bytes_per_swapped_param"] == (24 if precision == "mixed" else 8)
+
+
+@pytest.mark.gpu
+def test_cfg4_line_pool_roofline_e2e():
+    """configs[3] at a small size: p/m/v in the drop-in memascend::Pool
+    (registered, adaptive), the host-link roofline and the e2e object."""
+    j = run(["--config", "cfg4", "--params", "250000000", "--slot-params", "16777216",
+             "--steps", "3", "--warmup", "3", "--e2e-steps", "1"])
+    r = j["roofline"]
+    assert r["bound"] == "host-link" and 0 < r["frac"] < 1.3 and r["bytes_per_param"] == 24
+    assert "memascend::Pool" in j["config"]["state_pool"]
+    assert j["pinned_host_bytes"]["pool_payload"] == 12 * 250000000
+    assert j["e2e"]["h2d_bytes_per_step"] == 14 * 250000000 and j["e2e"]["value"] > 0
