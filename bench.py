@@ -425,23 +425,30 @@ def ours(args, n, rank, world, local_rank):
         # gradients produced (and L2 flushed) between steps: time the steps
         elapsed_ms = float(sum(e[0].elapsed_time(e[1]) for e in seg))
         region_ms = t0.elapsed_time(t1)
+    first = args.warmup
     if graph is None:
-        k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
-        k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+        timed_ev = ev
         kernel_timing = "CUDA events around K1 and K2 on the launching stream, timed region"
     else:
         # inside a graph replay the kernels cannot be bracketed: K1 / K2 are
         # timed over the same number of eager steps right after the region
-        cal = [[torch.cuda.Event(enable_timing=True) for _ in range(4)]
-               for _ in range(args.steps)]
+        timed_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                    for _ in range(args.steps)]
         for k in range(args.steps):
             prepare(args.warmup + args.steps + k)
-            chain(cal[k])
+            chain(timed_ev[k])
         torch.cuda.synchronize()
-        k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in cal]))
-        k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in cal]))
+        first = args.warmup + args.steps
         kernel_timing = ("CUDA events around K1 and K2 over as many eager steps right after "
                          "the graph-timed region")
+    # K2 of a skipped step returns at once: average K2 over the applied steps
+    applied = list(range(args.steps))
+    if inject:
+        of_all, _ = st.history()
+        applied = [k for k in range(args.steps) if not of_all[first + k]] or applied
+        kernel_timing += "; K2 averaged over the steps that applied an update"
+    k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in timed_ev]))
+    k2_ms = float(np.mean([timed_ev[k][2].elapsed_time(timed_ev[k][3]) for k in applied]))
     total_steps = args.warmup + args.steps * (2 if graph is not None else 1)
     state = st.state()
     assert state["steps"] == total_steps, state
@@ -480,7 +487,8 @@ def ours(args, n, rank, world, local_rank):
     if args.e2e_steps > 0 and not inject:
         # the gradient flat buffer in alignment-free registered host memory
         # (§4.3; torch's pin_memory would round 16.06 GB up to 32 GiB)
-        g_host = torch.from_numpy(mab.aligned_host_buffer(n * 2, register=True).view(np.int16))
+        g_buf = mab.aligned_host_buffer(n * 2, register=True)
+        g_host = torch.from_numpy(g_buf.view(np.int16))
         g_host.copy_(g.view(torch.int16), non_blocking=False)
         g_host = g_host.view(torch.bfloat16)
         res_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
@@ -518,6 +526,7 @@ def ours(args, n, rank, world, local_rank):
                        "(ma_stepper_check_host_async) -> flag exchange -> K2 over HBM-resident "
                        "state -> D2H of the step's flag/loss-scale"}
         del g_host
+        mab.host_unregister(g_buf)
     if graph is not None:
         graph.close()
     xc.close()
@@ -596,7 +605,8 @@ def host_grads_e2e(args, st, g, n, world, rank, dev, stream, step_rest):
 
     import paper_2505_23254_b200 as mab
 
-    g_host = torch.from_numpy(mab.aligned_host_buffer(n * 2, register=True).view(np.int16))
+    g_buf = mab.aligned_host_buffer(n * 2, register=True)
+    g_host = torch.from_numpy(g_buf.view(np.int16))
     g_host.copy_(g.view(torch.int16), non_blocking=False)
     g_host = g_host.view(torch.bfloat16)
     res_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
@@ -622,6 +632,7 @@ def host_grads_e2e(args, st, g, n, world, rank, dev, stream, step_rest):
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     del g_host
+    mab.host_unregister(g_buf)  # before the pages go back to the allocator
     return float(ms.item())
 
 

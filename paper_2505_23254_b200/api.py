@@ -918,14 +918,29 @@ def uring_available() -> bool:
     return bool(capi.lib().ma_swap_uring_available())
 
 
+_REGISTERED: set = set()  # base addresses registered through host_register
+
+
+def _unregister_at(ptr: int) -> None:
+    if ptr in _REGISTERED:
+        _REGISTERED.discard(ptr)
+        capi.lib().ma_host_unregister(C.c_void_p(ptr))
+
+
 def aligned_host_buffer(nbytes: int, register: bool = False) -> np.ndarray:
     """A 4096-aligned uint8 host array (the swap store's O_DIRECT buffers),
-    optionally registered for DMA (PinnedAllocator's registered state)."""
+    optionally registered for DMA (PinnedAllocator's registered state).  A
+    registered buffer is unregistered automatically when its memory is
+    released (a finalizer on the owning allocation, run before numpy frees
+    it), so freed pages never stay registered behind the allocator's back."""
+    import weakref
+
     raw = np.empty(nbytes + 4096, np.uint8)
     off = (-raw.ctypes.data) % 4096
     buf = raw[off:off + nbytes]
     if register:
         host_register(buf)
+        weakref.finalize(raw, _unregister_at, buf.ctypes.data)
     return buf
 
 
@@ -954,10 +969,12 @@ def host_register(array) -> None:
     """PinnedAllocator's "registered" state, made real (pinned.cpp:122-124)."""
     ptr, nbytes = _raw(array)
     check(capi.lib().ma_host_register(ptr, nbytes))
+    _REGISTERED.add(ptr)
 
 
 def host_unregister(array) -> None:
     ptr, _ = _raw(array)
+    _REGISTERED.discard(ptr)
     check(capi.lib().ma_host_unregister(ptr))
 
 

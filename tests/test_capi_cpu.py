@@ -113,3 +113,43 @@ def test_every_public_header_compiles_on_its_own(tmp_path):
     p = subprocess.run(["gcc", "-std=c11", "-fsyntax-only", "-I", inc, str(src)],
                        capture_output=True, text=True)
     assert p.returncode == 0, p.stderr[-2000:]
+
+
+def test_nccl_entry_points_without_a_gpu(so_path):
+    """The library resolves libnccl.so.2 at run time: the unique id works on
+    any host, a communicator needs a device (MA_ERR_NCCL here, no crash),
+    bad arguments are rejected before NCCL is touched."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2505_23254_b200 import capi
+
+    L = capi.lib()
+    uid = (C.c_ubyte * capi.NCCL_ID_BYTES)()
+    assert L.ma_comm_unique_id(uid) == 0 and any(bytes(uid))
+    h = C.c_void_p()
+    assert L.ma_comm_create(uid, 2, 5, C.byref(h)) == 1  # rank >= world
+    if not torch.cuda.is_available():
+        assert L.ma_comm_create(uid, 1, 0, C.byref(h)) == 102
+        assert b"nccl" in L.ma_last_error().lower()
+
+
+def test_state_pool_shim_plans_the_drop_in_pool():
+    """include/memascend/state_pool.h over memascend::Pool (CPU part): the
+    adaptive plan of a 1000-param / 300-param-sub-group state has one exact
+    class per distinct size, 4096-byte slot strides and every tensor checked
+    out; the device view needs a registered backing (a GPU)."""
+    import torch
+
+    import paper_2505_23254_b200 as mab
+
+    sp = mab.StatePool(1000, 300)
+    st = sp.stats()
+    assert st == {"capacity_bytes": 12000, "backing_bytes": 12 * 4096, "live_bytes": 12000,
+                  "checkouts": 12, "classes": 2}
+    if not torch.cuda.is_available():
+        with pytest.raises(mab.MemAscendError) as e:
+            sp.tensor(0, 0)
+        assert e.value.code == "capability"
+    sp.close()

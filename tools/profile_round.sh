@@ -4,7 +4,7 @@
 #   + one `ncu --set full` capture per hot kernel.
 # Summarise afterwards with tools/ncu_summary.py (see profiles/README.md).
 set -u
-TAG=${1:-r1}
+TAG=${1:-r2}
 mkdir -p gpurun_out
 NCU="ncu --clock-control none"
 timeout 900 $NCU --metrics gpu__time_duration.sum --csv --log-file gpurun_out/${TAG}_launches_bench_default.csv \
@@ -17,9 +17,15 @@ echo "k2 rc=$?"
 timeout 400 $FULL -k regex:k1_oneshot --launch-skip 3 -o gpurun_out/${TAG}_k1 \
     python bench.py --params 1000000000 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
 echo "k1 rc=$?"
-timeout 400 $FULL -k regex:k3_adam --launch-skip 3 -o gpurun_out/${TAG}_k3 \
-    python tools/bench_k4.py --n 268435456 --reps 1 > /dev/null 2>&1
+MA_K3_VARIANT=0 timeout 400 $FULL -k regex:k3_v2 --launch-skip 3 -o gpurun_out/${TAG}_k3 \
+    python tools/bench_k3.py --child --reps 2 > /dev/null 2>&1
 echo "k3 rc=$?"
+timeout 400 $FULL -k regex:k4_reduce_check --launch-skip 3 -o gpurun_out/${TAG}_k4_1src \
+    python tools/bench_k4.py --n 268435456 --reps 1 > /dev/null 2>&1
+echo "k4 1-src rc=$?"
 timeout 400 $FULL -k regex:k4_reduce_check --launch-skip 12 -o gpurun_out/${TAG}_k4 \
     python tools/bench_k4.py --n 134217728 --reps 1 > /dev/null 2>&1
 echo "k4 rc=$?"
+timeout 400 $FULL -k regex:k_ingest --launch-skip 7 -o gpurun_out/${TAG}_ingest_bf16 \
+    python tools/bench_k4.py --n 268435456 --reps 1 > /dev/null 2>&1
+echo "ingest rc=$?"
