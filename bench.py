@@ -536,7 +536,11 @@ def ours(args, n, rank, world, local_rank):
     peak, peak_kind = peaks()
     alg_bytes = BYTES_PER_PARAM * n
     k2_gbs = alg_bytes / (k2_ms / 1e3) / 1e9
-    launches_per_step = 1 + (len(groups) + 95) // 96 + 1
+    # K1 + K2 launches (96 sub-groups per launch) + finish, plus the producer
+    # (k_gen_grads) and cfg3's k_plant launches between the timed segments
+    launches_per_step = 1 + (len(groups) + 95) // 96 + 1 + 1
+    plants = (sum(len(plan.local(args.warmup + k, base, n)) for k in range(args.steps))
+              if inject else 0)
     # DRAM bytes per launch of K2 = ncu's dram__bytes_{read,write}.sum per param
     # (one `ncu --set full` capture, profiles/*_ncu_summary.json) x params/launch
     traffic = None
@@ -575,7 +579,7 @@ def ours(args, n, rank, world, local_rank):
                      "k2_ms": k2_ms, "k1_ms": k1_ms, "kernel_timing": kernel_timing,
                      "k1_gbs": 2 * n / (k1_ms / 1e3) / 1e9,
                      "step_frac": alg_bytes / (ms_per_step / 1e3) / 1e9 / peak},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches_per_step * args.steps + plants,
         "clocks": clocks,
         "e2e": e2e,
     }
@@ -763,7 +767,7 @@ def ours_streamed(args, n, rank, world, local_rank):
                      "frac": link / best, "traffic": None, "bytes_per_param": 24,
                      "peak_source": "measured concurrent pinned H2D+D2H, 1 GiB each"},
         "init_seconds": t_init,
-        "gpu_launches": (1 + ((n + slot - 1) // slot) + 1) * args.steps,
+        "gpu_launches": (1 + ((n + slot - 1) // slot) + 1 + 1) * args.steps,  # + producer
         "clocks": clk.summary(),
         "e2e": e2e,
     }

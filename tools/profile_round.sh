@@ -29,3 +29,12 @@ echo "k4 rc=$?"
 timeout 400 $FULL -k regex:k_ingest --launch-skip 7 -o gpurun_out/${TAG}_ingest_bf16 \
     python tools/bench_k4.py --n 268435456 --reps 1 > /dev/null 2>&1
 echo "ingest rc=$?"
+# summaries on the box (the .ncu-rep files are ~10-20 MB each; gpurun
+# copies back at most 64 MiB): keep K2's and K3's reports, drop the rest
+python tools/ncu_summary.py ${TAG} gpurun_out/${TAG}_k2.ncu-rep:268435456:28 \
+    gpurun_out/${TAG}_k1.ncu-rep:1000000000:2 gpurun_out/${TAG}_k3.ncu-rep:268435456:14 \
+    gpurun_out/${TAG}_k4_1src.ncu-rep:268435456:4 gpurun_out/${TAG}_k4.ncu-rep:134217728:18 \
+    gpurun_out/${TAG}_ingest_bf16.ncu-rep:268435456:4 && cp profiles/${TAG}_ncu_summary.json gpurun_out/
+rm -f gpurun_out/${TAG}_k1.ncu-rep gpurun_out/${TAG}_k4_1src.ncu-rep gpurun_out/${TAG}_k4.ncu-rep \
+    gpurun_out/${TAG}_ingest_bf16.ncu-rep
+du -sh gpurun_out
