@@ -292,9 +292,9 @@ class Exchange:
 
     @property
     def capturable(self):
-        # torch's all-reduce is not ours to capture; the p2p exchange takes its
-        # epoch from the host per launch, which a replayed graph would freeze
-        return self.world == 1 or self.mode == "nccl"
+        # torch's all-reduce is not ours to capture (the library's NCCL call
+        # and the fused p2p exchange, whose epoch lives on the device, are)
+        return not (self.world > 1 and self.mode == "torch")
 
     def describe(self):
         if self.world == 1:

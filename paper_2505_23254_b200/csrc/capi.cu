@@ -180,7 +180,7 @@ Scratch& scratch() {
 // ------------------------------------------------------------ K1 launch
 void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* first,
                uint64_t index_base, bool early_exit, cudaStream_t st,
-               const ma::XchgDev* xchg = nullptr, unsigned long long epoch = 0) {
+               const ma::XchgDev* xchg = nullptr) {
     if (n == 0 && !xchg) return;  // an empty rank still takes part in the exchange
     const DeviceInfo d = device_info();
     const uint32_t es = static_cast<uint32_t>(elem_bytes(dt));
@@ -188,7 +188,6 @@ void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* f
     if (addr % es) fail(MA_ERR_ALIGNMENT, "gradient buffer is not element-aligned");
     ma::K1Args a{};
     a.xchg = xchg;
-    a.epoch = epoch;
     a.raw = data;
     a.n = n;
     a.head = std::min<uint64_t>(((16 - (addr & 15)) & 15) / es, n);
@@ -371,8 +370,11 @@ void launch_k3(const ma_subgroup* groups, uint32_t count, int gdt, const ma::Ada
         }
         if (tab.count == 0) continue;
         tab.total_tiles = tiles;
-        const uint64_t grid = oneshot_grid(tab, kVec, scalar_elems, cap);
-        ma::launch_k3(gdt, variant, tab, a, static_cast<unsigned>(grid), st);
+        // one CTA per TPC tiles (kernels.cu k3_v2), then the trailing CTAs
+        const uint64_t tpc = static_cast<uint64_t>(ma::k3_tiles_per_cta(gdt, variant));
+        const uint64_t grid = oneshot_grid(tab, kVec, scalar_elems, cap) - tab.total_tiles +
+                              (tab.total_tiles + tpc - 1) / tpc;
+        ma::launch_k3(gdt, variant, tab, a, static_cast<unsigned>(std::max<uint64_t>(grid, 1)), st);
         CK(cudaGetLastError());
     }
 }
@@ -785,10 +787,9 @@ struct ma_xchg {
     int world = 1;
     int rank = 0;
     unsigned long long* slots = nullptr;  // [2][world], shared with peers via CUDA IPC
-    unsigned int* local = nullptr;        // [0] CTA counter, [1] error
+    unsigned int* local = nullptr;        // [0] CTA counter, [1] error, [2..3] epoch (u64)
     ma::XchgDev* d_desc = nullptr;
     std::vector<void*> opened;
-    unsigned long long epoch = 0;
     bool ready = false;
 };
 
@@ -805,8 +806,8 @@ ma_xchg* xchg_new(int world, int rank, void* ipc_handle_out) {
         x->rank = rank;
         CK(cudaMalloc(&x->slots, 2 * static_cast<size_t>(world) * sizeof(unsigned long long)));
         CK(cudaMemset(x->slots, 0, 2 * static_cast<size_t>(world) * sizeof(unsigned long long)));
-        CK(cudaMalloc(&x->local, 2 * sizeof(unsigned int)));
-        CK(cudaMemset(x->local, 0, 2 * sizeof(unsigned int)));
+        CK(cudaMalloc(&x->local, 4 * sizeof(unsigned int)));  // counter, error, epoch (u64)
+        CK(cudaMemset(x->local, 0, 4 * sizeof(unsigned int)));
         CK(cudaMalloc(&x->d_desc, sizeof(ma::XchgDev)));
         cudaIpcMemHandle_t h;
         CK(cudaIpcGetMemHandle(&h, x->slots));
@@ -847,6 +848,7 @@ void xchg_open_impl(ma_xchg* x, const void* all_handles, size_t stride) {
     desc.my_slots = x->slots;
     desc.counter = x->local;
     desc.error = x->local + 1;
+    desc.epoch = reinterpret_cast<unsigned long long*>(x->local + 2);
     desc.timeout_ns = peer_timeout_ns();
     for (int r = 0; r < x->world; ++r) {
         if (r == x->rank) {
@@ -916,10 +918,9 @@ int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n, ma_xch
         if (!s || !x) fail(MA_ERR_INVALID_ARGUMENT, "null stepper / exchange");
         if (!x->ready) fail(MA_ERR_LIFECYCLE, "peer exchange not opened (ma_xchg_open)");
         if (n && !g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
-        x->epoch += 1;
         alignas(16) static const uint32_t dummy[4] = {0, 0, 0, 0};  // never read (n == 0)
         launch_k1(n ? g : &dummy, n, s->g_dtype, &s->d_st->flag, nullptr, 0, true,
-                  as_stream(stream), x->d_desc, x->epoch);
+                  as_stream(stream), x->d_desc);
         s->last = as_stream(stream);
     });
 }
@@ -1649,8 +1650,7 @@ const void* allocation_base(const void* p) {
 uint32_t dtype_bytes(int dt) { return dt == MA_DT_F32 ? 4u : 2u; }
 
 void launch_reduce(ma_stepper* s, const void* const* srcs, int nsrc, int sdt, uint64_t n,
-                   float post_scale, void* dst, const ma::XchgDev* xd, unsigned long long epoch,
-                   cudaStream_t st) {
+                   float post_scale, void* dst, const ma::XchgDev* xd, cudaStream_t st) {
     if (n == 0 && !xd) return;
     const DeviceInfo d = device_info();
     ma::RsArgs a{};
@@ -1662,7 +1662,6 @@ void launch_reduce(ma_stepper* s, const void* const* srcs, int nsrc, int sdt, ui
     a.post_scale = post_scale;
     a.flag = &s->d_st->flag;
     a.xchg = xd;
-    a.epoch = epoch;
     // co-align every source and dst on 16 bytes at the same element
     for (uint64_t h = 0; n >= 8 && h < 8; ++h) {
         bool ok = (reinterpret_cast<uintptr_t>(dst) + h * ed) % 16 == 0;
@@ -1700,7 +1699,7 @@ int ma_stepper_reduce_check_async(ma_stepper* s, const void* const* srcs, int ns
         if (!srcs || !dst) fail(MA_ERR_INVALID_ARGUMENT, "null source list / destination");
         for (int r = 0; r < nsrc; ++r)
             if (!srcs[r]) fail(MA_ERR_INVALID_ARGUMENT, "null source pointer");
-        launch_reduce(s, srcs, nsrc, src_dtype, n, post_scale, dst, nullptr, 0, as_stream(stream));
+        launch_reduce(s, srcs, nsrc, src_dtype, n, post_scale, dst, nullptr, as_stream(stream));
         s->last = as_stream(stream);
     });
 }
@@ -1804,15 +1803,13 @@ int ma_stepper_reduce_scatter_async(ma_stepper* s, ma_rs* r, uint64_t base, uint
         std::vector<const void*> srcs(world);
         for (int k = 0; k < world; ++k) srcs[k] = static_cast<const uint8_t*>(r->grads[k]) + base * es;
         // entry: every rank's gradients are complete before anyone reads them
-        r->x->epoch += 1;
-        ma::launch_peer_barrier(r->x->d_desc, r->x->epoch, &s->d_st->flag, st);
+        ma::launch_peer_barrier(r->x->d_desc, st);
         CK(cudaGetLastError());
         // K4, whose last CTA is the exit barrier (no rank overwrites its
         // gradients while a peer still reads them) and the flag OR
-        r->x->epoch += 1;
         alignas(16) static const uint32_t dummy[4] = {0, 0, 0, 0};  // never written (n == 0)
         launch_reduce(s, srcs.data(), world, r->dtype, n, post_scale, n ? dst : const_cast<uint32_t*>(dummy),
-                      r->x->d_desc, r->x->epoch, st);
+                      r->x->d_desc, st);
         s->last = st;
     });
 }
@@ -1853,13 +1850,11 @@ int ma_stepper_apply_allgather_async(ma_stepper* s, const ma_subgroup* groups, u
                     static_cast<long long>(static_cast<const char*>(ag->grads[k]) - local);
         // entry: every rank is done with its copy of the previous weights
         // (a rank missing here forces this rank's skip, like the exchange)
-        ag->x->epoch += 1;
-        ma::launch_peer_barrier(ag->x->d_desc, ag->x->epoch, &s->d_st->flag, st);
+        ma::launch_peer_barrier(ag->x->d_desc, st);
         CK(cudaGetLastError());
         launch_k2(groups, count, s->g_dtype, s->w_dtype, a, st, /*allgather=*/true);
         // exit: every rank's pushes into every buffer are complete
-        ag->x->epoch += 1;
-        ma::launch_peer_barrier(ag->x->d_desc, ag->x->epoch, nullptr, st);
+        ma::launch_peer_barrier(ag->x->d_desc, st);
         CK(cudaGetLastError());
         s->last = st;
     });

@@ -96,8 +96,20 @@ __device__ uint32_t xchg_post_wait(const XchgDev& x, unsigned long long epoch, u
     return __any_sync(0xFFFFFFFFu, any != 0u);
 }
 
-__device__ void exchange_epilogue(const XchgDev* xp, unsigned long long epoch, uint32_t* flag,
-                                  unsigned lane) {
+// The exchange object's next epoch, read by lane 0 (the previous exchange on
+// this object completed earlier in stream order) and broadcast to the warp;
+// commit_epoch records it once every peer's value has been seen.
+__device__ __forceinline__ unsigned long long next_epoch(const XchgDev& x, unsigned lane) {
+    unsigned long long e = 0;
+    if (lane == 0) e = *reinterpret_cast<volatile unsigned long long*>(x.epoch) + 1ull;
+    return __shfl_sync(0xFFFFFFFFu, e, 0);
+}
+__device__ __forceinline__ void commit_epoch(const XchgDev& x, unsigned long long e,
+                                             unsigned lane) {
+    if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(x.epoch) = e;
+}
+
+__device__ void exchange_epilogue(const XchgDev* xp, uint32_t* flag, unsigned lane) {
     __shared__ uint32_t is_last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -109,7 +121,9 @@ __device__ void exchange_epilogue(const XchgDev* xp, unsigned long long epoch, u
     const XchgDev& x = *xp;
     __threadfence();
     const uint32_t local = *reinterpret_cast<volatile uint32_t*>(flag) != 0u;
+    const unsigned long long epoch = next_epoch(x, lane);
     const uint32_t any = xchg_post_wait(x, epoch, local, lane);
+    commit_epoch(x, epoch, lane);
     if (lane == 0) {
         *flag = any ? 1u : 0u;
         *x.counter = 0u;  // re-arm for the next launch (all CTAs have arrived)
@@ -118,13 +132,15 @@ __device__ void exchange_epilogue(const XchgDev* xp, unsigned long long epoch, u
 }
 
 __device__ __forceinline__ void k1_exchange_epilogue(const K1Args& a, unsigned lane) {
-    exchange_epilogue(a.xchg, a.epoch, a.flag, lane);
+    exchange_epilogue(a.xchg, a.flag, lane);
 }
 
 // Entry / exit barrier of the peer-memory collectives (same fatal rule).
-__global__ void k_peer_barrier(const XchgDev* xp, unsigned long long epoch, uint32_t* flag) {
-    (void)flag;
-    xchg_post_wait(*xp, epoch, 0u, threadIdx.x & 31u);
+__global__ void k_peer_barrier(const XchgDev* xp) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned long long epoch = next_epoch(*xp, lane);
+    xchg_post_wait(*xp, epoch, 0u, lane);
+    commit_epoch(*xp, epoch, lane);
 }
 
 // One-shot K1 (production): CTA b scans the U * 256 consecutive 16-byte
@@ -1282,14 +1298,20 @@ __device__ __forceinline__ void k3_probe8(const K3Raw<GK>& r, uint4& po, uint4& 
                     narrow2_num<kBF16>(V[4], V[5]), narrow2_num<kBF16>(V[6], V[7]));
 }
 
-template <int GK, int U, int MINB, bool PROBE = false, int GUARD = 0>
+// TPC consecutive tiles per CTA (one after the other): the per-CTA set-up
+// (step scalars, segment lookup, ...) is paid once per TPC tiles.
+template <int GK, int U, int MINB, bool PROBE = false, int GUARD = 0, int TPC = 1>
 __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs a) {
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
     const AdamConsts c = a.c;
     constexpr uint32_t kGB = GK == kF32 ? 4u : 2u;
-    const uint64_t t = blockIdx.x;
-    if (t < tab.total_tiles) {
+    const uint64_t main_ctas = (tab.total_tiles + TPC - 1) / TPC;
+    if (blockIdx.x < main_ctas) {
+#pragma unroll 1
+    for (int it = 0; it < TPC; ++it) {
+        const uint64_t t = static_cast<uint64_t>(blockIdx.x) * TPC + it;
+        if (t >= tab.total_tiles) break;
         const Seg& sg = tab.seg[seg_of_tile(tab, t)];
         const uint64_t lt = t - sg.tile_begin;
         const uint64_t j0 = lt * (U * kK2Threads) + threadIdx.x;
@@ -1330,10 +1352,11 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
                 __stcs(V + u * kS, vo);
             }
         }
+    }
         return;
     }
-    const uint64_t q0 = t - tab.total_tiles;
-    const uint64_t nq = gridDim.x - tab.total_tiles;
+    const uint64_t q0 = blockIdx.x - main_ctas;
+    const uint64_t nq = gridDim.x - main_ctas;
     for (uint32_t k = 0; k < tab.count; ++k) {
         const Seg& sg = tab.seg[k];
         if (sg.vector_ok) {
@@ -1498,6 +1521,24 @@ __device__ __forceinline__ uint32_t rs_store8(void* base, uint64_t j, const floa
         for (int k = 0; k < 4; ++k) {
             w[k] = narrow2<K>(x[2 * k], x[2 * k + 1]);
         }
+        __stcs(reinterpret_cast<uint4*>(base) + j, make_uint4(w[0], w[1], w[2], w[3]));
+        return ((w[0] & sw.mask) + sw.inc) | ((w[1] & sw.mask) + sw.inc) |
+               ((w[2] & sw.mask) + sw.inc) | ((w[3] & sw.mask) + sw.inc);
+    }
+}
+
+// rs_store8 without the per-pair NaN branch (pair conversions only): the
+// stored words carry the GPU's canonical NaN; callers re-store a unit whose
+// check bits show a non-finite value with the defined NaN rule.
+template <int K>
+__device__ __forceinline__ uint32_t rs_store8_num(void* base, uint64_t j, const float (&x)[8]) {
+    const ScanWord sw = scan_word(K);
+    if constexpr (K == kF32) {
+        return rs_store8<K>(base, j, x);
+    } else {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = narrow2_num<K>(x[2 * k], x[2 * k + 1]);
         __stcs(reinterpret_cast<uint4*>(base) + j, make_uint4(w[0], w[1], w[2], w[3]));
         return ((w[0] & sw.mask) + sw.inc) | ((w[1] & sw.mask) + sw.inc) |
                ((w[2] & sw.mask) + sw.inc) | ((w[3] & sw.mask) + sw.inc);
@@ -1690,13 +1731,22 @@ __global__ void __launch_bounds__(256, ONE ? 6 : HALF ? 5 : 3) k4_reduce_check(R
             }
         }
         uint8_t* dbody = static_cast<uint8_t*>(a.dst) + a.head * kDstBytes;
+        const bool scaled = a.post_scale != 1.0f;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t j = j0 + static_cast<uint64_t>(u) * blockDim.x;
             if (j >= a.nvec) continue;
+            float y[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) acc[u][k] = rs_finish(acc[u][k], a.post_scale);
-            acc_bits |= rs_store8<DK>(dbody, j, acc[u]);
+            for (int k = 0; k < 8; ++k) y[k] = scaled ? __fmul_rn(acc[u][k], a.post_scale) : acc[u][k];
+            const uint32_t unit = rs_store8_num<DK>(dbody, j, y);
+            if ((unit & top) != 0u) {
+                // a non-finite unit (rare): the defined canonical NaN
+#pragma unroll
+                for (int k = 0; k < 8; ++k) y[k] = rs_finish(acc[u][k], a.post_scale);
+                rs_store8<DK>(dbody, j, y);
+            }
+            acc_bits |= unit;
         }
     } else {
         // trailing CTAs: the scalar head and tail (everything when nvec == 0)
@@ -1711,7 +1761,7 @@ __global__ void __launch_bounds__(256, ONE ? 6 : HALF ? 5 : 3) k4_reduce_check(R
         *a.flag = 1u;
         if (a.xchg) __threadfence();
     }
-    if (a.xchg) exchange_epilogue(a.xchg, a.epoch, a.flag, lane);
+    if (a.xchg) exchange_epilogue(a.xchg, a.flag, lane);
 }
 
 // MA_K4_SINGLE=0 (A/B only) keeps single-source launches on the general kernel
@@ -1757,9 +1807,8 @@ void launch_reduce_check(int sk, int dk, const RsArgs& a, unsigned grid, cudaStr
 #undef MA_RS
 }
 
-void launch_peer_barrier(const XchgDev* x, unsigned long long epoch, uint32_t* flag,
-                         cudaStream_t st) {
-    k_peer_barrier<<<1, 32, 0, st>>>(x, epoch, flag);
+void launch_peer_barrier(const XchgDev* x, cudaStream_t st) {
+    k_peer_barrier<<<1, 32, 0, st>>>(x);
 }
 
 __global__ void k_plant(void* buf, int dtype, uint64_t index, uint32_t bits) {
@@ -2093,6 +2142,11 @@ int k3_slots(int gk, int variant) {
     }
 }
 
+int k3_tiles_per_cta(int gk, int variant) {
+    if (gk != kBF16) return 1;
+    return variant == 19 ? 2 : variant == 20 ? 4 : 1;
+}
+
 int k3_vec(int gk, int variant) {
     if (gk != kBF16) return 8;
     return (variant >= 1 && variant <= 3) || (variant >= 6 && variant <= 8) || variant == 15 ? 4 : 8;
@@ -2120,6 +2174,8 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 9: return f(k3_v2<kBF16, 2, 4>);
         case 16: return f(k3_v2<kBF16, 2, 4, true>);
         case 18: return f(k3_v2<kBF16, 2, 3, false, 1>);
+        case 19: return f(k3_v2<kBF16, 2, 4, false, 1, 2>);
+        case 20: return f(k3_v2<kBF16, 2, 4, false, 1, 4>);
         default: return f(k3_v2<kBF16, 2, 4, false, 1>);
     }
 }

@@ -26,6 +26,8 @@ struct XchgDev {
     unsigned long long* my_slots;               // this rank's slot array [2][world]
     unsigned int* counter;                      // K1 CTAs finished (last CTA exchanges)
     unsigned int* error;                        // set before a fatal timeout / poison trap
+    unsigned long long* epoch;                  // exchanges completed (device-side, so a
+                                                // captured graph replays correctly)
     uint32_t world;
     uint32_t rank;
     unsigned long long timeout_ns;              // MA_PEER_TIMEOUT_S (default 300 s)
@@ -48,7 +50,6 @@ struct K1Args {
     uint32_t elem_bytes;
     int early_exit;
     const XchgDev* xchg;    // non-null: exchange the flag with all ranks at the end
-    unsigned long long epoch;
 };
 
 struct Seg {
@@ -120,6 +121,7 @@ constexpr int kK3Slots = 4;
 int k3_slots(int gk, int variant);
 // elements per vector (slot) of the K3 variant: 4, or 8 for A/B variants 4/5
 int k3_vec(int gk, int variant);
+int k3_tiles_per_cta(int gk, int variant);
 int k3_blocks_per_sm(int gk, int variant);
 void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st);
@@ -141,15 +143,13 @@ struct RsArgs {
     float post_scale;
     uint32_t* flag;
     const XchgDev* xchg;  // non-null: exit barrier + flag OR fused into the last CTA
-    unsigned long long epoch;
 };
 void launch_reduce_check(int sk, int dk, const RsArgs& a, unsigned grid, cudaStream_t st);
 // units per thread the launch for (source kind, source count) uses (host tile size)
 int rs_units_for(int sk, uint32_t nsrc);
-// all ranks meet at `epoch` (one warp; peers' slots over NVLink); a timeout
-// sets *flag (when non-null) so the step is skipped
-void launch_peer_barrier(const XchgDev* x, unsigned long long epoch, uint32_t* flag,
-                         cudaStream_t st);
+// all ranks meet at the exchange object's next epoch (one warp; peers'
+// slots over NVLink); a peer missing for MA_PEER_TIMEOUT_S stops every rank
+void launch_peer_barrier(const XchgDev* x, cudaStream_t st);
 void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, float eps,
                         cudaStream_t s);
 void launch_step_prepare(StepDev* st, const float2* bc_table, float eps, cudaStream_t s);

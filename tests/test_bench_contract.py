@@ -108,6 +108,18 @@ def test_cfg3_injection_line(nproc):
 
 
 @pytest.mark.gpu
+def test_cfg3_p2p_exchange_inside_a_graph_two_ranks():
+    """The fused K1 flag exchange keeps its epoch on the device, so the
+    captured step replays correctly: two ranks (one GPU), the injection plan,
+    decisions and scales checked against the committed plan by bench.py."""
+    j = run(["--config", "cfg3", "--flag-exchange", "p2p", "--graph", "--params", "50000000",
+             "--steps", "10", "--warmup", "3", "--no-cpu-baseline"], nproc=2,
+            env={"MA_BENCH_BACKEND": "gloo", "MA_BENCH_DEVICE": "0"})
+    assert j["config"]["graph"] is True and "peer memory" in j["config"]["flag_exchange"]
+    assert j["cfg3_check"]["decisions_match"] and j["cfg3_check"]["steps_checked"] == 23
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg3"])
 def test_graph_replay_line(cfg):
     j = run(["--config", cfg, "--graph", "--params", "67108864", "--steps", "8", "--warmup", "3",
