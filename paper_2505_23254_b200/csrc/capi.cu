@@ -978,7 +978,6 @@ int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t co
         a.c = s->c;
         a.skip = &s->d_st->flag;
         a.st = s->d_st;
-        a.bc_table = s->d_bc;
         launch_k2(groups, count, s->g_dtype, s->w_dtype, a, as_stream(stream));
         s->last = as_stream(stream);
     });
@@ -995,7 +994,6 @@ int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups, u
         a.c = s->c;
         a.skip = &s->d_st->flag;
         a.st = s->d_st;
-        a.bc_table = s->d_bc;
         std::vector<ma_subgroup> gs(count);
         for (uint32_t k = 0; k < count; ++k) {
             gs[k] = ma_subgroup{reinterpret_cast<float*>(groups[k].p),
@@ -1270,7 +1268,6 @@ ma::AdamArgs stepper_args(ma_stepper* s) {
     a.c = s->c;
     a.skip = &s->d_st->flag;
     a.st = s->d_st;
-    a.bc_table = s->d_bc;
     return a;
 }
 
@@ -1843,7 +1840,6 @@ int ma_stepper_apply_allgather_async(ma_stepper* s, const ma_subgroup* groups, u
         a.c = s->c;
         a.skip = &s->d_st->flag;
         a.st = s->d_st;
-        a.bc_table = s->d_bc;
         for (int k = 0; k < world; ++k)
             if (k != rank)
                 a.peers.delta[a.peers.n++] =

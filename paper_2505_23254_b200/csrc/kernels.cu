@@ -2123,8 +2123,8 @@ void launch_k2_allgather(int gk, int wk, const SegTable& tab, const AdamArgs& a,
 // reductions (0.981).  Other k3_v2 shapes: 9 = per-element compare guard
 // (0.975), 10 = 9 at 3 CTA/SM (0.95), 11 = one slot at 4 (0.87), 12 = four
 // slots at 2 (0.96), 13 = two slots unbounded (0.80), 14 = one slot at 6
-// (0.87), 18 = 0 at 3 CTA/SM (0.95), 16 = access-pattern probe, no Adam
-// (1.01: the ceiling).  Round-1 kernels (k3_adam_bf16, 4-element slots):
+// (0.87), 18 = 0 at 3 CTA/SM (0.95), 19 / 20 = 0 with 2 / 4 tiles per CTA
+// (0.93), 16 = access-pattern probe, no Adam (1.01: the ceiling).  Round-1 kernels (k3_adam_bf16, 4-element slots):
 // 15 = 4 slots at 4 CTA/SM (the round-1 production, 0.94 before / 0.89 after
 // the x86-NaN exact path), 1 = 4 slots unbounded (0.90), 2 = 2 slots at 4
 // (0.84), 3 = 8 slots (0.89), 4/5 = 8-element slots at 4 / unbounded

@@ -88,7 +88,8 @@ struct AdamArgs {
     float scale, bc1, bc2;
     const uint32_t* skip;    // optional skip flag
     const StepDev* st;       // optional device-resident scaler
-    const float2* bc_table;  // (1-b1^t, 1-b2^t) for t = 1.. when st != nullptr
+    // (st != nullptr: the step scalars are read from st, precomputed by
+    //  k_step_prepare / k_step_finish from the bias-correction table)
     PeerW peers;             // fused all-gather targets (launch_k2_allgather only)
 };
 

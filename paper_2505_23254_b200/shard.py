@@ -11,7 +11,11 @@ updates identically and its LossScaler / t evolve identically (SURVEY.md
 
 The step driver is backend-agnostic so the same exchange logic is exercised
 with the B200 kernels (``DeviceShard``) and, in tests, with any object that
-implements the four-method backend protocol.
+implements the four-method backend protocol.  With ``DeviceShard`` the OR
+runs in one of three places: a host-side ``allreduce`` callable
+(torch.distributed), the library's own NCCL communicator
+(``DeviceShard.comm = NcclComm(...)``, no Python on the step path) or K1's
+last CTA over peer memory (``DeviceShard.xchg = FlagExchange(...)``).
 """
 from __future__ import annotations
 
@@ -162,12 +166,17 @@ class DeviceShard:
         plant_bits(self.g, local_index, bits)
 
     xchg = None  # FlagExchange: fuse the cross-rank OR into K1 (no all-reduce)
+    comm = None  # NcclComm: the library's own ncclAllReduce(max) of the flag
 
     def check(self) -> None:
         if self.xchg is not None:
             self.st.check(self.g if self.n else None, xchg=self.xchg)
         elif self.n:
             self.st.check(self.g)
+        if self.comm is not None:
+            # the cross-rank OR inside the library (ma_stepper_allreduce_flag_async),
+            # on the compute stream: pass allreduce=None to ShardStepper
+            self.st.allreduce_flag(self.comm)
 
     def apply(self) -> None:
         if self.n:

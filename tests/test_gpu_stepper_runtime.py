@@ -172,3 +172,57 @@ def test_subgroup_validation():
         r.st.apply([(r.p, r.m, r.v[:-1], r.g, r.w)])
     with pytest.raises(mab.MemAscendError):  # missing working weights
         r.st.apply([(r.p, r.m, r.v, r.g, None)])
+
+
+def test_shard_stepper_with_library_nccl():
+    """shard.py's ShardStepper with the OR in the library's NCCL communicator
+    (DeviceShard.comm, world 1) over cfg3's plan == the single-process oracle."""
+    from paper_2505_23254_b200.shard import DeviceShard, FaultPlan, ShardStepper
+
+    plan = FaultPlan(N, SUB, seed=7)
+    be = DeviceShard(N, 0, SUB, seed=SEED, hyper=mab.AdamHyper(**HYP))
+    be.comm = mab.NcclComm(1, 0, lambda b: b)
+    drv = ShardStepper(be, 0, N, plan, allreduce=None)
+    for s in range(8):
+        drv.step(s)
+    torch.cuda.synchronize()
+    faults = [(p.step, p.index, p.bits) for s in range(8) for p in plan.at(s)]
+    ref = ora.train(N, 8, SEED, g_kind="bf16", w_kind="bf16", hyp=ora.hyper(**HYP),
+                    faults=faults)
+    of, sc = be.st.history()
+    assert of.tolist() == ref["overflow"].astype(bool).tolist()
+    assert sc.tolist() == ref["scale_after"].tolist()
+    for k in "pmv":
+        got = getattr(be, k).cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, ref[k].view(np.uint32)), k
+    be.comm.close()
+
+
+def test_fused_exchange_single_rank_in_a_graph():
+    """K1's fused flag exchange at world 1 (the last-CTA completion counter,
+    the device-side epoch, the slot protocol) eager and replayed from a graph:
+    decisions / state equal the oracle — in one process, so compute-sanitizer
+    sees the protocol (tools/sanitize.sh)."""
+    ref = oracle(10)
+    r = Run()
+    x = mab.api.FlagExchange(1, 0, lambda b: [b])
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+
+    def chain():
+        r.st.check(r.g, stream=stream, xchg=x)
+        r.st.apply(r.groups, stream=stream)
+        r.st.finish(stream=stream)
+
+    for s in range(3):  # eager
+        r.produce(s, stream=stream)
+        chain()
+    graph = r.st.capture(chain, stream, reserve_steps=64)
+    for s in range(3, 10):
+        r.produce(s, stream=stream)
+        graph.launch(stream)
+    stream.synchronize()
+    same(r, ref)
+    assert not x.timed_out()
+    graph.close()
+    x.close()

@@ -58,9 +58,20 @@ def _worker(rank, world, port, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        run_rank(rank, world, out_dir, mab.api.torch_all_gather_bytes())
+    finally:
+        dist.destroy_process_group()
+
+
+def run_rank(rank, world, out_dir, gather):
+    """One rank's steps (also called in-process with world 1 and an identity
+    gather, so the whole peer-memory protocol runs under compute-sanitizer in
+    a single process)."""
+    import paper_2505_23254_b200 as mab
+
+    if True:
         torch.cuda.set_device(0)
         dev = torch.device("cuda", 0)
-        gather = mab.api.torch_all_gather_bytes()
         G = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)   # full-length grads
         W = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)   # full working weights
         P0 = torch.empty(N_TOTAL, dtype=torch.float32, device=dev)
@@ -93,8 +104,6 @@ def _worker(rank, world, port, out_dir):
         rs.close()
         ag.close()
         st.close()
-    finally:
-        dist.destroy_process_group()
 
 
 def oracle_run(world):
@@ -148,3 +157,21 @@ def test_fused_zero_step_over_peer_memory(world):
             b, n = int(res["base"]), int(res["n"])
             for k in "pmv":
                 assert np.array_equal(res[k].view(np.uint32), want[k][b:b + n].view(np.uint32)), (r, k)
+
+
+def test_fused_zero_step_single_process():
+    """World 1 in this process: the entry barrier, K4 with its exit barrier /
+    flag OR and K2's all-gather with both barriers all run (on one rank), so
+    compute-sanitizer sees every peer-memory kernel (tools/sanitize.sh)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    want = oracle_run(1)
+    assert any(want["overflow"]) and not all(want["overflow"])
+    with tempfile.TemporaryDirectory() as d:
+        run_rank(0, 1, d, lambda b: [b])
+        res = np.load(os.path.join(d, "rank0.npz"))
+        assert res["overflow"].astype(bool).tolist() == want["overflow"]
+        assert res["scale"].tolist() == want["scale"]
+        assert np.array_equal(res["W"], want["w"])
+        for k in "pmv":
+            assert np.array_equal(res[k].view(np.uint32), want[k].view(np.uint32)), k

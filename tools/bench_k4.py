@@ -54,7 +54,9 @@ def main():
     st = mab.Stepper(mab.AdamHyper(weight_decay=0.01), 65536.0, 2000, "bf16", "bf16")
     srcs = [torch.randn(n, device="cuda").to(torch.bfloat16) for _ in range(8)]
     dst = torch.empty(n, dtype=torch.bfloat16, device="cuda")
-    for k in (1, 2, 4, 8):
+    # one source measured first and again last: its first figure carries
+    # whatever state the allocations above left (clocks, dirty L2 lines)
+    for k in (1, 2, 4, 8, 1):
         ms = timed(lambda: st.reduce_check(srcs[:k], dst, post_scale=1.0 / k), args.reps)
         byts = (2 * k + 2) * n
         out["k4"].append({"nsrc": k, "ms": ms, "gbs": byts / ms / 1e6,
