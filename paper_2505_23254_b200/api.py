@@ -337,8 +337,8 @@ class Stepper:
         keep = []
         for k, (state, g, w) in enumerate(groups):
             n = g.numel()
-            if n > slot_elems:
-                raise MemAscendError(1, f"group {k}: {n} elements exceed slot_elems {slot_elems}")
+            if n > slot_elems:  # the C ABI's code for this case (size_violation)
+                raise MemAscendError(7, f"group {k}: {n} elements exceed slot_elems {slot_elems}")
             if w is not None and w.numel() != n:
                 raise MemAscendError(1, f"group {k}: working-weight length differs")
             if isinstance(state[0], str):
@@ -378,8 +378,11 @@ class Stepper:
         arr = (capi.SwapGroupBf16 * len(groups))()
         keep = []
         for k, (state, p, g) in enumerate(groups):
-            if p.numel() > slot_elems or g.numel() != p.numel():
-                raise MemAscendError(1, f"group {k}: length exceeds slot_elems or g/p differ")
+            if p.numel() > slot_elems:
+                raise MemAscendError(7, f"group {k}: {p.numel()} elements exceed slot_elems "
+                                        f"{slot_elems}")
+            if g.numel() != p.numel():
+                raise MemAscendError(1, f"group {k}: gradient and weight lengths differ")
             if isinstance(state[0], str):
                 keys = [x.encode() for x in state]
                 keep.append(keys)

@@ -69,41 +69,40 @@ def run_rank(rank, world, out_dir, gather):
     a single process)."""
     import paper_2505_23254_b200 as mab
 
-    if True:
-        torch.cuda.set_device(0)
-        dev = torch.device("cuda", 0)
-        G = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)   # full-length grads
-        W = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)   # full working weights
-        P0 = torch.empty(N_TOTAL, dtype=torch.float32, device=dev)
-        mab.gen_seeded_weights(P0, W, seed=SEED)
-        base, n = shard_range(N_TOTAL, world, rank, SUBGROUP)
-        p = P0[base:base + n].clone()
-        m = torch.zeros(n, dtype=torch.float32, device=dev)
-        v = torch.zeros(n, dtype=torch.float32, device=dev)
-        gp = torch.empty(n, dtype=torch.bfloat16, device=dev)        # reduced partition grads
-        rs = mab.api.GradReduceScatter(world, rank, G, gather)
-        ag = mab.api.GradReduceScatter(world, rank, W, gather)
-        st = mab.Stepper(mab.AdamHyper(**HYP), 65536.0, 2000, "bf16", "bf16", device=dev)
-        w = W[base:base + n]
-        groups = [(p[o:o + SUBGROUP], m[o:o + SUBGROUP], v[o:o + SUBGROUP], gp[o:o + SUBGROUP],
-                   w[o:o + SUBGROUP]) for o in range(0, n, SUBGROUP)]
-        for s in range(STEPS):
-            scale = st.state()["scale"]
-            G.copy_(torch.from_numpy(rank_grads(rank, s, scale).view(np.int16)).to(dev)
-                    .view(torch.bfloat16))
-            st.reduce_scatter(rs, base, n, gp, post_scale=1.0 / world)
-            st.apply_allgather(groups, ag)
-            st.finish()
-        torch.cuda.synchronize()
-        assert not rs.timed_out() and not ag.timed_out()
-        of, sc = st.history()
-        np.savez(os.path.join(out_dir, f"rank{rank}.npz"),
-                 W=W.view(torch.int16).cpu().numpy().view(np.uint16), p=p.cpu().numpy(),
-                 m=m.cpu().numpy(), v=v.cpu().numpy(), overflow=of.astype(np.uint8), scale=sc,
-                 base=base, n=n)
-        rs.close()
-        ag.close()
-        st.close()
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    G = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)   # full-length grads
+    W = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)   # full working weights
+    P0 = torch.empty(N_TOTAL, dtype=torch.float32, device=dev)
+    mab.gen_seeded_weights(P0, W, seed=SEED)
+    base, n = shard_range(N_TOTAL, world, rank, SUBGROUP)
+    p = P0[base:base + n].clone()
+    m = torch.zeros(n, dtype=torch.float32, device=dev)
+    v = torch.zeros(n, dtype=torch.float32, device=dev)
+    gp = torch.empty(n, dtype=torch.bfloat16, device=dev)        # reduced partition grads
+    rs = mab.api.GradReduceScatter(world, rank, G, gather)
+    ag = mab.api.GradReduceScatter(world, rank, W, gather)
+    st = mab.Stepper(mab.AdamHyper(**HYP), 65536.0, 2000, "bf16", "bf16", device=dev)
+    w = W[base:base + n]
+    groups = [(p[o:o + SUBGROUP], m[o:o + SUBGROUP], v[o:o + SUBGROUP], gp[o:o + SUBGROUP],
+               w[o:o + SUBGROUP]) for o in range(0, n, SUBGROUP)]
+    for s in range(STEPS):
+        scale = st.state()["scale"]
+        G.copy_(torch.from_numpy(rank_grads(rank, s, scale).view(np.int16)).to(dev)
+                .view(torch.bfloat16))
+        st.reduce_scatter(rs, base, n, gp, post_scale=1.0 / world)
+        st.apply_allgather(groups, ag)
+        st.finish()
+    torch.cuda.synchronize()
+    assert not rs.timed_out() and not ag.timed_out()
+    of, sc = st.history()
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"),
+             W=W.view(torch.int16).cpu().numpy().view(np.uint16), p=p.cpu().numpy(),
+             m=m.cpu().numpy(), v=v.cpu().numpy(), overflow=of.astype(np.uint8), scale=sc,
+             base=base, n=n)
+    rs.close()
+    ag.close()
+    st.close()
 
 
 def oracle_run(world):
