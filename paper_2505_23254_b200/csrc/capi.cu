@@ -710,7 +710,7 @@ int ma_stepper_create(const ma_adam_hyper* h, float init_scale, uint32_t growth_
             CK(cudaMemcpy(s->d_st, &init, sizeof init, cudaMemcpyHostToDevice));
             CK(cudaMemset(s->d_log, 0, sizeof(ma::StepLog) * ma::kHistory));
             stepper_grow_bc(s, 1024);
-            ma::launch_step_prepare(s->d_st, s->d_bc, s->c.eps, nullptr);
+            ma::launch_step_prepare(s->d_st, s->d_bc, s->c, nullptr);
             CK(cudaGetLastError());
             CK(cudaDeviceSynchronize());
         } catch (...) {
@@ -1382,7 +1382,7 @@ int ma_stepper_finish_async(ma_stepper* s, void* stream) {
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         stepper_grow_bc(s, s->t_base + s->issued + 2);  // the next update's scalars
-        ma::launch_step_finish(s->d_st, s->d_log, s->d_bc, s->c.eps, as_stream(stream));
+        ma::launch_step_finish(s->d_st, s->d_log, s->d_bc, s->c, as_stream(stream));
         CK(cudaGetLastError());
         s->issued += 1;
         s->last = as_stream(stream);
@@ -1424,7 +1424,7 @@ int ma_stepper_set_state(ma_stepper* s, float scale, uint32_t clean_steps, uint6
         s->t_base = updates;
         s->issued = 0;
         stepper_grow_bc(s, updates + 2);
-        ma::launch_step_prepare(s->d_st, s->d_bc, s->c.eps, nullptr);
+        ma::launch_step_prepare(s->d_st, s->d_bc, s->c, nullptr);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
     });

@@ -291,13 +291,13 @@ __global__ void __launch_bounds__(kK1Threads) k1_overflow(K1Args a) {
 
 // ============================================================== K2
 // Per-step scalars of an explicit step (scale, bc1, bc2 from the host).
-__device__ __forceinline__ void scalars_from(float scale, float bc1, float bc2, float eps,
-                                             StepScalars& s) {
+__device__ __forceinline__ void scalars_from(float scale, float bc1, float bc2,
+                                             const AdamConsts& c, StepScalars& s) {
     s.scale = scale;
     s.bc1 = bc1;
     s.bc2 = bc2;
     s.scale_pow2 = exact_reciprocal(s.scale, &s.inv_scale);
-    s.fast = s.scale_pow2 && fast_step_ok(s.bc1, s.bc2, eps);
+    s.fast = s.scale_pow2 && fast_step_ok(s.bc1, s.bc2, c.eps, c.lr, c.lr_wd);
     s.y1 = s.fast ? rcp_refined(s.bc1) : 0.0f;
     s.y2 = s.fast ? rcp_refined(s.bc2) : 0.0f;
 }
@@ -322,7 +322,7 @@ __device__ __forceinline__ bool resolve_step(const AdamArgs& a, StepScalars& s) 
         return true;
     }
     if (a.skip != nullptr && *a.skip != 0u) return false;
-    scalars_from(a.scale, a.bc1, a.bc2, a.c.eps, s);
+    scalars_from(a.scale, a.bc1, a.bc2, a.c, s);
     return true;
 }
 
@@ -409,7 +409,7 @@ template <int GK, int WK, int AG = 0>
 __device__ __forceinline__ void adam_scalar(const Seg& sg, uint64_t e, const AdamConsts& c,
                                             const StepScalars& s, const PeerW& pw = kNoPeers) {
     float p = sg.p[e], m = sg.m[e], v = sg.v[e];
-    adam_elem(p, m, v, load_grad1<GK>(sg.g, e), c, s);
+    adam_any(p, m, v, load_grad1<GK>(sg.g, e), c, s);
     sg.p[e] = p;
     sg.m[e] = m;
     sg.v[e] = v;
@@ -541,10 +541,10 @@ struct Exact4 {
 template <int ORD>
 __device__ __noinline__ Exact4 adam_exact4(float4 p, float4 m, float4 v, float4 g,
                                            const AdamConsts c, const StepScalars s) {
-    adam_elem<ORD>(p.x, m.x, v.x, g.x, c, s);
-    adam_elem<ORD>(p.y, m.y, v.y, g.y, c, s);
-    adam_elem<ORD>(p.z, m.z, v.z, g.z, c, s);
-    adam_elem<ORD>(p.w, m.w, v.w, g.w, c, s);
+    adam_any<ORD>(p.x, m.x, v.x, g.x, c, s);
+    adam_any<ORD>(p.y, m.y, v.y, g.y, c, s);
+    adam_any<ORD>(p.z, m.z, v.z, g.z, c, s);
+    adam_any<ORD>(p.w, m.w, v.w, g.w, c, s);
     return Exact4{p, m, v};
 }
 
@@ -914,7 +914,7 @@ __device__ __forceinline__ void bf16_state_scalar(const Seg& sg, uint64_t e, con
     uint16_t* M = reinterpret_cast<uint16_t*>(sg.m);
     uint16_t* V = reinterpret_cast<uint16_t*>(sg.v);
     float p = widen_bf16(P[e]), m = widen_bf16(M[e]), v = widen_bf16(V[e]);
-    adam_elem<kOrdBf16>(p, m, v, load_grad1<GK>(sg.g, e), c, s);
+    adam_any<kOrdBf16>(p, m, v, load_grad1<GK>(sg.g, e), c, s);
     P[e] = narrow<kBF16>(p);
     M[e] = narrow<kBF16>(m);
     V[e] = narrow<kBF16>(v);
@@ -1203,7 +1203,7 @@ __device__ __noinline__ void adam_exact8_bf16(K3Raw<GK> r, uint4* out, const Ada
         p[k] = bf16_lane(r.p, k);
         m[k] = bf16_lane(r.m, k);
         v[k] = bf16_lane(r.v, k);
-        adam_elem<kOrdBf16>(p[k], m[k], v[k], k3_grad<GK>(r, k), c, s);
+        adam_any<kOrdBf16>(p[k], m[k], v[k], k3_grad<GK>(r, k), c, s);
     }
     out[0] = make_uint4(narrow2<kBF16>(p[0], p[1]), narrow2<kBF16>(p[2], p[3]),
                         narrow2<kBF16>(p[4], p[5]), narrow2<kBF16>(p[6], p[7]));
@@ -1278,6 +1278,7 @@ __device__ __forceinline__ bool k3_fast8(const K3Raw<GK>& r, uint4& po, uint4& m
     return ok;
 }
 
+
 // NOT an optimizer: the same loads / stores / grid with a trivial update
 // (A/B variant 16, MA_K3_VARIANT=16) — the access pattern's own ceiling.
 template <int GK>
@@ -1341,6 +1342,8 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
                 if constexpr (PROBE) {
                     k3_probe8<GK>(q[u], po, mo, vo);
                 } else if (!(sc.fast && k3_fast8<GK, GUARD>(q[u], po, mo, vo, c, sc))) {
+                    // includes cold slots: adam_exact8_bf16 -> adam_any (fast, cold
+                    // second chance, else the full exact sequence) per element
                     uint4 out[3];
                     adam_exact8_bf16<GK>(q[u], out, c, sc);
                     po = out[0];
@@ -1376,10 +1379,10 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
 
 // ============================================================== step finish
 // The next update's scalars (t = updates + 1, current scale) into StepDev.
-__device__ void step_prepare(StepDev* st, const float2* bc_table, float eps) {
+__device__ void step_prepare(StepDev* st, const float2* bc_table, const AdamConsts c) {
     const float2 bc = bc_table[st->updates];
     StepScalars s;
-    scalars_from(st->scale, bc.x, bc.y, eps, s);
+    scalars_from(st->scale, bc.x, bc.y, c, s);
     st->inv_scale = s.scale_pow2 ? s.inv_scale : 0.0f;
     st->bc1 = s.bc1;
     st->bc2 = s.bc2;
@@ -1388,14 +1391,15 @@ __device__ void step_prepare(StepDev* st, const float2* bc_table, float eps) {
     st->mode = (s.scale_pow2 ? 1u : 0u) | (s.fast ? 2u : 0u);
 }
 
-__global__ void k_step_prepare(StepDev* st, const float2* bc_table, float eps) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) step_prepare(st, bc_table, eps);
+__global__ void k_step_prepare(StepDev* st, const float2* bc_table, const AdamConsts c) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) step_prepare(st, bc_table, c);
 }
 
 // LossScaler::on_overflow / on_clean_step (optimizer.hpp:24-34) and the
 // update counter (simulator.cpp:438-444,491); re-arms the flag and prepares
 // the next update's scalars.
-__global__ void k_step_finish(StepDev* st, StepLog* log, const float2* bc_table, float eps) {
+__global__ void k_step_finish(StepDev* st, StepLog* log, const float2* bc_table,
+                              const AdamConsts c) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const uint32_t of = st->flag != 0u;
     if (of) {
@@ -1413,7 +1417,7 @@ __global__ void k_step_finish(StepDev* st, StepLog* log, const float2* bc_table,
     st->steps += 1ull;
     st->last_overflow = of;
     st->flag = 0u;
-    step_prepare(st, bc_table, eps);
+    step_prepare(st, bc_table, c);
 }
 
 // ============================================================== generators
@@ -2193,13 +2197,14 @@ void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsi
     k3_dispatch(gk, variant, [&](auto fn) { fn<<<grid, kK2Threads, 0, st>>>(tab, a); });
 }
 
-void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, float eps,
+void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, const AdamConsts& c,
                         cudaStream_t s) {
-    k_step_finish<<<1, 32, 0, s>>>(st, log, bc_table, eps);
+    k_step_finish<<<1, 32, 0, s>>>(st, log, bc_table, c);
 }
 
-void launch_step_prepare(StepDev* st, const float2* bc_table, float eps, cudaStream_t s) {
-    k_step_prepare<<<1, 32, 0, s>>>(st, bc_table, eps);
+void launch_step_prepare(StepDev* st, const float2* bc_table, const AdamConsts& c,
+                         cudaStream_t s) {
+    k_step_prepare<<<1, 32, 0, s>>>(st, bc_table, c);
 }
 
 void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,
