@@ -1301,13 +1301,26 @@ __device__ __forceinline__ void k3_probe8(const K3Raw<GK>& r, uint4& po, uint4& 
 
 // TPC consecutive tiles per CTA (one after the other): the per-CTA set-up
 // (step scalars, segment lookup, ...) is paid once per TPC tiles.
-template <int GK, int U, int MINB, bool PROBE = false, int GUARD = 0, int TPC = 1>
+// DEFER: a slot that fails the fast guard is not computed in the hot loop
+// (no call there); its index goes to a shared-memory list and, after the
+// tile, all threads of the CTA process the listed slots element by element
+// (adam_any: fast, cold second chance, else the full exact sequence) — no
+// SIMT divergence, and cold or non-finite slots cost their own work only.
+template <int GK, int U, int MINB, bool PROBE = false, int GUARD = 0, int TPC = 1,
+          bool DEFER = false>
 __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs a) {
+    static_assert(!DEFER || TPC == 1, "deferred slots: one tile per CTA");
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
     const AdamConsts c = a.c;
     constexpr uint32_t kGB = GK == kF32 ? 4u : 2u;
     const uint64_t main_ctas = (tab.total_tiles + TPC - 1) / TPC;
+    __shared__ uint32_t dlist[DEFER ? U * kK2Threads : 1];
+    __shared__ uint32_t dn;
+    if constexpr (DEFER) {
+        if (threadIdx.x == 0) dn = 0;
+        __syncthreads();
+    }
     if (blockIdx.x < main_ctas) {
 #pragma unroll 1
     for (int it = 0; it < TPC; ++it) {
@@ -1342,17 +1355,63 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
                 if constexpr (PROBE) {
                     k3_probe8<GK>(q[u], po, mo, vo);
                 } else if (!(sc.fast && k3_fast8<GK, GUARD>(q[u], po, mo, vo, c, sc))) {
-                    // includes cold slots: adam_exact8_bf16 -> adam_any (fast, cold
-                    // second chance, else the full exact sequence) per element
-                    uint4 out[3];
-                    adam_exact8_bf16<GK>(q[u], out, c, sc);
-                    po = out[0];
-                    mo = out[1];
-                    vo = out[2];
+                    if constexpr (DEFER) {
+                        dlist[atomicAdd(&dn, 1u)] = u * kK2Threads + threadIdx.x;
+                        continue;
+                    } else {
+                        // includes cold slots: adam_exact8_bf16 -> adam_any (fast,
+                        // cold second chance, else the full exact sequence)
+                        uint4 out[3];
+                        adam_exact8_bf16<GK>(q[u], out, c, sc);
+                        po = out[0];
+                        mo = out[1];
+                        vo = out[2];
+                    }
                 }
                 __stcs(P + u * kS, po);
                 __stcs(M + u * kS, mo);
                 __stcs(V + u * kS, vo);
+            }
+        }
+        if constexpr (DEFER) {
+            // one listed slot per thread, 16-byte accesses as in the hot loop
+            __syncthreads();
+            const uint32_t nd = dn;
+            if (nd == 0) continue;
+            // the tile's slot 0, recomputed here so no pointer stays live
+            // through the hot loop for this rare phase
+            const Seg& sd = tab.seg[seg_of_tile(tab, t)];
+            const uint64_t b0 = sd.head + 8 * ((t - sd.tile_begin) * (U * kK2Threads));
+            uint4* P0 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sd.p) + b0);
+            uint4* M0 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sd.m) + b0);
+            uint4* V0 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sd.v) + b0);
+            const uint4* G0 = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(sd.g) + b0 * kGB);
+            for (uint32_t d = threadIdx.x; d < nd; d += kK2Threads) {
+                const uint32_t sl = dlist[d];
+                K3Raw<GK> r;
+                r.p = __ldcs(P0 + sl);
+                r.m = __ldcs(M0 + sl);
+                r.v = __ldcs(V0 + sl);
+                r.g[0] = __ldcs(G0 + sl * (kGB / 2));
+                if constexpr (GK == kF32) r.g[1] = __ldcs(G0 + sl * 2 + 1);
+                uint32_t wp[4], wm[4], wv[4];
+#pragma unroll
+                for (int k = 0; k < 8; k += 2) {
+                    float p2[2], m2[2], v2[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        p2[h] = bf16_lane(r.p, k + h);
+                        m2[h] = bf16_lane(r.m, k + h);
+                        v2[h] = bf16_lane(r.v, k + h);
+                        adam_any<kOrdBf16>(p2[h], m2[h], v2[h], k3_grad<GK>(r, k + h), c, sc);
+                    }
+                    wp[k >> 1] = narrow2<kBF16>(p2[0], p2[1]);
+                    wm[k >> 1] = narrow2<kBF16>(m2[0], m2[1]);
+                    wv[k >> 1] = narrow2<kBF16>(v2[0], v2[1]);
+                }
+                __stcs(P0 + sl, make_uint4(wp[0], wp[1], wp[2], wp[3]));
+                __stcs(M0 + sl, make_uint4(wm[0], wm[1], wm[2], wm[3]));
+                __stcs(V0 + sl, make_uint4(wv[0], wv[1], wv[2], wv[3]));
             }
         }
     }
@@ -2121,19 +2180,21 @@ void launch_k2_allgather(int gk, int wk, const SegTable& tab, const AdamArgs& a,
 #undef MA_AG
 }
 
-// K3 A/B (MA_K3_VARIANT; DESIGN.md §5), fractions of the copy peak at 268 M
-// params, bf16 g.  0 (= 17) = production: k3_v2, two 8-element slots per
-// thread at 4 CTA/SM, the admission guard on NaN-propagating min / max
-// reductions (0.981).  Other k3_v2 shapes: 9 = per-element compare guard
+// K3 A/B (MA_K3_VARIANT; DESIGN.md §3.2), fractions of the copy peak at 268 M
+// params, bf16 g.  0 = production: k3_v2, two 8-element slots per thread at
+// 4 CTA/SM, the admission guard on NaN-propagating min / max reductions,
+// slots that fail it deferred to a shared-memory list and computed after the
+// tile (no call in the hot loop; 1.00).  17 = the same with the exact path
+// called from the hot loop (0.98), 9 = 17 with five compares per element
 // (0.975), 10 = 9 at 3 CTA/SM (0.95), 11 = one slot at 4 (0.87), 12 = four
 // slots at 2 (0.96), 13 = two slots unbounded (0.80), 14 = one slot at 6
-// (0.87), 18 = 0 at 3 CTA/SM (0.95), 19 / 20 = 0 with 2 / 4 tiles per CTA
-// (0.93), 16 = access-pattern probe, no Adam (1.01: the ceiling).  Round-1 kernels (k3_adam_bf16, 4-element slots):
-// 15 = 4 slots at 4 CTA/SM (the round-1 production, 0.94 before / 0.89 after
-// the x86-NaN exact path), 1 = 4 slots unbounded (0.90), 2 = 2 slots at 4
-// (0.84), 3 = 8 slots (0.89), 4/5 = 8-element slots at 4 / unbounded
-// (0.90 / 0.80), 6 = 2 slots at 5 (0.86), 7 = 3 slots at 4 (0.91), 8 = 4
-// slots at 5 (0.88).
+// (0.87), 18 = 17 at 3 CTA/SM (0.95), 19 / 20 = 17 with 2 / 4 tiles per CTA
+// (0.93), 16 = access-pattern probe, no Adam (1.01: the ceiling).  Round-1
+// kernels (k3_adam_bf16, 4-element slots): 15 = 4 slots at 4 CTA/SM (the
+// round-1 production, 0.94 before / 0.89 after the x86-NaN exact path), 1 =
+// 4 slots unbounded (0.90), 2 = 2 slots at 4 (0.84), 3 = 8 slots (0.89),
+// 4/5 = 8-element slots at 4 / unbounded (0.90 / 0.80), 6 = 2 slots at 5
+// (0.86), 7 = 3 slots at 4 (0.91), 8 = 4 slots at 5 (0.88).
 int k3_slots(int gk, int variant) {
     if (gk != kBF16) return 2;  // k3_v2<GK, 2, 4>
     switch (variant) {
@@ -2158,8 +2219,8 @@ int k3_vec(int gk, int variant) {
 
 template <typename F>
 void k3_dispatch(int gk, int variant, F&& f) {
-    if (gk == kF32) return f(k3_v2<kF32, 2, 4, false, 1>);
-    if (gk == kF16) return f(k3_v2<kF16, 2, 4, false, 1>);
+    if (gk == kF32) return f(k3_v2<kF32, 2, 4, false, 1, 1, true>);
+    if (gk == kF16) return f(k3_v2<kF16, 2, 4, false, 1, 1, true>);
     switch (variant) {
         case 1: return f(k3_adam_bf16<kBF16, 4, 1>);
         case 2: return f(k3_adam_bf16<kBF16, 2, 4>);
@@ -2179,8 +2240,9 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 16: return f(k3_v2<kBF16, 2, 4, true>);
         case 18: return f(k3_v2<kBF16, 2, 3, false, 1>);
         case 19: return f(k3_v2<kBF16, 2, 4, false, 1, 2>);
+        case 17: return f(k3_v2<kBF16, 2, 4, false, 1>);
         case 20: return f(k3_v2<kBF16, 2, 4, false, 1, 4>);
-        default: return f(k3_v2<kBF16, 2, 4, false, 1>);
+        default: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true>);
     }
 }
 
