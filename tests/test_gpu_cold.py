@@ -84,3 +84,45 @@ def test_k3_cold_elements_equal_reference(t):
                        mab.AdamHyper(lr=1e-3, weight_decay=0.01), 65536.0)
     for got, want in zip(d, ref):
         assert np.array_equal(got.cpu().numpy().view(np.uint16), want)
+
+
+@pytest.mark.parametrize("kernel", ["k2", "k3"])
+def test_cold_rows_over_120_steps_equal_oracle(kernel):
+    """An embedding-like table of 256 rows x 4096 over 120 steps: some rows
+    never receive a gradient (m = v = 0 throughout), some only in the first
+    step (their momentum decays through 2^-50 into the decayed-moment
+    shortcut: beta1 = 0.5), the rest at random half of the steps.  State
+    equal to the oracle (the reference's arithmetic) bit for bit at every
+    10th step and at the end."""
+    rows, cols, steps = 256, 4096, 120
+    n = rows * cols
+    rng = np.random.default_rng(11)
+    kind = rng.integers(0, 3, rows)           # 0 never, 1 first step only, 2 intermittent
+    h = ora.hyper(lr=1e-3, beta1=0.5, beta2=0.999, weight_decay=0.01)
+    hd = mab.AdamHyper(lr=1e-3, beta1=0.5, beta2=0.999, weight_decay=0.01)
+    p0 = (rng.standard_normal(n) * 0.1).astype(f32)
+    if kernel == "k2":
+        ref = [p0.copy(), np.zeros(n, f32), np.zeros(n, f32)]
+        d = [torch.from_numpy(x.copy()).cuda() for x in ref]
+    else:
+        ref = [(p0.view(np.uint32) >> 16).astype(np.uint16), np.zeros(n, np.uint16),
+               np.zeros(n, np.uint16)]
+        d = [torch.from_numpy(x.view(np.int16).copy()).cuda() for x in ref]
+    for t in range(1, steps + 1):
+        live = np.where(kind == 2, rng.random(rows) < 0.5, (kind == 1) & (t == 1))
+        g = (rng.standard_normal(n) * 64).astype(f32) * np.repeat(live, cols).astype(f32)
+        gd = torch.from_numpy(g).cuda()
+        if kernel == "k2":
+            ora.adam_step(*ref, g, t, h, 65536.0)
+            mab.adam_step_fp32(*d, gd, t, hd, 65536.0)
+        else:
+            ora.adam_step_bf16(*ref, g, t, h, 65536.0)
+            mab.adam_step_bf16(*d, gd, t, hd, 65536.0)
+        if t % 10 == 0 or t == steps:
+            for got, want, name in zip(d, ref, "pmv"):
+                a = got.cpu().numpy().view(want.dtype)
+                assert np.array_equal(a, want), (t, name)
+    # the decayed-moment route was exercised: first-step-only rows' m is tiny
+    if kernel == "k2":
+        m_once = np.abs(ref[1].reshape(rows, cols)[kind == 1])
+        assert ((m_once > 0) & (m_once < 2.0 ** -50)).mean() > 0.5
