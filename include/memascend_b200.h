@@ -354,6 +354,16 @@ MA_API int ma_host_register(void* ptr, uint64_t bytes);
 MA_API int ma_host_unregister(void* ptr);
 /* 1 if ptr is device memory, 2 registered/pinned host, 0 pageable host. */
 MA_API int ma_pointer_kind(const void* ptr, int* kind);
+/* NUMA placement (multi-socket hosts, e.g. 8 x B200 on two sockets): the
+ * node of the current device's PCIe root (-1 if unknown), and the node
+ * backing a host address (-1 if unknown).  ma_host_register first prefers
+ * the device's node for the region's pages (mbind, moving pages already
+ * touched) unless MA_NUMA_BIND=0 — best effort, a no-op on one-node hosts. */
+MA_API int ma_device_numa_node(int* node);
+/* The same placement alone, for memory about to be first touched (call it
+ * before filling a fresh allocation; ma_host_register would move the pages). */
+MA_API int ma_host_place(void* ptr, uint64_t bytes);
+MA_API int ma_host_numa_node(const void* ptr, int* node);
 
 /* ------------------------------------------------------------------ */
 /* Swap store (DirectIoEngine, proj/include/memascend/direct_io.hpp:23-180,

@@ -199,6 +199,9 @@ SIGNATURES = [
     ("ma_host_register", _I, [_VP, _U64]),
     ("ma_host_unregister", _I, [_VP]),
     ("ma_pointer_kind", _I, [_VP, C.POINTER(_I)]),
+    ("ma_device_numa_node", _I, [C.POINTER(_I)]),
+    ("ma_host_place", _I, [_VP, _U64]),
+    ("ma_host_numa_node", _I, [_VP, C.POINTER(_I)]),
     ("ma_debug_cast_sweep", _I, [_I, _I, _VP]),
     ("ma_debug_mask_sweep", _I, [_I, C.POINTER(_U64)]),
     ("ma_debug_fast_sweep", _I, [_I, _VP, _U32, _U64, _U64, C.POINTER(_U64), C.POINTER(_U64)]),

@@ -6,13 +6,17 @@
 // code plus a thread-local message; nothing here falls back to the CPU.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstddef>
 #include <cstring>
+#include <fstream>
 #include <mutex>
 #include <condition_variable>
 #include <deque>
@@ -175,6 +179,50 @@ Scratch& scratch() {
     int d = 0;
     cudaGetDevice(&d);
     return s[d % 16];
+}
+
+// ------------------------------------------------------------ NUMA
+// Host memory the GPU streams from (gradients, the state pool, staging
+// slots) belongs on the NUMA node of the GPU's PCIe root: on a two-socket
+// 8 x B200 box the other socket's memory reaches the GPU through the
+// inter-socket link at a fraction of the PCIe rate.  The node comes from
+// sysfs; pages are preferred there (and already-touched ones moved) with
+// mbind before cudaHostRegister pins them.  Best effort: one-node hosts,
+// containers without mbind, and MA_NUMA_BIND=0 leave the placement alone.
+int current_device_numa_node() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) return -1;
+    std::string id(bus);
+    for (char& ch : id) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+    std::ifstream f("/sys/bus/pci/devices/" + id + "/numa_node");
+    int node = -1;
+    if (!(f >> node)) return -1;
+    return node;
+}
+
+int host_numa_nodes() {
+    std::ifstream f("/sys/devices/system/node/possible");  // e.g. "0-1"
+    std::string s;
+    if (!(f >> s)) return 1;
+    const auto dash = s.find('-');
+    return dash == std::string::npos ? 1 : std::atoi(s.c_str() + dash + 1) + 1;
+}
+
+void numa_place_for_device(void* ptr, uint64_t bytes) {
+    if (const char* e = std::getenv("MA_NUMA_BIND"); e && e[0] == '0') return;
+    static const int nodes = host_numa_nodes();
+    if (nodes < 2) return;
+    const int node = current_device_numa_node();
+    if (node < 0 || node >= 1024) return;
+    const uintptr_t page = 4096;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(ptr) & ~(page - 1);
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(ptr) + bytes + page - 1) & ~(page - 1);
+    unsigned long mask[16] = {0};
+    mask[node / 64] |= 1ul << (node % 64);
+    // MPOL_PREFERRED (1), MPOL_MF_MOVE (2): errors are ignored (best effort)
+    ::syscall(SYS_mbind, lo, hi - lo, 1ul, mask, 1024ul, 2ul);
 }
 
 // ------------------------------------------------------------ K1 launch
@@ -1500,7 +1548,34 @@ int ma_host_register(void* ptr, uint64_t bytes) {
     return guarded([&] {
         if (!ptr || bytes == 0) fail(MA_ERR_INVALID_ARGUMENT, "empty host region");
         device_info();
+        numa_place_for_device(ptr, bytes);  // before pinning: pages can still move
         CK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+    });
+}
+
+int ma_host_place(void* ptr, uint64_t bytes) {
+    return guarded([&] {
+        if (!ptr || bytes == 0) fail(MA_ERR_INVALID_ARGUMENT, "empty host region");
+        numa_place_for_device(ptr, bytes);
+    });
+}
+
+int ma_device_numa_node(int* node) {
+    return guarded([&] {
+        if (!node) fail(MA_ERR_INVALID_ARGUMENT, "null output");
+        device_info();
+        *node = current_device_numa_node();
+    });
+}
+
+int ma_host_numa_node(const void* ptr, int* node) {
+    return guarded([&] {
+        if (!ptr || !node) fail(MA_ERR_INVALID_ARGUMENT, "null argument");
+        int n = -1;
+        // get_mempolicy(MPOL_F_NODE | MPOL_F_ADDR): the node backing the page
+        if (::syscall(SYS_get_mempolicy, &n, nullptr, 0ul, const_cast<void*>(ptr), 3ul) != 0)
+            n = -1;
+        *node = n;
     });
 }
 

@@ -127,6 +127,9 @@ PinnedRegion PinnedAllocator::allocate(std::uint64_t request, const AllocationPo
         raise(ErrorCode::out_of_memory,
               "posix_memalign failed for " + std::to_string(capacity) + " bytes");
     }
+    // first touch on the NUMA node of the current GPU (best effort, no-op on
+    // one-node hosts or without a device), then the reference's zero fill
+    (void)ma_host_place(raw, capacity);
     std::memset(raw, 0, static_cast<std::size_t>(capacity));
     // cudaHostRegister page-locks and maps the region for DMA / device access.
     const bool registered = ma_host_register(raw, capacity) == MA_OK;

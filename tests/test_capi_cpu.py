@@ -153,3 +153,23 @@ def test_state_pool_shim_plans_the_drop_in_pool():
             sp.tensor(0, 0)
         assert e.value.code == "capability"
     sp.close()
+
+
+def test_numa_placement_entry_points(so_path):
+    """ma_host_numa_node reports the node backing a page; ma_host_place is a
+    best-effort no-op where it cannot act (one node / no device); the
+    device's node needs a device."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2505_23254_b200 import capi
+
+    L = capi.lib()
+    a = np.ones(1 << 20, np.uint8)
+    node = C.c_int()
+    assert L.ma_host_numa_node(a.ctypes.data, C.byref(node)) == 0 and node.value >= -1
+    assert L.ma_host_place(a.ctypes.data, a.nbytes) == 0
+    if not torch.cuda.is_available():
+        assert L.ma_device_numa_node(C.byref(node)) == 101

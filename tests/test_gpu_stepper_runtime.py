@@ -226,3 +226,22 @@ def test_fused_exchange_single_rank_in_a_graph():
     assert not x.timed_out()
     graph.close()
     x.close()
+
+
+def test_registered_host_memory_sits_on_the_gpus_numa_node():
+    """On a multi-socket host the pages of a registered buffer are placed on
+    the NUMA node of the GPU's PCIe root (ma_host_register); on one node the
+    query still answers."""
+    import ctypes as C
+    import os
+
+    dev_node, page_node = C.c_int(), C.c_int()
+    mab.capi.check(mab.capi.lib().ma_device_numa_node(C.byref(dev_node)))
+    buf = mab.aligned_host_buffer(64 << 20, register=True)
+    mab.capi.check(mab.capi.lib().ma_host_numa_node(buf.ctypes.data, C.byref(page_node)))
+    nodes = len([d for d in os.listdir("/sys/devices/system/node") if d.startswith("node")])
+    if nodes > 1 and dev_node.value >= 0:
+        assert page_node.value == dev_node.value
+    else:
+        assert page_node.value >= -1
+    mab.host_unregister(buf)
