@@ -306,6 +306,8 @@ MA_API int ma_stepper_set_state(ma_stepper* s, float scale, uint32_t clean_steps
  * Loss scale, skip flag and t live on the device, so one graph serves every
  * later step; `reserve_steps` sizes the bias-correction table the graph
  * holds (a launch beyond it fails with MA_ERR_LIFECYCLE: capture again).
+ * The peer-memory collectives (check_xchg, reduce_scatter,
+ * apply_allgather) keep their epoch on the device and replay correctly too.
  * Calls that synchronise with the host (apply_streamed / apply_swapped,
  * state, set_state) cannot be captured. */
 typedef struct ma_graph ma_graph;
