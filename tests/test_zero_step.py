@@ -174,3 +174,56 @@ def test_fused_zero_step_single_process():
         assert np.array_equal(res["W"], want["w"])
         for k in "pmv":
             assert np.array_equal(res[k].view(np.uint32), want[k].view(np.uint32)), k
+
+
+def test_fused_zero_step_single_process_in_a_graph():
+    """The same world-1 ZeRO step captured once as a CUDA graph (entry
+    barrier, K4 + exit barrier / flag OR, K2 + all-gather barriers, scaler)
+    and replayed every step: the exchange epochs live on the device, so the
+    replays equal the eager run and the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    import paper_2505_23254_b200 as mab
+
+    want = oracle_run(1)
+    dev = torch.device("cuda", 0)
+    G = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)
+    W = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)
+    p = torch.empty(N_TOTAL, dtype=torch.float32, device=dev)
+    mab.gen_seeded_weights(p, W, seed=SEED)
+    m = torch.zeros(N_TOTAL, dtype=torch.float32, device=dev)
+    v = torch.zeros(N_TOTAL, dtype=torch.float32, device=dev)
+    gp = torch.empty(N_TOTAL, dtype=torch.bfloat16, device=dev)
+    one = lambda b: [b]  # noqa: E731
+    rs = mab.api.GradReduceScatter(1, 0, G, one)
+    ag = mab.api.GradReduceScatter(1, 0, W, one)
+    st = mab.Stepper(mab.AdamHyper(**HYP), 65536.0, 2000, "bf16", "bf16", device=dev)
+    groups = [(p[o:o + SUBGROUP], m[o:o + SUBGROUP], v[o:o + SUBGROUP], gp[o:o + SUBGROUP],
+               W[o:o + SUBGROUP]) for o in range(0, N_TOTAL, SUBGROUP)]
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+
+    def chain():
+        st.reduce_scatter(rs, 0, N_TOTAL, gp, post_scale=1.0, stream=stream)
+        st.apply_allgather(groups, ag, stream=stream)
+        st.finish(stream=stream)
+
+    graph = st.capture(chain, stream, reserve_steps=64)
+    for s in range(STEPS):
+        stream.synchronize()
+        scale = st.state()["scale"]
+        G.copy_(torch.from_numpy(rank_grads(0, s, scale).view(np.int16)).to(dev)
+                .view(torch.bfloat16))
+        torch.cuda.current_stream().synchronize()
+        graph.launch(stream)
+    stream.synchronize()
+    of, sc = st.history()
+    assert of.astype(bool).tolist() == want["overflow"]
+    assert sc.tolist() == want["scale"]
+    assert np.array_equal(W.view(torch.int16).cpu().numpy().view(np.uint16), want["w"])
+    for k, t in zip("pmv", (p, m, v)):
+        assert np.array_equal(t.cpu().numpy().view(np.uint32), want[k].view(np.uint32)), k
+    graph.close()
+    rs.close()
+    ag.close()
+    st.close()
