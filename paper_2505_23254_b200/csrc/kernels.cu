@@ -609,6 +609,36 @@ __device__ __forceinline__ void update_slot(const Seg& sg, uint64_t e, Slot4& s,
     }
 }
 
+// The fast half of update_slot for the deferred K2 (A/B variant 19): true
+// and stored when the slot passes the guard (incl. the cold second chance),
+// false — nothing stored — otherwise; the caller lists the slot for the
+// CTA's deferred phase (k2_oneshot DEFER).
+template <int GK, int WK>
+__device__ __forceinline__ bool update_slot_fast(const Seg& sg, uint64_t e, const Slot4& s,
+                                                 const AdamConsts& c, const StepScalars& sc) {
+    if (!sc.fast) return false;
+    float g[4];
+    if constexpr (GK == kF32) {
+        g[0] = __uint_as_float(s.g.x); g[1] = __uint_as_float(s.g.y);
+        g[2] = __uint_as_float(s.g.z); g[3] = __uint_as_float(s.g.w);
+    } else {
+        g[0] = widen<GK>(s.g.x & 0xFFFFu); g[1] = widen<GK>(s.g.x >> 16);
+        g[2] = widen<GK>(s.g.y & 0xFFFFu); g[3] = widen<GK>(s.g.y >> 16);
+    }
+    float p[4] = {s.p.x, s.p.y, s.p.z, s.p.w};
+    float m[4] = {s.m.x, s.m.y, s.m.z, s.m.w};
+    float v[4] = {s.v.x, s.v.y, s.v.z, s.v.w};
+    if (!adam_fast<4>(p, m, v, g, c, sc)) return false;
+    __stcs(reinterpret_cast<float4*>(sg.p + e), make_float4(p[0], p[1], p[2], p[3]));
+    __stcs(reinterpret_cast<float4*>(sg.m + e), make_float4(m[0], m[1], m[2], m[3]));
+    __stcs(reinterpret_cast<float4*>(sg.v + e), make_float4(v[0], v[1], v[2], v[3]));
+    if constexpr (WK != kNone) {
+        __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sg.w) + e),
+               make_uint2(narrow2_num<WK>(p[0], p[1]), narrow2_num<WK>(p[2], p[3])));
+    }
+    return true;
+}
+
 template <int GK, int U, int LD = 0>
 __device__ __forceinline__ void load_tile(const Seg& sg, uint64_t lt, Slot4 (&t)[U]) {
 #pragma unroll
@@ -700,12 +730,19 @@ __device__ __forceinline__ uint32_t seg_of_tile(const SegTable& tab, uint64_t t)
     return lo;
 }
 
-template <int GK, int WK, int U, int MATH = 0, int MINB = 1, int AG = 0>
+template <int GK, int WK, int U, int MATH = 0, int MINB = 1, int AG = 0, bool DEFER = false>
 __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, AdamArgs a) {
+    static_assert(!DEFER || (AG == 0 && MATH == 0), "deferred slots: plain K2 only");
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
     const AdamConsts c = a.c;
     const uint64_t t = blockIdx.x;
+    __shared__ uint32_t dlist[DEFER ? U * kK2Threads : 1];
+    __shared__ uint32_t dn;
+    if constexpr (DEFER) {
+        if (threadIdx.x == 0) dn = 0;
+        __syncthreads();
+    }
     if (t < tab.total_tiles) {
         const Seg& sg = tab.seg[seg_of_tile(tab, t)];
         const uint64_t lt = t - sg.tile_begin;
@@ -729,8 +766,42 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, Ada
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (full || j0 + u * kK2Threads < nv) {
-                update_slot<GK, WK, MATH, AG>(loc, 4 * u * kK2Threads, cur[u], c, sc, a.peers);
+                if constexpr (DEFER) {
+                    if (!update_slot_fast<GK, WK>(loc, 4 * u * kK2Threads, cur[u], c, sc))
+                        dlist[atomicAdd(&dn, 1u)] = u * kK2Threads + threadIdx.x;
+                } else {
+                    update_slot<GK, WK, MATH, AG>(loc, 4 * u * kK2Threads, cur[u], c, sc, a.peers);
+                }
             }
+        }
+        if constexpr (DEFER) {
+            // listed slots: one per thread, element by element (adam_any)
+            __syncthreads();
+            const uint32_t nd = dn;
+            if (nd == 0) return;
+            const Seg& sd = tab.seg[seg_of_tile(tab, t)];
+            const uint64_t b0 = sd.head + 4 * ((t - sd.tile_begin) * (U * kK2Threads));
+            for (uint32_t d = threadIdx.x; d < nd; d += kK2Threads) {
+                const uint64_t e = b0 + 4ull * dlist[d];
+                float4 p4 = __ldcs(reinterpret_cast<const float4*>(sd.p + e));
+                float4 m4 = __ldcs(reinterpret_cast<const float4*>(sd.m + e));
+                float4 v4 = __ldcs(reinterpret_cast<const float4*>(sd.v + e));
+                float g[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) g[k] = load_grad1<GK>(sd.g, e + k);
+                adam_any(p4.x, m4.x, v4.x, g[0], c, sc);
+                adam_any(p4.y, m4.y, v4.y, g[1], c, sc);
+                adam_any(p4.z, m4.z, v4.z, g[2], c, sc);
+                adam_any(p4.w, m4.w, v4.w, g[3], c, sc);
+                __stcs(reinterpret_cast<float4*>(sd.p + e), p4);
+                __stcs(reinterpret_cast<float4*>(sd.m + e), m4);
+                __stcs(reinterpret_cast<float4*>(sd.v + e), v4);
+                if constexpr (WK != kNone) {
+                    __stcs(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(sd.w) + e),
+                           make_uint2(narrow2<WK>(p4.x, p4.y), narrow2<WK>(p4.z, p4.w)));
+                }
+            }
+            return;
         }
         // peer stores reach system scope before the exit barrier's release
         if constexpr (AG != 0) __threadfence_system();
@@ -2028,6 +2099,8 @@ template <int GK, int WK> struct K2Kernel<GK, WK, 16> { static constexpr auto fn
 // exact intrinsics only (no hoisted-guard fast path) — the previous production
 template <int GK, int WK> struct K2Kernel<GK, WK, 17> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 0, 3>; };
 template <int GK, int WK> struct K2Kernel<GK, WK, 18> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 2>; };
+// 19: variant 14 with rejected slots deferred to the CTA's list (no call in the hot loop)
+template <int GK, int WK> struct K2Kernel<GK, WK, 19> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 0, 1, 0, true>; };
 
 template <int GK, int WK, int V>
 int k2_occupancy() {
@@ -2060,6 +2133,7 @@ void k2_variants(int variant, F&& f) {
             case 16: f(std::integral_constant<int, 16>{}); return;
             case 17: f(std::integral_constant<int, 17>{}); return;
             case 18: f(std::integral_constant<int, 18>{}); return;
+            case 19: f(std::integral_constant<int, 19>{}); return;
             default: break;
         }
     }
@@ -2115,7 +2189,7 @@ int k2_effective_variant(int gk, int wk, int variant) {
     return v;
 }
 
-bool k2_variant_oneshot(int variant) { return variant >= 13 && variant <= 18; }
+bool k2_variant_oneshot(int variant) { return variant >= 13 && variant <= 19; }
 
 void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
     if (is_tma(variant)) {
