@@ -424,13 +424,17 @@ class Stepper:
         with StepGraph.launch().  Nothing executes during the capture."""
         sp = _stream_ptr(stream)
         check(capi.lib().ma_stepper_graph_begin(self._h, reserve_steps, sp))
+        g = C.c_void_p()
         try:
             with torch.cuda.stream(stream):
                 fn()
-        finally:
-            g = C.c_void_p()
-            st = capi.lib().ma_stepper_graph_end(self._h, sp, C.byref(g))
-        check(st)
+        except BaseException:
+            # end the capture (the stream must not stay in capture mode) and
+            # drop the partial graph
+            if capi.lib().ma_stepper_graph_end(self._h, sp, C.byref(g)) == 0 and g:
+                capi.lib().ma_graph_destroy(g)
+            raise
+        check(capi.lib().ma_stepper_graph_end(self._h, sp, C.byref(g)))
         return StepGraph(g, self)
 
     def step(self, grads_list, groups, allreduce=None, stream=None):

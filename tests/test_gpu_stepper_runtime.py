@@ -245,3 +245,22 @@ def test_registered_host_memory_sits_on_the_gpus_numa_node():
     else:
         assert page_node.value >= -1
     mab.host_unregister(buf)
+
+
+def test_failed_capture_leaves_the_stepper_usable():
+    """An exception inside the captured function ends the capture and drops
+    the partial graph; the stepper then steps eagerly as before."""
+    ref = oracle(3)
+    r = Run()
+    stream = torch.cuda.Stream()
+
+    def bad():
+        r.st.check(r.g, stream=stream)
+        raise RuntimeError("user code failed mid-capture")
+
+    with pytest.raises(RuntimeError):
+        r.st.capture(bad, stream)
+    for s in range(3):
+        r.produce(s)
+        r.st.step([r.g], r.groups)
+    same(r, ref)
