@@ -14,7 +14,10 @@ cast working weights are equal BIT FOR BIT, NaN payloads included:
     the step is not skipped (the check tests the stored gradients), m and v
     become infinite and p NaN, and the NaN state then propagates for several
     more steps;
-  * eps = 0 with v = 0: 0/0 in mh / den.
+  * eps = 0 with v = 0: 0/0 in mh / den;
+  * the offloaded pipelines (configs[3] streamed from registered host memory,
+    configs[4] through the O_DIRECT swap store) with non-finite and cold
+    state: what lands back in host memory / the store equals the reference.
 """
 import numpy as np
 import pytest
@@ -171,3 +174,79 @@ def test_eps_zero_zero_variance():
         assert np.array_equal(u32(got), exp.view(np.uint32))
     assert np.array_equal(w.cpu().numpy().view(np.uint16), ora.cast_from_f32(ref[0], "f16"))
     assert (w.cpu().numpy().view(np.uint16)[1::3] == 0xFE00).all()
+
+
+def _adversarial_state_finite_grads(seed, n):
+    """Adversarial p/m/v (NaN payloads, infinities, negative v, cold zeros)
+    with FINITE gradients, so the step is not skipped and the non-finite
+    values reach K2 inside the offloaded pipelines."""
+    p, m, v, _ = ni.state(seed, n, p_special=0.3)
+    rng = np.random.default_rng(seed + 1)
+    g = (rng.standard_normal(n) * 1024).astype(np.float32)
+    g[rng.random(n) < 0.2] = 0.0
+    return p, m, v, ora.cast_from_f32(g, "bf16")
+
+
+@pytest.mark.parametrize("slots,slot_elems", [(2, 8192), (3, 30000)])
+def test_streamed_path_adversarial_state_equals_reference(slots, slot_elems):
+    """configs[3]'s path (p/m/v in registered host memory, staged through
+    device slots) with non-finite / cold state: p/m/v and the bf16 working
+    weights equal the reference bit for bit."""
+    n, sub = 70_001, 30_000
+    p, m, v, g16 = _adversarial_state_finite_grads(5, n)
+    h = ora.hyper(lr=1e-3, weight_decay=0.01)
+    ref = [x.copy() for x in (p, m, v)]
+    ora.ref_adam_step_fp32(*ref, ora.widen(g16, "bf16"), 1, h, 65536.0)
+    host = [torch.from_numpy(x.copy()).pin_memory() for x in (p, m, v)]
+    gd = torch.from_numpy(g16.view(np.int16)).to(DEV).view(torch.bfloat16)
+    w = torch.zeros(n, dtype=torch.bfloat16, device=DEV)
+    st = mab.Stepper(mab.AdamHyper(lr=1e-3, weight_decay=0.01), 65536.0, 2000, "bf16", "bf16")
+    groups = [(host[0][o:o + sub], host[1][o:o + sub], host[2][o:o + sub], gd[o:o + sub],
+               w[o:o + sub]) for o in range(0, n, sub)]
+    staging = torch.empty(3 * slots * slot_elems, dtype=torch.float32, device=DEV)
+    assert not st.apply_streamed(groups, staging, slot_elems, slots)
+    st.finish()
+    torch.cuda.synchronize()
+    for got, want, name in zip(host, ref, "pmv"):
+        assert np.array_equal(got.numpy().view(np.uint32), want.view(np.uint32)), name
+    assert np.array_equal(w.view(torch.int16).cpu().numpy().view(np.uint16),
+                          ora.cast_from_f32(ref[0], "bf16"))
+
+
+def test_swapped_path_adversarial_state_equals_reference(tmp_path):
+    """configs[4]'s path (master/m/v in the O_DIRECT swap store, read ahead
+    into registered host slots, through HBM, written back) with non-finite /
+    cold state: what the store holds afterwards equals the reference."""
+    n, sub, slot = 50_003, 20_000, 20_480
+    p, m, v, g16 = _adversarial_state_finite_grads(9, n)
+    h = ora.hyper(lr=1e-3, weight_decay=0.01)
+    ref = [x.copy() for x in (p, m, v)]
+    ora.ref_adam_step_fp32(*ref, ora.widen(g16, "bf16"), 1, h, 65536.0)
+    store = mab.DirectIoEngine(mab.DirectIoEngine.create_virtual_devices(str(tmp_path), 2,
+                                                                         8 << 20))
+    buf = mab.aligned_host_buffer(slot * 4)
+    gd = torch.from_numpy(g16.view(np.int16)).to(DEV).view(torch.bfloat16)
+    w = torch.zeros(n, dtype=torch.bfloat16, device=DEV)
+    groups = []
+    for k, o in enumerate(range(0, n, sub)):
+        ln = min(sub, n - o)
+        keys = tuple(f"{t}.g{k}" for t in ("master", "m", "v"))
+        for key, arr in zip(keys, (p, m, v)):
+            buf.view(np.float32)[:ln] = arr[o:o + ln]
+            store.write_tensor(key, buf, ln * 4)
+        groups.append((keys, gd[o:o + ln], w[o:o + ln]))
+    hstage = mab.aligned_host_buffer(2 * 3 * slot * 4, register=True)
+    dstage = torch.empty(3 * 2 * slot, dtype=torch.float32, device=DEV)
+    st = mab.Stepper(mab.AdamHyper(lr=1e-3, weight_decay=0.01), 65536.0, 2000, "bf16", "bf16")
+    assert not st.apply_swapped(store, groups, hstage, 2, dstage, 2, slot)
+    st.finish()
+    torch.cuda.synchronize()
+    for k, o in enumerate(range(0, n, sub)):
+        ln = min(sub, n - o)
+        for key, want, name in zip(groups[k][0], ref, "pmv"):
+            store.read_tensor(key, buf)
+            got = buf.view(np.float32)[:ln]
+            assert np.array_equal(got.view(np.uint32), want[o:o + ln].view(np.uint32)), (k, name)
+    assert np.array_equal(w.view(torch.int16).cpu().numpy().view(np.uint16),
+                          ora.cast_from_f32(ref[0], "bf16"))
+    store.close()
