@@ -186,14 +186,18 @@ def cpu_reference_run(n, steps, warmup, threads):
 
 
 def cpu_model():
+    """lscpu's model name and socket count (record both)."""
+    model, sockets = "unknown", None
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
         for line in out.splitlines():
             if line.startswith("Model name"):
-                return line.split(":", 1)[1].strip()
+                model = line.split(":", 1)[1].strip()
+            elif line.startswith("Socket(s)"):
+                sockets = line.split(":", 1)[1].strip()
     except Exception:
         pass
-    return "unknown"
+    return model if sockets is None else f"{model}, {sockets} socket(s)"
 
 
 def reference_swapped_run(args, steps, warmup, threads, groups=2):
@@ -587,11 +591,11 @@ def ours(args, n, rank, world, local_rank):
         line["cfg3_check"] = check
     if world == 1 and not args.no_cpu_baseline and not inject:
         threads = os.cpu_count() or 1
-        cb = cpu_reference_run(min(args.cpu_sample, n), 3, 1, threads)
+        cb = cpu_reference_run(min(args.cpu_sample, n), 5, 1, threads)  # >= 5
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         # the reference's path at 1 worker too (the reference's
         # simulator calls adam_step_fp32 with its default workers = 1)
-        one = cpu_reference_run(min(args.cpu_sample, n), 1, 0, 1)
+        one = cpu_reference_run(min(args.cpu_sample, n), 5, 1, 1)
         line["cpu_baseline"]["single_thread"] = {"value": one["value"], "unit": "params/s",
                                                  "cores": 1}
         line["host"] = {"cpu": cpu_model(), "nproc": threads}
