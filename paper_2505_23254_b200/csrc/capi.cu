@@ -470,8 +470,9 @@ struct ma_stepper {
     int w_dtype = MA_DT_BF16;
     ma::StepDev* d_st = nullptr;
     ma::StepLog* d_log = nullptr;
-    float2* d_bc = nullptr;
+    float2* d_bc = nullptr;  // bias corrections of t = bc_first .. bc_first + bc_cap - 1
     uint64_t bc_cap = 0;
+    uint64_t bc_first = 1;
     uint64_t issued = 0;  // finish calls enqueued since creation / the last set_state
     uint64_t t_base = 0;  // updates at creation / the last set_state (resumed runs)
     cudaStream_t last = nullptr;
@@ -497,22 +498,39 @@ struct ma_stepper {
 
 namespace {
 
-void stepper_grow_bc(ma_stepper* s, uint64_t need) {
-    if (need <= s->bc_cap) return;
-    uint64_t cap = std::max<uint64_t>(s->bc_cap ? s->bc_cap * 2 : 65536, need);
-    std::vector<float2> host(cap);
-    for (uint64_t t = 1; t <= cap; ++t) {
-        bias_corrections(t, s->h.beta1, s->h.beta2, &host[t - 1].x, &host[t - 1].y);
-    }
+// The bias-correction table is a window of t values: finish / prepare read
+// the entry of t = updates + 1, and the host only bounds `updates` (it is
+// t_base + the number of applied steps, and skips are decided on the
+// device): t_base <= updates <= t_base + issued.  The window must cover
+// [t_base + 1, last_t]; when it does not, the actual updates is read back
+// (one synchronisation, every ~65536 steps) and a fresh window starts
+// there, so the table's size never depends on how far training has gone
+// (a run resumed at t = 10^9 holds the same 0.5 MB as a fresh one).
+void stepper_cover_bc(ma_stepper* s, uint64_t last_t) {
+    if (s->d_bc && s->bc_first <= s->t_base + 1 && last_t < s->bc_first + s->bc_cap) return;
     if (s->capturing)
-        fail(MA_ERR_LIFECYCLE, "bias-correction table exhausted during graph capture");
+        fail(MA_ERR_LIFECYCLE, "bias-correction window exhausted during graph capture");
+    CK(cudaDeviceSynchronize());  // `updates` below is final
+    unsigned long long updates = 0;
+    CK(cudaMemcpy(&updates, &s->d_st->updates, sizeof updates, cudaMemcpyDeviceToHost));
+    // exact now: issued keeps counting the finishes after t_base
+    const uint64_t applied = updates - std::min<uint64_t>(updates, s->t_base);
+    s->issued -= std::min<uint64_t>(s->issued, applied);
+    last_t = std::max<uint64_t>(last_t, updates + 2);
+    s->t_base = updates;
+    const uint64_t first = updates + 1;
+    const uint64_t cap = (last_t - first + 1) + 65536;
+    std::vector<float2> host(cap);
+    for (uint64_t k = 0; k < cap; ++k)
+        bias_corrections(first + k, s->h.beta1, s->h.beta2, &host[k].x, &host[k].y);
     float2* fresh = nullptr;
     CK(cudaMalloc(&fresh, cap * sizeof(float2)));
     CK(cudaMemcpy(fresh, host.data(), cap * sizeof(float2), cudaMemcpyHostToDevice));
-    // in-flight steps and captured graphs may still read the old table: it
-    // is retired, not freed, until the stepper is destroyed
+    // captured graphs may still read the old window: retired, not freed,
+    // until the stepper is destroyed
     if (s->d_bc) s->retired.push_back(s->d_bc);
     s->d_bc = fresh;
+    s->bc_first = first;
     s->bc_cap = cap;
 }
 
@@ -757,8 +775,8 @@ int ma_stepper_create(const ma_adam_hyper* h, float init_scale, uint32_t growth_
             init.growth_interval = growth_interval;
             CK(cudaMemcpy(s->d_st, &init, sizeof init, cudaMemcpyHostToDevice));
             CK(cudaMemset(s->d_log, 0, sizeof(ma::StepLog) * ma::kHistory));
-            stepper_grow_bc(s, 1024);
-            ma::launch_step_prepare(s->d_st, s->d_bc, s->c, nullptr);
+            stepper_cover_bc(s, 2);
+            ma::launch_step_prepare(s->d_st, s->d_bc, s->bc_first, s->c, nullptr);
             CK(cudaGetLastError());
             CK(cudaDeviceSynchronize());
         } catch (...) {
@@ -1021,7 +1039,6 @@ int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t co
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        stepper_grow_bc(s, s->t_base + s->issued + 2);  // t <= updates + 1, +1 prepared
         ma::AdamArgs a{};
         a.c = s->c;
         a.skip = &s->d_st->flag;
@@ -1037,7 +1054,6 @@ int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups, u
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        stepper_grow_bc(s, s->t_base + s->issued + 2);
         ma::AdamArgs a{};
         a.c = s->c;
         a.skip = &s->d_st->flag;
@@ -1122,7 +1138,6 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
     if (skipped) *skipped = flag ? 1 : 0;
     s->last = cs;
     if (flag) return;
-    stepper_grow_bc(s, s->t_base + s->issued + 2);
     int dev = 0;
     CK(cudaGetDevice(&dev));
     ma::swp::Engine* engp = e ? e->e : nullptr;
@@ -1429,8 +1444,9 @@ int ma_stepper_finish_async(ma_stepper* s, void* stream) {
     NvtxRange nvtx_range("ma_stepper_finish_async");
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
-        stepper_grow_bc(s, s->t_base + s->issued + 2);  // the next update's scalars
-        ma::launch_step_finish(s->d_st, s->d_log, s->d_bc, s->c, as_stream(stream));
+        stepper_cover_bc(s, s->t_base + s->issued + 2);  // the next update's scalars
+        ma::launch_step_finish(s->d_st, s->d_log, s->d_bc, s->bc_first, s->c,
+                               as_stream(stream));
         CK(cudaGetLastError());
         s->issued += 1;
         s->last = as_stream(stream);
@@ -1471,8 +1487,8 @@ int ma_stepper_set_state(ma_stepper* s, float scale, uint32_t clean_steps, uint6
         CK(cudaMemcpy(s->d_st, &st, sizeof st, cudaMemcpyHostToDevice));
         s->t_base = updates;
         s->issued = 0;
-        stepper_grow_bc(s, updates + 2);
-        ma::launch_step_prepare(s->d_st, s->d_bc, s->c, nullptr);
+        stepper_cover_bc(s, updates + 2);
+        ma::launch_step_prepare(s->d_st, s->d_bc, s->bc_first, s->c, nullptr);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
     });
@@ -1910,7 +1926,6 @@ int ma_stepper_apply_allgather_async(ma_stepper* s, const ma_subgroup* groups, u
                                                   "rank's shared weight buffer");
         }
         const cudaStream_t st = as_stream(stream);
-        stepper_grow_bc(s, s->t_base + s->issued + 2);
         ma::AdamArgs a{};
         a.c = s->c;
         a.skip = &s->d_st->flag;
@@ -1944,7 +1959,8 @@ struct ma_graph {
     ma_stepper* s = nullptr;
     cudaGraphExec_t exec = nullptr;
     uint64_t finishes = 0;  // finish calls per replay
-    uint64_t bc_cap = 0;    // capacity of the table the graph's kernels read
+    uint64_t bc_first = 0;  // the window of bias corrections the graph's kernels read
+    uint64_t bc_cap = 0;
 };
 
 extern "C" {
@@ -1954,7 +1970,7 @@ int ma_stepper_graph_begin(ma_stepper* s, uint64_t reserve_steps, void* stream) 
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (!stream) fail(MA_ERR_INVALID_ARGUMENT, "graph capture needs a non-default stream");
         if (s->capturing) fail(MA_ERR_LIFECYCLE, "graph capture already in progress");
-        stepper_grow_bc(s, s->t_base + s->issued + reserve_steps + 2);
+        stepper_cover_bc(s, s->t_base + s->issued + reserve_steps + 2);
         CK(cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal));
         s->capturing = true;
         s->capture_issued = s->issued;
@@ -1974,6 +1990,7 @@ int ma_stepper_graph_end(ma_stepper* s, void* stream, ma_graph** out) {
         auto* g = new ma_graph();
         g->s = s;
         g->finishes = finishes;
+        g->bc_first = s->bc_first;
         g->bc_cap = s->bc_cap;
         const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
         cudaGraphDestroy(graph);
@@ -1989,8 +2006,9 @@ int ma_graph_launch(ma_graph* g, void* stream) {
     return guarded([&] {
         if (!g) fail(MA_ERR_INVALID_ARGUMENT, "null graph");
         ma_stepper* s = g->s;
-        if (s->t_base + s->issued + g->finishes + 1 > g->bc_cap)
-            fail(MA_ERR_LIFECYCLE, "graph's bias-correction table exhausted: capture again");
+        if (s->t_base + 1 < g->bc_first ||
+            s->t_base + s->issued + g->finishes + 1 >= g->bc_first + g->bc_cap)
+            fail(MA_ERR_LIFECYCLE, "graph's bias-correction window exhausted: capture again");
         CK(cudaGraphLaunch(g->exec, as_stream(stream)));
         s->issued += g->finishes;
         s->last = as_stream(stream);

@@ -1509,8 +1509,9 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
 
 // ============================================================== step finish
 // The next update's scalars (t = updates + 1, current scale) into StepDev.
-__device__ void step_prepare(StepDev* st, const float2* bc_table, const AdamConsts c) {
-    const float2 bc = bc_table[st->updates];
+__device__ void step_prepare(StepDev* st, const float2* bc_table, unsigned long long bc_first,
+                             const AdamConsts c) {
+    const float2 bc = bc_table[st->updates + 1ull - bc_first];  // t = updates + 1
     StepScalars s;
     scalars_from(st->scale, bc.x, bc.y, c, s);
     st->inv_scale = s.scale_pow2 ? s.inv_scale : 0.0f;
@@ -1521,15 +1522,16 @@ __device__ void step_prepare(StepDev* st, const float2* bc_table, const AdamCons
     st->mode = (s.scale_pow2 ? 1u : 0u) | (s.fast ? 2u : 0u);
 }
 
-__global__ void k_step_prepare(StepDev* st, const float2* bc_table, const AdamConsts c) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) step_prepare(st, bc_table, c);
+__global__ void k_step_prepare(StepDev* st, const float2* bc_table, unsigned long long bc_first,
+                               const AdamConsts c) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) step_prepare(st, bc_table, bc_first, c);
 }
 
 // LossScaler::on_overflow / on_clean_step (optimizer.hpp:24-34) and the
 // update counter (simulator.cpp:438-444,491); re-arms the flag and prepares
 // the next update's scalars.
 __global__ void k_step_finish(StepDev* st, StepLog* log, const float2* bc_table,
-                              const AdamConsts c) {
+                              unsigned long long bc_first, const AdamConsts c) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const uint32_t of = st->flag != 0u;
     if (of) {
@@ -1547,7 +1549,7 @@ __global__ void k_step_finish(StepDev* st, StepLog* log, const float2* bc_table,
     st->steps += 1ull;
     st->last_overflow = of;
     st->flag = 0u;
-    step_prepare(st, bc_table, c);
+    step_prepare(st, bc_table, bc_first, c);
 }
 
 // ============================================================== generators
@@ -2333,14 +2335,14 @@ void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsi
     k3_dispatch(gk, variant, [&](auto fn) { fn<<<grid, kK2Threads, 0, st>>>(tab, a); });
 }
 
-void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, const AdamConsts& c,
-                        cudaStream_t s) {
-    k_step_finish<<<1, 32, 0, s>>>(st, log, bc_table, c);
+void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, uint64_t bc_first,
+                        const AdamConsts& c, cudaStream_t s) {
+    k_step_finish<<<1, 32, 0, s>>>(st, log, bc_table, bc_first, c);
 }
 
-void launch_step_prepare(StepDev* st, const float2* bc_table, const AdamConsts& c,
-                         cudaStream_t s) {
-    k_step_prepare<<<1, 32, 0, s>>>(st, bc_table, c);
+void launch_step_prepare(StepDev* st, const float2* bc_table, uint64_t bc_first,
+                         const AdamConsts& c, cudaStream_t s) {
+    k_step_prepare<<<1, 32, 0, s>>>(st, bc_table, bc_first, c);
 }
 
 void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,

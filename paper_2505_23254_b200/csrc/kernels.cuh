@@ -151,10 +151,11 @@ int rs_units_for(int sk, uint32_t nsrc);
 // all ranks meet at the exchange object's next epoch (one warp; peers'
 // slots over NVLink); a peer missing for MA_PEER_TIMEOUT_S stops every rank
 void launch_peer_barrier(const XchgDev* x, cudaStream_t st);
-void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, const AdamConsts& c,
-                        cudaStream_t s);
-void launch_step_prepare(StepDev* st, const float2* bc_table, const AdamConsts& c,
-                         cudaStream_t s);
+// bc_table holds (1-b1^t, 1-b2^t) for t = bc_first, bc_first + 1, ...
+void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, uint64_t bc_first,
+                        const AdamConsts& c, cudaStream_t s);
+void launch_step_prepare(StepDev* st, const float2* bc_table, uint64_t bc_first,
+                         const AdamConsts& c, cudaStream_t s);
 void launch_gen_weights(int wk, float* p, uint16_t* w, uint64_t n, uint64_t base, uint64_t seed,
                         unsigned grid, cudaStream_t st);
 void launch_gen_grads(int gk, int wk, void* g, const uint16_t* w, uint64_t n, uint64_t base,

@@ -264,3 +264,62 @@ def test_failed_capture_leaves_the_stepper_usable():
         r.produce(s)
         r.st.step([r.g], r.groups)
     same(r, ref)
+
+
+def test_resume_at_huge_t_keeps_a_small_window():
+    """A run resumed at t = 10^9 (OptimizerState::step_t) continues exactly:
+    the bias-correction window starts at the restored t instead of holding
+    every t from 1 (which would be 8 GB here)."""
+    n = 20_011
+    rng = np.random.default_rng(2)
+    p0 = (rng.standard_normal(n) * 0.1).astype(np.float32)
+    m0 = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    v0 = (np.abs(rng.standard_normal(n)) * 1e-6).astype(np.float32)
+    t0 = 10 ** 9
+    h = ora.hyper(**HYP)
+    ref = [p0.copy(), m0.copy(), v0.copy()]
+    dev = torch.device("cuda", 0)
+    p, m, v = (torch.from_numpy(x.copy()).to(dev) for x in (p0, m0, v0))
+    w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    st = mab.Stepper(mab.AdamHyper(**HYP), 1024.0, 2000, "bf16", "bf16")
+    st.set_state(1024.0, 5, t0)
+    for s in range(4):
+        gs = ora.cast_from_f32((rng.standard_normal(n) * 1024).astype(np.float32), "bf16")
+        g.view(torch.int16).copy_(torch.from_numpy(gs.view(np.int16)))
+        st.step([g], [(p, m, v, g, w)])
+        ora.adam_step(*ref, ora.widen(gs, "bf16"), t0 + s + 1, h, 1024.0)
+    torch.cuda.synchronize()
+    for got, want, name in zip((p, m, v), ref, "pmv"):
+        assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32)), name
+    assert st.state()["updates"] == t0 + 4
+
+
+def test_bias_window_rolls_over_past_65536_steps():
+    """70 000 eager steps on a small partition: the bias-correction window
+    (65 536 entries) is re-based once on the way; decisions, scales and the
+    final state equal the oracle's 70 000-step run bit for bit."""
+    n, steps = 4099, 70_000
+    ref = ora.train(n, steps, SEED, g_kind="bf16", w_kind="bf16", hyp=ora.hyper(**HYP),
+                    scale=65536.0, growth=2000)
+    dev = torch.device("cuda", 0)
+    p = torch.empty(n, dtype=torch.float32, device=dev)
+    m = torch.zeros(n, dtype=torch.float32, device=dev)
+    v = torch.zeros(n, dtype=torch.float32, device=dev)
+    w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    mab.gen_seeded_weights(p, w, seed=SEED)
+    st = mab.Stepper(mab.AdamHyper(**HYP), 65536.0, 2000, "bf16", "bf16")
+    groups = mab.Stepper.subgroups([(p, m, v, g, w)], "bf16", "bf16")
+    for s in range(steps):
+        mab.gen_pseudo_grads(g, w, step=s, seed=SEED, d_scale=st.scale_t)
+        st.check(g)
+        st.apply(groups)
+        st.finish()
+    torch.cuda.synchronize()
+    of, sc = st.history(cap=steps)
+    assert of.tolist() == ref["overflow"].astype(bool)[-of.size:].tolist()
+    assert sc.tolist() == ref["scale_after"][-sc.size:].tolist()
+    for k, t in zip("pmv", (p, m, v)):
+        assert np.array_equal(t.cpu().numpy().view(np.uint32), ref[k].view(np.uint32)), k
+    assert st.state()["updates"] == int(ref["updates"]) > 65_536
