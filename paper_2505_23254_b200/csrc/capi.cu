@@ -226,9 +226,12 @@ void numa_place_for_device(void* ptr, uint64_t bytes) {
 }
 
 // ------------------------------------------------------------ K1 launch
+// keep_tail: a stepper check whose gradients K2 reads next — the buffer's
+// last MA_K1_KEEP_MB (default 32 MiB) are loaded under an L2 evict_last
+// policy so K2's last tiles find them in L2 (kernels.cu k1_load).
 void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* first,
                uint64_t index_base, bool early_exit, cudaStream_t st,
-               const ma::XchgDev* xchg = nullptr) {
+               const ma::XchgDev* xchg = nullptr, bool keep_tail = false) {
     if (n == 0 && !xchg) return;  // an empty rank still takes part in the exchange
     const DeviceInfo d = device_info();
     const uint32_t es = static_cast<uint32_t>(elem_bytes(dt));
@@ -247,6 +250,11 @@ void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* f
     a.kind = dt;
     a.elem_bytes = es;
     a.early_exit = early_exit ? 1 : 0;
+    static const uint64_t keep_vecs = [] {
+        const char* e = std::getenv("MA_K1_KEEP_MB");  // A/B only
+        return (e ? std::strtoull(e, nullptr, 10) : 32ull) << 16;  // MiB / 16 B
+    }();
+    a.keep_from = keep_tail ? a.nvec - std::min<uint64_t>(a.nvec, keep_vecs) : a.nvec;
     // MA_K1_UNROLL / MA_K1_CTAS_PER_SM: A/B knobs (defaults 4 and 8)
     static const int unroll = [] {
         const char* e = std::getenv("MA_K1_UNROLL");
@@ -347,7 +355,7 @@ uint64_t oneshot_grid(const ma::SegTable& tab, int vec, uint64_t scalar_elems, u
 void launch_k2(const ma_subgroup* groups, uint32_t count, int gdt, int wdt, const ma::AdamArgs& a,
                cudaStream_t st, bool allgather = false) {
     const DeviceInfo d = device_info();
-    // the fused all-gather runs in the production one-shot shape (variant 14)
+    // the fused all-gather runs in the production one-shot tile shape (U = 4)
     const int variant = allgather ? ma::kK2DefaultVariant
                                   : ma::k2_effective_variant(gdt, wdt, k2_variant());
     int vec, tile_vectors;
@@ -807,7 +815,8 @@ int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void* strea
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (n && !g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
-        launch_k1(g, n, s->g_dtype, &s->d_st->flag, nullptr, 0, true, as_stream(stream));
+        launch_k1(g, n, s->g_dtype, &s->d_st->flag, nullptr, 0, true, as_stream(stream), nullptr,
+                  true);
         s->last = as_stream(stream);
     });
 }
@@ -840,7 +849,7 @@ int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, 
             CK(cudaEventRecord(landed, cs));
             CK(cudaStreamWaitEvent(st, landed, 0));
             launch_k1(static_cast<uint8_t*>(dev_g) + off * es, len, s->g_dtype, &s->d_st->flag,
-                      nullptr, 0, true, st);
+                      nullptr, 0, true, st, nullptr, off + len == n);
         }
         s->last = st;
     });
@@ -986,7 +995,7 @@ int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n, ma_xch
         if (n && !g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
         alignas(16) static const uint32_t dummy[4] = {0, 0, 0, 0};  // never read (n == 0)
         launch_k1(n ? g : &dummy, n, s->g_dtype, &s->d_st->flag, nullptr, 0, true,
-                  as_stream(stream), x->d_desc);
+                  as_stream(stream), x->d_desc, true);
         s->last = as_stream(stream);
     });
 }

@@ -13,9 +13,21 @@
 // one-touch state does not thrash L2.
 #include "kernels.cuh"
 
+#include <cstdlib>
 #include <type_traits>
+#include <utility>
 
 namespace ma {
+
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start once every
+// CTA of the previous kernel has executed launch_dependents (or exited);
+// griddepcontrol.wait then blocks until that kernel has completed and its
+// writes are visible.  Both are no-ops without a programmatic dependency.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ============================================================== K1
 // One pass over the raw bits; each thread ORs (w & MASK) + INC over its
@@ -149,8 +161,25 @@ __global__ void k_peer_barrier(const XchgDev* xp) {
 // (6.9 vs 6.2 TB/s for the grid-stride form, tools/layout_probe.cu).  A CTA
 // that starts after the flag is already set skips its loads (the reference's
 // cooperative early exit); with an exchange it still takes part in it.
-template <bool kTrack, int U>
+// K1 load flavour for the vectors from keep_from on (the buffer's last
+// MA_K1_KEEP_MB, default 32 MiB, of a stepper check; keep_from = nvec
+// otherwise): 1 = L2 evict_last policy (production) — those gradients stay
+// in L2 while K2 streams p/m/v through it with evict-first accesses, and K2's
+// last tiles read them from L2 (configs[0]: K2 282.6 -> 274.5 us); A/B:
+// MA_K1_LDK=0 (everything ld.global.cs) / 2 (default caching for the tail).
+template <int LDK>
+__device__ __forceinline__ uint4 k1_load(const uint4* p, uint64_t pol) {
+    if constexpr (LDK == 0) return __ldcs(p);
+    if constexpr (LDK == 2) return *p;  // default (evict_normal) caching
+    uint4 r;
+    asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+    return r;
+}
+
+template <bool kTrack, int U, int LDK = 0>
 __global__ void __launch_bounds__(kK1Threads) k1_oneshot(K1Args a) {
+    pdl_trigger();  // K2 (PDL launch) may be scheduled during K1's last wave
     const ScanWord sw = scan_word(a.kind);
     const unsigned lane = threadIdx.x & 31u;
     const uint32_t per_vec = 16u / a.elem_bytes;
@@ -158,11 +187,17 @@ __global__ void __launch_bounds__(kK1Threads) k1_oneshot(K1Args a) {
     uint32_t acc = 0;
     const bool skip = !kTrack && a.early_exit && *reinterpret_cast<volatile uint32_t*>(a.flag) != 0u;
     if (!skip) {
+        uint64_t pol = 0;
+        if constexpr (LDK == 1) {
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        }
         uint4 q[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t i = first + static_cast<uint64_t>(u) * blockDim.x;
-            q[u] = i < a.nvec ? __ldcs(a.body + i) : make_uint4(0, 0, 0, 0);
+            q[u] = i >= a.nvec ? make_uint4(0, 0, 0, 0)
+                   : (LDK != 0 && i >= a.keep_from) ? k1_load<LDK>(a.body + i, pol)
+                                                    : __ldcs(a.body + i);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -730,13 +765,30 @@ __device__ __forceinline__ uint32_t seg_of_tile(const SegTable& tab, uint64_t t)
     return lo;
 }
 
-template <int GK, int WK, int U, int MATH = 0, int MINB = 1, int AG = 0, bool DEFER = false>
+// PDL (programmatic dependent launch, A/B variants 20/21): 1 = launched
+// while the previous kernel (K1) drains, griddepcontrol.wait before anything
+// else; 2 = the tile's p/m/v/g loads are issued before the wait (only the
+// stores and the skip decision depend on K1; the launch must follow a kernel
+// that writes none of p/m/v/g).
+template <int GK, int WK, int U, int MATH = 0, int MINB = 1, int AG = 0, bool DEFER = false,
+          int PDL = 0, bool REV = false>
 __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, AdamArgs a) {
     static_assert(!DEFER || (AG == 0 && MATH == 0), "deferred slots: plain K2 only");
+    static_assert(PDL == 0 || (AG == 0 && !DEFER), "PDL: plain K2 only");
     StepScalars sc;
-    if (!resolve_step(a, sc)) return;
+    if constexpr (PDL != 0) pdl_trigger();
+    if constexpr (PDL == 1) pdl_wait();
+    // REV (A/B): tiles back to front, so the first tiles read the gradients
+    // K1 touched last (still in L2)
+    const uint64_t t = REV && blockIdx.x < tab.total_tiles ? tab.total_tiles - 1 - blockIdx.x
+                                                           : blockIdx.x;
+    if constexpr (PDL == 2) {
+        if (t >= tab.total_tiles) pdl_wait();
+    }
+    if (PDL != 2 || t >= tab.total_tiles) {
+        if (!resolve_step(a, sc)) return;
+    }
     const AdamConsts c = a.c;
-    const uint64_t t = blockIdx.x;
     __shared__ uint32_t dlist[DEFER ? U * kK2Threads : 1];
     __shared__ uint32_t dn;
     if constexpr (DEFER) {
@@ -762,6 +814,10 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, Ada
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (full || j0 + u * kK2Threads < nv) load_slot<GK>(loc, 4 * u * kK2Threads, cur[u]);
+        }
+        if constexpr (PDL == 2) {
+            pdl_wait();
+            if (!resolve_step(a, sc)) return;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -1532,6 +1588,7 @@ __global__ void k_step_prepare(StepDev* st, const float2* bc_table, unsigned lon
 // the next update's scalars.
 __global__ void k_step_finish(StepDev* st, StepLog* log, const float2* bc_table,
                               unsigned long long bc_first, const AdamConsts c) {
+    pdl_wait();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const uint32_t of = st->flag != 0u;
     if (of) {
@@ -2053,13 +2110,50 @@ __global__ void k_mask_sweep(int kind, unsigned long long* mismatches) {
 }
 
 // ============================================================== launchers
+// Launch as a programmatic dependent of the previous kernel in the stream
+// (the kernel must pdl_wait() before consuming that kernel's results).
+template <typename... P, typename... A>
+void launch_pdl(void (*fn)(P...), unsigned grid, unsigned block, cudaStream_t st, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
+}
+
+int k1_ldk() {
+    static const int v = [] {
+        const char* e = std::getenv("MA_K1_LDK");  // A/B only
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+bool pdl_finish() {
+    static const bool on = [] {
+        const char* e = std::getenv("MA_PDL_FINISH");  // A/B only (0 = plain launch)
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void launch_k1(const K1Args& a, bool track, int unroll, bool oneshot, unsigned grid,
                cudaStream_t st) {
     if (oneshot) {
         if (track) {
             k1_oneshot<true, kK1Unroll><<<grid, kK1Threads, 0, st>>>(a);
+        } else if (k1_ldk() == 0 || a.keep_from >= a.nvec) {
+            k1_oneshot<false, kK1Unroll, 0><<<grid, kK1Threads, 0, st>>>(a);
+        } else if (k1_ldk() == 2) {
+            k1_oneshot<false, kK1Unroll, 2><<<grid, kK1Threads, 0, st>>>(a);
         } else {
-            k1_oneshot<false, kK1Unroll><<<grid, kK1Threads, 0, st>>>(a);
+            k1_oneshot<false, kK1Unroll, 1><<<grid, kK1Threads, 0, st>>>(a);
         }
         return;
     }
@@ -2103,6 +2197,12 @@ template <int GK, int WK> struct K2Kernel<GK, WK, 17> { static constexpr auto fn
 template <int GK, int WK> struct K2Kernel<GK, WK, 18> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 2>; };
 // 19: variant 14 with rejected slots deferred to the CTA's list (no call in the hot loop)
 template <int GK, int WK> struct K2Kernel<GK, WK, 19> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 0, 1, 0, true>; };
+// 20 / 21: variant 14 launched as a programmatic dependent of K1 (wait first /
+// the tile's loads issued before the wait)
+template <int GK, int WK> struct K2Kernel<GK, WK, 20> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 0, 1, 0, false, 1>; };
+template <int GK, int WK> struct K2Kernel<GK, WK, 21> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 0, 1, 0, false, 2>; };
+// 22: variant 14 with the tiles in reverse order (L2 reuse of K1's last gradients)
+template <int GK, int WK> struct K2Kernel<GK, WK, 22> { static constexpr auto fn = k2_oneshot<GK, WK, 4, 0, 1, 0, false, 0, true>; };
 
 template <int GK, int WK, int V>
 int k2_occupancy() {
@@ -2136,6 +2236,9 @@ void k2_variants(int variant, F&& f) {
             case 17: f(std::integral_constant<int, 17>{}); return;
             case 18: f(std::integral_constant<int, 18>{}); return;
             case 19: f(std::integral_constant<int, 19>{}); return;
+            case 20: f(std::integral_constant<int, 20>{}); return;
+            case 21: f(std::integral_constant<int, 21>{}); return;
+            case 22: f(std::integral_constant<int, 22>{}); return;
             default: break;
         }
     }
@@ -2191,7 +2294,7 @@ int k2_effective_variant(int gk, int wk, int variant) {
     return v;
 }
 
-bool k2_variant_oneshot(int variant) { return variant >= 13 && variant <= 19; }
+bool k2_variant_oneshot(int variant) { return variant >= 13 && variant <= 22; }
 
 void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream) {
     if (is_tma(variant)) {
@@ -2239,8 +2342,13 @@ void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs&
         return;
     }
     k2_dispatch(gk, wk, variant, [&](auto G, auto W, auto V) {
-        K2Kernel<decltype(G)::value, decltype(W)::value, decltype(V)::value>::fn
-            <<<grid, kK2Threads, 0, st>>>(tab, a);
+        constexpr int v = decltype(V)::value;
+        auto fn = K2Kernel<decltype(G)::value, decltype(W)::value, v>::fn;
+        if constexpr (v == 20 || v == 21) {
+            launch_pdl(fn, grid, kK2Threads, st, tab, a);
+        } else {
+            fn<<<grid, kK2Threads, 0, st>>>(tab, a);
+        }
     });
 }
 
@@ -2337,7 +2445,11 @@ void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsi
 
 void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, uint64_t bc_first,
                         const AdamConsts& c, cudaStream_t s) {
-    k_step_finish<<<1, 32, 0, s>>>(st, log, bc_table, bc_first, c);
+    if (pdl_finish()) {
+        launch_pdl(k_step_finish, 1, 32, s, st, log, bc_table, static_cast<unsigned long long>(bc_first), c);
+    } else {
+        k_step_finish<<<1, 32, 0, s>>>(st, log, bc_table, bc_first, c);
+    }
 }
 
 void launch_step_prepare(StepDev* st, const float2* bc_table, uint64_t bc_first,

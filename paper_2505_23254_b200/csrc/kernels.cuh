@@ -50,6 +50,8 @@ struct K1Args {
     uint32_t elem_bytes;
     int early_exit;
     const XchgDev* xchg;    // non-null: exchange the flag with all ranks at the end
+    uint64_t keep_from;     // vectors from here on are loaded with an L2 evict_last
+                            // policy (the tail K2 reads last; nvec = none)
 };
 
 struct Seg {
@@ -103,9 +105,11 @@ void launch_k1(const K1Args& a, bool track, int unroll, bool oneshot, unsigned g
 // 0 thread-contiguous VEC=8, 1 thread-contiguous VEC=4, 2 warp-contiguous
 // U=2, 3 U=1 + prefetch, 4 U=2 + prefetch, 5 U=4, 6/9 forced occupancy,
 // 7/8 load cache hints, 10/11 TMA bulk-copy ring, 12 approximate-math probe;
-// one tile per CTA: 13 U=2, **14 U=4 (production)**, 15 U=1.  Dtype pairs other
-// than (bf16, bf16) only carry kK2DefaultVariant.
-constexpr int kK2DefaultVariant = 14;
+// one tile per CTA: 13 U=2, 14 U=4, 15 U=1; **20 = 14 launched as a
+// programmatic dependent of K1 (production)**, 21 = 20 with the tile's loads
+// before griddepcontrol.wait, 22 = 14 with the tiles back to front.  Dtype
+// pairs other than (bf16, bf16) only carry kK2DefaultVariant.
+constexpr int kK2DefaultVariant = 20;
 int k2_effective_variant(int gk, int wk, int variant);
 void k2_variant_shape(int variant, int* vec, int* tile_vectors, bool* stream);
 // one tile per CTA: grid = total_tiles + trailing CTAs for the scalar remainder
