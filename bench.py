@@ -68,8 +68,9 @@ def parse():
                          "full-length gradients, K2 update + weight all-gather (per-rank "
                          "partition --params, default 1e9)")
     ap.add_argument("--precision", choices=["mixed", "pure_bf16"], default="mixed",
-                    help="cfg5 optimizer state: fp32 master/m/v (K2) or bf16 m/v + bf16 "
-                         "weights (OptimPrecision::pure_bf16, K3)")
+                    help="optimizer state: fp32 master/m/v (K2) or bf16 m/v + bf16 weights "
+                         "(OptimPrecision::pure_bf16, K3) — in HBM for cfg1/cfg2/cfg3, "
+                         "swapped for cfg5")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--flag-exchange", choices=["nccl", "torch", "p2p"], default="nccl",
                     help="N>1: all-reduce the skip flag with the library's own NCCL "
@@ -185,6 +186,40 @@ def cpu_reference_run(n, steps, warmup, threads):
             "seconds_per_step": t}
 
 
+def cpu_reference_run_bf16(n, steps, warmup, threads):
+    """The reference's pure-bf16 step (OptimPrecision::pure_bf16,
+    simulator.cpp:431-486: fused_overflow_check over the fp32 flat buffer,
+    then adam_step_bf16 per sub-group on the bf16 weights / m / v) from
+    oracle/_ref on a bounded sample, all `threads` host threads."""
+    from oracle import oracle as ora
+
+    if not ora.ref_available():
+        raise SystemExit("cpu baseline: oracle/_ref (the compiled reference) is missing")
+    _, w = ora.fill_weights(n, seed=1, w_kind="bf16", threads=threads)
+    _, g32 = ora.fill_grads(w, 0, seed=1, scale=65536.0, g_kind="bf16", w_kind="bf16",
+                            threads=threads)
+    m = np.zeros(n, np.uint16)
+    v = np.zeros(n, np.uint16)
+    h = ora.hyper(**HYPER)
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        of, _ = ora.ref_fused_overflow_check(g32, workers=threads)
+        assert not of
+        for o in range(0, n, SUBGROUP):
+            e = min(n, o + SUBGROUP)
+            ora.ref_adam_step_bf16(w[o:e], m[o:e], v[o:e], g32[o:e], s + 1, h, 65536.0, threads)
+        if s >= warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    return {"value": n / t, "unit": "params/s", "cores": threads, "kind": "reference",
+            "sample": f"{n} params, pure-bf16 state (bf16 weights/m/v, bf16-rounded grads "
+                      f"widened to the reference's fp32 flat buffer), fused_overflow_check + "
+                      f"adam_step_bf16 per {SUBGROUP // 1_000_000}M sub-group, median of {steps} "
+                      f"steps after {warmup} warm-up, {threads} threads",
+            "seconds_per_step": t}
+
+
 def cpu_model():
     """lscpu's model name and socket count (record both)."""
     model, sockets = "unknown", None
@@ -229,6 +264,9 @@ def reference_arm(args, n_per_gpu, rank, world):
     threads = os.cpu_count() or 1
     if args.config == "cfg5":
         res = reference_swapped_run(args, max(1, min(args.steps, 3)), 1, threads)
+    elif args.precision == "pure_bf16":
+        sample = min(args.cpu_sample, n_per_gpu)
+        res = cpu_reference_run_bf16(sample, max(1, args.steps), max(1, args.warmup), threads)
     else:
         sample = min(args.cpu_sample, n_per_gpu)
         res = cpu_reference_run(sample, max(1, args.steps), max(1, args.warmup), threads)
@@ -255,15 +293,19 @@ def workload_config(args, n, world):
             and not args.params
             else "llama3-70b-shard-swapped-nvme+dram" if args.config == "cfg5"
             and not args.params else f"custom-{n}")
+    if args.precision == "pure_bf16" and args.config != "cfg5":
+        name += "-pure-bf16"
     state = ("fp32 master/m/v in the registered host pool, staged H2D/D2H"
              if args.config == "cfg4" else
              "fp32 master/m/v split between the O_DIRECT swap store and the registered host pool"
-             if args.config == "cfg5" else "fp32 master/m/v in HBM")
+             if args.config == "cfg5" else
+             "bf16 weights/m/v in HBM (OptimPrecision::pure_bf16)" if args.precision == "pure_bf16"
+             else "fp32 master/m/v in HBM")
     return {"workload": name, "params_per_gpu": n, "subgroup_params": min(SUBGROUP, n),
             "grads": "bf16", "working_weights": "bf16", "state": state,
             "optimizer": "AdamW lr=1e-3 b1=0.9 b2=0.999 eps=1e-8 wd=0.01, loss scale 65536",
             "parallelism": f"zero-partition x{world} (flag all-reduce only)",
-            "l2": "inputs larger than L2 (no flush needed)" if n * 28 > 4 * 126e6
+            "l2": "inputs larger than L2 (no flush needed)" if n * 14 > 4 * 126e6
             else "L2 flushed between steps"}
 
 
@@ -330,29 +372,44 @@ def ours(args, n, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    # --precision pure_bf16: OptimPrecision::pure_bf16 (simulator.cpp:470-486)
+    # — the bf16 weights are the parameters, bf16 m/v, K3 instead of K2
+    bf16_state = args.precision == "pure_bf16"
+    bpp = 14 if bf16_state else BYTES_PER_PARAM
     free, total = torch.cuda.mem_get_info()
-    need = n * 16 + (1 << 30)
+    need = n * (8 if bf16_state else 16) + (1 << 30)
     if need > free:
         raise SystemExit(f"rank {rank}: need {need / 1e9:.1f} GB of HBM, {free / 1e9:.1f} free")
-    p = torch.empty(n, dtype=torch.float32, device=dev)
-    m = torch.zeros(n, dtype=torch.float32, device=dev)
-    v = torch.zeros(n, dtype=torch.float32, device=dev)
-    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    sdt = torch.bfloat16 if bf16_state else torch.float32
     w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    p = w if bf16_state else torch.empty(n, dtype=torch.float32, device=dev)
+    m = torch.zeros(n, dtype=sdt, device=dev)
+    v = torch.zeros(n, dtype=sdt, device=dev)
+    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
     base = rank * n
-    mab.gen_seeded_weights(p, w, base=base, seed=1)
+    mab.gen_seeded_weights(None if bf16_state else p, w, base=base, seed=1)
     mab.gen_pseudo_grads(g, w, step=0, base=base, seed=1, scale=65536.0)
     st = mab.Stepper(mab.AdamHyper(**HYPER), 65536.0, 2000, "bf16", "bf16", device=dev)
     sub = min(SUBGROUP, n)
-    groups = mab.Stepper.subgroups(
-        [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub], w[o:o + sub])
-         for o in range(0, n, sub)], "bf16", "bf16")
+    if bf16_state:
+        groups = [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub])
+                  for o in range(0, n, sub)]
+
+        def apply_step(stream):
+            st.apply_bf16(groups, stream=stream)
+    else:
+        groups = mab.Stepper.subgroups(
+            [(p[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub], w[o:o + sub])
+             for o in range(0, n, sub)], "bf16", "bf16")
+
+        def apply_step(stream):
+            st.apply(groups, stream=stream)
     stream = torch.cuda.Stream(device=dev)  # non-default: capturable
     stream.wait_stream(torch.cuda.current_stream(dev))
     inject = args.config == "cfg3"
     plan = FaultPlan(n * world, sub, seed=2505) if inject else None
     flush = flush_read = None
-    if n * BYTES_PER_PARAM < 4 * 126e6:  # small configs: flush L2 between steps
+    if n * bpp < 4 * 126e6:  # small configs: flush L2 between steps
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         flush_read = torch.empty(1, dtype=torch.int64, device=dev)
     xc = Exchange(args.flag_exchange, world, rank)
@@ -367,7 +424,7 @@ def ours(args, n, rank, world, local_rank):
         xc.after_check(st, stream)
         if with_events:
             with_events[2].record(stream)
-        st.apply(groups, stream=stream)
+        apply_step(stream)
         st.finish(stream=stream)
         if with_events:
             with_events[3].record(stream)
@@ -502,7 +559,7 @@ def ours(args, n, rank, world, local_rank):
             if xc.xchg is not None:
                 st.check(None, stream=stream, xchg=xc.xchg)  # exchange-only K1 launch
             xc.after_check(st, stream)
-            st.apply(groups, stream=stream)
+            apply_step(stream)
             st.finish(stream=stream)
             with torch.cuda.stream(stream):
                 res_host.copy_(st.state_t[:16], non_blocking=True)  # flag/scale readback
@@ -527,7 +584,8 @@ def ours(args, n, rank, world, local_rank):
                "h2d_bytes_per_step": n * 2, "d2h_bytes_per_step": 16,
                "ms_per_step": e2e_ms,
                "path": "pinned host bf16 grads -> chunked H2D overlapped with K1 "
-                       "(ma_stepper_check_host_async) -> flag exchange -> K2 over HBM-resident "
+                       "(ma_stepper_check_host_async) -> flag exchange -> "
+                       f"{'K3' if bf16_state else 'K2'} over HBM-resident "
                        "state -> D2H of the step's flag/loss-scale"}
         del g_host
         mab.host_unregister(g_buf)
@@ -538,7 +596,7 @@ def ours(args, n, rank, world, local_rank):
     if rank != 0:
         return
     peak, peak_kind = peaks()
-    alg_bytes = BYTES_PER_PARAM * n
+    alg_bytes = bpp * n
     k2_gbs = alg_bytes / (k2_ms / 1e3) / 1e9
     # K1 + K2 launches (96 sub-groups per launch) + finish, plus the producer
     # (k_gen_grads) and cfg3's k_plant launches between the timed segments
@@ -552,7 +610,8 @@ def ours(args, n, rank, world, local_rank):
         if name.endswith("_ncu_summary.json"):
             try:
                 summ = json.load(open(os.path.join(ROOT, "profiles", name)))
-                k2 = next(v for v in summ.values() if "k2_" in v.get("Kernel Name", ""))
+                tag = "k3_" if bf16_state else "k2_"
+                k2 = next(v for v in summ.values() if tag in v.get("Kernel Name", ""))
                 traffic = k2["dram_bytes_per_param"] * n
                 break
             except Exception:
@@ -575,11 +634,13 @@ def ours(args, n, rank, world, local_rank):
         "dtype": "f32", "data": "synthetic (reference generators seeded_weight/pseudo_gradient)",
         "config": cfg,
         "hbm_gbs_per_gpu": alg_bytes / (ms_per_step / 1e3) / 1e9,
-        "roofline": {"bound": "hbm", "kernel": "k2_oneshot (K2 fused unscale+AdamW+cast)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("k3_v2 (K3 fused unscale+AdamW on bf16 weights/m/v)" if bf16_state
+                                else "k2_oneshot (K2 fused unscale+AdamW+cast)"),
                      "achieved": k2_gbs, "peak": peak, "unit": "GB/s",
                      "frac": k2_gbs / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                     "bytes_per_param": BYTES_PER_PARAM, "params_per_launch": n,
+                     "bytes_per_param": bpp, "params_per_launch": n,
                      "k2_ms": k2_ms, "k1_ms": k1_ms, "kernel_timing": kernel_timing,
                      "k1_gbs": 2 * n / (k1_ms / 1e3) / 1e9,
                      "step_frac": alg_bytes / (ms_per_step / 1e3) / 1e9 / peak},
@@ -589,7 +650,12 @@ def ours(args, n, rank, world, local_rank):
     }
     if check is not None:
         line["cfg3_check"] = check
-    if world == 1 and not args.no_cpu_baseline and not inject:
+    if world == 1 and not args.no_cpu_baseline and not inject and bf16_state:
+        threads = os.cpu_count() or 1
+        cb = cpu_reference_run_bf16(min(args.cpu_sample, n), 5, 1, threads)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["host"] = {"cpu": cpu_model(), "nproc": threads}
+    elif world == 1 and not args.no_cpu_baseline and not inject:
         threads = os.cpu_count() or 1
         cb = cpu_reference_run(min(args.cpu_sample, n), 5, 1, threads)  # >= 5
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

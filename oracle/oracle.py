@@ -349,6 +349,16 @@ def ref_adam_step_fp32(p, m, v, g, t, h: Hyper, scale, workers=1):
         raise ValueError(ref().ref_last_error().decode())
 
 
+def ref_adam_step_bf16(p16, m16, v16, g, t, h: Hyper, scale, workers=1):
+    """The reference's adam_step_bf16 (optimizer.cpp:111-118) on raw bf16
+    (uint16) state and fp32 gradients, in place."""
+    hv = ref_hyper_array(h)
+    r = ref().ref_adam_step_bf16(_ptr(p16), _ptr(m16), _ptr(v16), _ptr(g), p16.size, t,
+                                 _ptr(hv), scale, workers)
+    if r:
+        raise ValueError(ref().ref_last_error().decode())
+
+
 def ref_fused_overflow_check(g, workers=1, chunk_bytes=1 << 20, early_exit=True, track=False):
     of, first = C.c_int(), C.c_uint64()
     r = ref().ref_fused_overflow_check(_ptr(g), g.size, workers, chunk_bytes, int(early_exit),

@@ -297,8 +297,20 @@ class Stepper:
         """Pure-bf16 mode: groups of (p_bf16, m_bf16, v_bf16, g) tensors (K3)."""
         arr = (capi.SubgroupBf16 * len(groups))()
         for k, (p, m, v, g) in enumerate(groups):
-            arr[k] = capi.SubgroupBf16(p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
-                                       p.numel())
+            n = p.numel()
+            for name, x in (("p", p), ("m", m), ("v", v)):
+                _, nx, _ = _info(x, "bf16")
+                if nx != n:
+                    raise MemAscendError(1, f"sub-group {k}: p/m/v lengths differ")
+                if not _kind_ok(x, "bf16"):
+                    raise MemAscendError(1, f"sub-group {k}: {name} must hold bf16 bits")
+            _, ng, _ = _info(g, self.g_dtype)
+            if ng != n:
+                raise MemAscendError(1, f"sub-group {k}: gradient length differs")
+            if not _kind_ok(g, self.g_dtype):
+                raise MemAscendError(1, f"sub-group {k}: gradients are {g.dtype}, the stepper's "
+                                        f"gradient kind is {self.g_dtype}")
+            arr[k] = capi.SubgroupBf16(p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), n)
         check(capi.lib().ma_stepper_apply_bf16_async(self._h, arr, len(arr), _stream_ptr(stream)))
 
     def apply_streamed(self, groups, staging, slot_elems, slots=2, stream=None,

@@ -189,15 +189,24 @@ __global__ void __launch_bounds__(kK1Threads) k1_oneshot(K1Args a) {
     if (!skip) {
         uint64_t pol = 0;
         if constexpr (LDK == 1) {
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
         }
         uint4 q[U];
+        // only the CTAs that reach the kept tail take the per-vector test
+        const bool keep = LDK != 0 && first - threadIdx.x + U * blockDim.x > a.keep_from;
+        if (keep) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t i = first + static_cast<uint64_t>(u) * blockDim.x;
-            q[u] = i >= a.nvec ? make_uint4(0, 0, 0, 0)
-                   : (LDK != 0 && i >= a.keep_from) ? k1_load<LDK>(a.body + i, pol)
-                                                    : __ldcs(a.body + i);
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = first + static_cast<uint64_t>(u) * blockDim.x;
+                q[u] = i >= a.nvec ? make_uint4(0, 0, 0, 0)
+                       : i >= a.keep_from ? k1_load<LDK>(a.body + i, pol) : __ldcs(a.body + i);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = first + static_cast<uint64_t>(u) * blockDim.x;
+                q[u] = i < a.nvec ? __ldcs(a.body + i) : make_uint4(0, 0, 0, 0);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -1437,6 +1446,10 @@ template <int GK, int U, int MINB, bool PROBE = false, int GUARD = 0, int TPC = 
           bool DEFER = false>
 __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs a) {
     static_assert(!DEFER || TPC == 1, "deferred slots: one tile per CTA");
+    // programmatic dependent of K1 (production launch, §3.5): nothing is read
+    // before the previous grid has completed (no-ops on a plain launch)
+    pdl_trigger();
+    pdl_wait();
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
     const AdamConsts c = a.c;
@@ -2440,7 +2453,20 @@ int k3_blocks_per_sm(int gk, int variant) {
 
 void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsigned grid,
                cudaStream_t st) {
-    k3_dispatch(gk, variant, [&](auto fn) { fn<<<grid, kK2Threads, 0, st>>>(tab, a); });
+    // the production k3_v2 waits on entry: launched as a programmatic
+    // dependent (MA_PDL_K3=0: plain launch, A/B); the older A/B kernels do not
+    static const bool pdl = [] {
+        const char* e = std::getenv("MA_PDL_K3");
+        return !(e && e[0] == '0');
+    }();
+    const bool production = gk != kBF16 || variant == 0 || variant > 20;
+    k3_dispatch(gk, variant, [&](auto fn) {
+        if (pdl && production) {
+            launch_pdl(fn, grid, kK2Threads, st, tab, a);
+        } else {
+            fn<<<grid, kK2Threads, 0, st>>>(tab, a);
+        }
+    });
 }
 
 void launch_step_finish(StepDev* st, StepLog* log, const float2* bc_table, uint64_t bc_first,

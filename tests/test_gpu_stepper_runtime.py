@@ -100,6 +100,24 @@ def test_set_state_validation():
         r.st.set_state(1024.0, 2000, 3)  # clean_steps must stay below growth_interval
 
 
+def test_apply_bf16_validation():
+    """apply_bf16 checks kinds and lengths before anything reaches the device."""
+    st = mab.Stepper(mab.AdamHyper(), 65536.0, 2000, "bf16", "bf16")
+    n = 4096
+    b = lambda k=n: torch.zeros(k, dtype=torch.bfloat16, device="cuda")  # noqa: E731
+    with pytest.raises(mab.MemAscendError):  # fp32 moments
+        st.apply_bf16([(b(), torch.zeros(n, device="cuda"), b(), b())])
+    with pytest.raises(mab.MemAscendError):  # short variance
+        st.apply_bf16([(b(), b(), b(n - 8), b())])
+    with pytest.raises(mab.MemAscendError):  # fp32 grads for a bf16 stepper
+        st.apply_bf16([(b(), b(), b(), torch.zeros(n, device="cuda"))])
+    with pytest.raises(mab.MemAscendError):  # non-contiguous
+        st.apply_bf16([(b(2 * n)[::2], b(), b(), b())])
+    st.apply_bf16([(b(), b(), b(), b())])  # well-formed: runs
+    torch.cuda.synchronize()
+    st.close()
+
+
 @pytest.mark.parametrize("with_comm", [False, True])
 def test_graph_replay_equals_eager(with_comm):
     ref = oracle(10)
