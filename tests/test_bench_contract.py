@@ -48,6 +48,16 @@ def test_reference_arm_line(nproc):
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0
 
 
+def test_reference_arm_line_pure_bf16():
+    """The reference arm in the pure-bf16 mode times the reference's own
+    fused_overflow_check + adam_step_bf16 (oracle/_ref)."""
+    j = run(["--impl", "reference", "--precision", "pure_bf16", "--steps", "1", "--warmup", "1",
+             "--cpu-sample", "1000000"])
+    assert REQUIRED <= set(j) and j["value"] > 0
+    assert j["config"]["workload"].endswith("-pure-bf16")
+    assert "adam_step_bf16" in j["cpu_baseline"]["sample"]
+
+
 def run_plain(args, env=None, timeout=600):
     """bench.py WITHOUT a launcher (the driver's `python bench.py --gpus N`)."""
     e = dict(os.environ, **(env or {}))
@@ -138,6 +148,18 @@ def test_our_arm_line_n1():
     r = j["roofline"]
     assert r["bound"] == "hbm" and 0 < r["frac"] < 1.2 and r["unit"] == "GB/s"
     assert j["e2e"]["h2d_bytes_per_step"] == 2 * 200000000 and j["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graph", [False, True])
+def test_our_arm_line_pure_bf16(graph):
+    j = run(["--precision", "pure_bf16", "--params", "200000000", "--steps", "3", "--warmup",
+             "3", "--e2e-steps", "1", "--cpu-sample", "1000000"] + (["--graph"] if graph else []))
+    assert REQUIRED <= set(j) and {"roofline", "cpu_baseline", "gpu_launches"} <= set(j)
+    r = j["roofline"]
+    assert r["bytes_per_param"] == 14 and "k3_v2" in r["kernel"] and 0 < r["frac"] < 1.2
+    assert j["config"]["state"].startswith("bf16 weights/m/v in HBM")
+    assert "adam_step_bf16" in j["cpu_baseline"]["sample"]
 
 
 @pytest.mark.gpu
