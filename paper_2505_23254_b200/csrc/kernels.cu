@@ -1366,11 +1366,57 @@ __device__ __forceinline__ float max3n(float a, float b, float c) {
 
 // GUARD: 0 = five compares per element, 1 = the same ranges tested once per
 // slot on NaN-propagating min / max reductions (FMNMX3.NAN).
-template <int GK, int GUARD = 0>
+// EARLY (GUARD 1 only): the guard is evaluated on M, V, p before the
+// division / square-root sequences, and a warp whose active lanes all fail
+// it returns at once (cold rows, non-finite blocks: the deferred phase
+// recomputes those slots anyway); a warp with any admitted lane computes as
+// before.
+template <int GK, int GUARD = 0, bool EARLY = false>
 __device__ __forceinline__ bool k3_fast8(const K3Raw<GK>& r, uint4& po, uint4& mo, uint4& vo,
                                          const AdamConsts& c, const StepScalars& s) {
+    static_assert(!EARLY || GUARD != 0, "early reject: reduction guard only");
     float P[8], M[8], V[8], AM[8], AP[8];
     bool ok = true;
+    if constexpr (EARLY) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float m = bf16_lane(r.m, k), v = bf16_lane(r.v, k);
+            const float g = __fmul_rn(k3_grad<GK>(r, k), s.inv_scale);
+            M[k] = __fadd_rn(__fmul_rn(c.beta1, m), __fmul_rn(c.one_minus_b1, g));
+            V[k] = __fadd_rn(__fmul_rn(c.beta2, v), __fmul_rn(c.one_minus_b2, __fmul_rn(g, g)));
+            AM[k] = fabsf(M[k]);
+            AP[k] = fabsf(bf16_lane(r.p, k));
+        }
+        const float mn_m = min3n(min3n(AM[0], AM[1], AM[2]), min3n(AM[3], AM[4], AM[5]),
+                                 min3n(AM[6], AM[7], AM[7]));
+        const float mx_m = max3n(max3n(AM[0], AM[1], AM[2]), max3n(AM[3], AM[4], AM[5]),
+                                 max3n(AM[6], AM[7], AM[7]));
+        const float mn_v = min3n(min3n(V[0], V[1], V[2]), min3n(V[3], V[4], V[5]),
+                                 min3n(V[6], V[7], V[7]));
+        const float mx_v = max3n(max3n(V[0], V[1], V[2]), max3n(V[3], V[4], V[5]),
+                                 max3n(V[6], V[7], V[7]));
+        const float mx_p = max3n(max3n(AP[0], AP[1], AP[2]), max3n(AP[3], AP[4], AP[5]),
+                                 max3n(AP[6], AP[7], AP[7]));
+        ok = (mn_m >= 0x1p-50f) & (mx_m < 0x1p51f) & (mn_v >= 0x1p-96f) & (mx_v < 0x1p80f) &
+             (mx_p < __uint_as_float(0x7F800000u));
+        if (!__any_sync(__activemask(), ok)) return false;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float p = bf16_lane(r.p, k);
+            const float mh = div_by(M[k], s.bc1, s.y1);
+            const float vh = div_by(V[k], s.bc2, s.y2);
+            const float den = __fadd_rn(sqrt_fast(vh), c.eps);
+            const float upd = __fmul_rn(c.lr, div_by(mh, den, rcp_refined(den)));
+            P[k] = __fsub_rn(__fsub_rn(p, upd), __fmul_rn(c.lr_wd, p));
+        }
+        po = make_uint4(narrow2_num<kBF16>(P[0], P[1]), narrow2_num<kBF16>(P[2], P[3]),
+                        narrow2_num<kBF16>(P[4], P[5]), narrow2_num<kBF16>(P[6], P[7]));
+        mo = make_uint4(narrow2_num<kBF16>(M[0], M[1]), narrow2_num<kBF16>(M[2], M[3]),
+                        narrow2_num<kBF16>(M[4], M[5]), narrow2_num<kBF16>(M[6], M[7]));
+        vo = make_uint4(narrow2_num<kBF16>(V[0], V[1]), narrow2_num<kBF16>(V[2], V[3]),
+                        narrow2_num<kBF16>(V[4], V[5]), narrow2_num<kBF16>(V[6], V[7]));
+        return ok;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const float p = bf16_lane(r.p, k), m = bf16_lane(r.m, k), v = bf16_lane(r.v, k);
@@ -1442,8 +1488,12 @@ __device__ __forceinline__ void k3_probe8(const K3Raw<GK>& r, uint4& po, uint4& 
 // tile, all threads of the CTA process the listed slots element by element
 // (adam_any: fast, cold second chance, else the full exact sequence) — no
 // SIMT divergence, and cold or non-finite slots cost their own work only.
+// COLD (with DEFER), bit 0: k3_fast8's early warp-uniform reject; bit 1: a
+// listed slot whose eight elements all take the M == 0 shortcut of
+// cold_elem (m = g = 0: an untouched row) is finished in one vector step
+// instead of eight adam_any calls.
 template <int GK, int U, int MINB, bool PROBE = false, int GUARD = 0, int TPC = 1,
-          bool DEFER = false>
+          bool DEFER = false, int COLD = 0>
 __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs a) {
     static_assert(!DEFER || TPC == 1, "deferred slots: one tile per CTA");
     // programmatic dependent of K1 (production launch, §3.5): nothing is read
@@ -1494,7 +1544,7 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
                 uint4 po, mo, vo;
                 if constexpr (PROBE) {
                     k3_probe8<GK>(q[u], po, mo, vo);
-                } else if (!(sc.fast && k3_fast8<GK, GUARD>(q[u], po, mo, vo, c, sc))) {
+                } else if (!(sc.fast && k3_fast8<GK, GUARD, (COLD & 1) != 0>(q[u], po, mo, vo, c, sc))) {
                     if constexpr (DEFER) {
                         dlist[atomicAdd(&dn, 1u)] = u * kK2Threads + threadIdx.x;
                         continue;
@@ -1535,6 +1585,45 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
                 r.g[0] = __ldcs(G0 + sl * (kGB / 2));
                 if constexpr (GK == kF32) r.g[1] = __ldcs(G0 + sl * 2 + 1);
                 uint32_t wp[4], wm[4], wv[4];
+                if constexpr ((COLD & 2) != 0) {
+                    // all eight cold (M == 0, V >= 0, p finite): cold_elem's
+                    // first route, P = (p - lr * M) - lr_wd * p; the test
+                    // first, then the pairs recomputed (no 24 live floats)
+                    bool cold = sc.fast;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float g = __fmul_rn(k3_grad<GK>(r, k), sc.inv_scale);
+                        const float M = __fadd_rn(__fmul_rn(c.beta1, bf16_lane(r.m, k)),
+                                                  __fmul_rn(c.one_minus_b1, g));
+                        const float V = __fadd_rn(__fmul_rn(c.beta2, bf16_lane(r.v, k)),
+                                                  __fmul_rn(c.one_minus_b2, __fmul_rn(g, g)));
+                        cold &= (M == 0.0f) & (V >= 0.0f) & fast_p_ok(bf16_lane(r.p, k));
+                    }
+                    if (cold) {
+#pragma unroll
+                        for (int k = 0; k < 8; k += 2) {
+                            float P[2], M[2], V[2];
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const float p = bf16_lane(r.p, k + h);
+                                const float g = __fmul_rn(k3_grad<GK>(r, k + h), sc.inv_scale);
+                                M[h] = __fadd_rn(__fmul_rn(c.beta1, bf16_lane(r.m, k + h)),
+                                                 __fmul_rn(c.one_minus_b1, g));
+                                V[h] = __fadd_rn(__fmul_rn(c.beta2, bf16_lane(r.v, k + h)),
+                                                 __fmul_rn(c.one_minus_b2, __fmul_rn(g, g)));
+                                P[h] = __fsub_rn(__fsub_rn(p, __fmul_rn(c.lr, M[h])),
+                                                 __fmul_rn(c.lr_wd, p));
+                            }
+                            wp[k >> 1] = narrow2<kBF16>(P[0], P[1]);
+                            wm[k >> 1] = narrow2<kBF16>(M[0], M[1]);
+                            wv[k >> 1] = narrow2<kBF16>(V[0], V[1]);
+                        }
+                        __stcs(P0 + sl, make_uint4(wp[0], wp[1], wp[2], wp[3]));
+                        __stcs(M0 + sl, make_uint4(wm[0], wm[1], wm[2], wm[3]));
+                        __stcs(V0 + sl, make_uint4(wv[0], wv[1], wv[2], wv[3]));
+                        continue;
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < 8; k += 2) {
                     float p2[2], m2[2], v2[2];
@@ -2439,6 +2528,9 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 19: return f(k3_v2<kBF16, 2, 4, false, 1, 2>);
         case 17: return f(k3_v2<kBF16, 2, 4, false, 1>);
         case 20: return f(k3_v2<kBF16, 2, 4, false, 1, 4>);
+        case 21: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 3>);
+        case 22: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 2>);
+        case 23: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 1>);
         default: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true>);
     }
 }
@@ -2459,7 +2551,7 @@ void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsi
         const char* e = std::getenv("MA_PDL_K3");
         return !(e && e[0] == '0');
     }();
-    const bool production = gk != kBF16 || variant == 0 || variant > 20;
+    const bool production = gk != kBF16 || variant == 0 || variant >= 21;
     k3_dispatch(gk, variant, [&](auto fn) {
         if (pdl && production) {
             launch_pdl(fn, grid, kK2Threads, st, tab, a);
