@@ -2480,7 +2480,11 @@ void launch_k2_allgather(int gk, int wk, const SegTable& tab, const AdamArgs& a,
 // round-1 production, 0.94 before / 0.89 after the x86-NaN exact path), 1 =
 // 4 slots unbounded (0.90), 2 = 2 slots at 4 (0.84), 3 = 8 slots (0.89),
 // 4/5 = 8-element slots at 4 / unbounded (0.90 / 0.80), 6 = 2 slots at 5
-// (0.86), 7 = 3 slots at 4 (0.91), 8 = 4 slots at 5 (0.88).
+// (0.86), 7 = 3 slots at 4 (0.91), 8 = 4 slots at 5 (0.88).  Cold routes
+// (round 2 final; production = 21 = COLD 3): 24 = the deferred kernel without
+// them (100% cold rows 0.57 -> 0.84, 20% 0.88 -> 0.97), 22 = only the
+// vectorised M == 0 route of the deferred phase, 23 = only the early
+// warp-uniform reject (slower: 0.94 on live state).
 int k3_slots(int gk, int variant) {
     if (gk != kBF16) return 2;  // k3_v2<GK, 2, 4>
     switch (variant) {
@@ -2505,8 +2509,8 @@ int k3_vec(int gk, int variant) {
 
 template <typename F>
 void k3_dispatch(int gk, int variant, F&& f) {
-    if (gk == kF32) return f(k3_v2<kF32, 2, 4, false, 1, 1, true>);
-    if (gk == kF16) return f(k3_v2<kF16, 2, 4, false, 1, 1, true>);
+    if (gk == kF32) return f(k3_v2<kF32, 2, 4, false, 1, 1, true, 3>);
+    if (gk == kF16) return f(k3_v2<kF16, 2, 4, false, 1, 1, true, 0>);  // COLD 3 spills here
     switch (variant) {
         case 1: return f(k3_adam_bf16<kBF16, 4, 1>);
         case 2: return f(k3_adam_bf16<kBF16, 2, 4>);
@@ -2531,7 +2535,8 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 21: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 3>);
         case 22: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 2>);
         case 23: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 1>);
-        default: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true>);
+        case 24: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 0>);  // production until the cold routes
+        default: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 3>);
     }
 }
 

@@ -1,4 +1,5 @@
-# K3 cold-slot A/B (MA_K3_VARIANT 0 = production, 21 = early warp reject +
+# K3 cold-slot A/B (MA_K3_VARIANT 0 = production (when run: the deferred kernel without
+# cold routes, now variant 24), 21 = early warp reject +
 # vectorised cold route in the deferred phase, 22 = cold route only, 23 =
 # early reject only): normal-case speed + bit-exactness (bench_k3.py), cold
 # layouts (bench_slowpath.py), and the cold / NaN / parity tests per variant.
