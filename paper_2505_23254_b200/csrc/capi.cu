@@ -226,12 +226,16 @@ void numa_place_for_device(void* ptr, uint64_t bytes) {
 }
 
 // ------------------------------------------------------------ K1 launch
-// keep_tail: a stepper check whose gradients K2 reads next — the buffer's
-// last MA_K1_KEEP_MB (default 32 MiB) are loaded under an L2 evict_last
-// policy so K2's last tiles find them in L2 (kernels.cu k1_load).
+// keep_tail: a stepper check whose gradients K2 reads next — with
+// MA_K1_KEEP_MB > 0 (A/B; default 0 = off) the buffer's last
+// MA_K1_KEEP_MB are loaded under an L2 evict_last policy so K2's last tiles
+// find them in L2 (kernels.cu k1_load).
+// kept_lo / kept_lines (keep_tail only): the 128-byte lines now under
+// evict_last, for the update to demote (ma::AdamArgs::demote).
 void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* first,
                uint64_t index_base, bool early_exit, cudaStream_t st,
-               const ma::XchgDev* xchg = nullptr, bool keep_tail = false) {
+               const ma::XchgDev* xchg = nullptr, bool keep_tail = false,
+               const char** kept_lo = nullptr, uint64_t* kept_lines = nullptr) {
     if (n == 0 && !xchg) return;  // an empty rank still takes part in the exchange
     const DeviceInfo d = device_info();
     const uint32_t es = static_cast<uint32_t>(elem_bytes(dt));
@@ -252,9 +256,20 @@ void launch_k1(const void* data, uint64_t n, int dt, uint32_t* flag, uint64_t* f
     a.early_exit = early_exit ? 1 : 0;
     static const uint64_t keep_vecs = [] {
         const char* e = std::getenv("MA_K1_KEEP_MB");  // A/B only
-        return (e ? std::strtoull(e, nullptr, 10) : 32ull) << 16;  // MiB / 16 B
+        return (e ? std::strtoull(e, nullptr, 10) : 0ull) << 16;  // MiB / 16 B (default off)
     }();
     a.keep_from = keep_tail ? a.nvec - std::min<uint64_t>(a.nvec, keep_vecs) : a.nvec;
+    if (kept_lo && kept_lines) {
+        if (a.keep_from < a.nvec) {
+            const uintptr_t lo = reinterpret_cast<uintptr_t>(a.body + a.keep_from) & ~uintptr_t(127);
+            const uintptr_t hi = (reinterpret_cast<uintptr_t>(a.body + a.nvec) + 127) & ~uintptr_t(127);
+            *kept_lo = reinterpret_cast<const char*>(lo);
+            *kept_lines = (hi - lo) / 128;
+        } else {
+            *kept_lo = nullptr;
+            *kept_lines = 0;
+        }
+    }
     // MA_K1_UNROLL / MA_K1_CTAS_PER_SM: A/B knobs (defaults 4 and 8)
     static const int unroll = [] {
         const char* e = std::getenv("MA_K1_UNROLL");
@@ -487,6 +502,8 @@ struct ma_stepper {
     int device = 0;
     bool owns_state = true;
     bool capturing = false;        // between ma_stepper_graph_begin / _end
+    const char* kept_lo = nullptr; // gradient lines the last check kept in L2,
+    uint64_t kept_lines = 0;       // demoted by the next update (stepper_args)
     uint64_t capture_issued = 0;
     std::vector<float2*> retired;  // superseded bias tables (graphs may hold them)
     std::vector<cudaEvent_t> events;
@@ -505,6 +522,19 @@ struct ma_stepper {
 };
 
 namespace {
+
+// AdamArgs of a stepper update
+ma::AdamArgs stepper_args(ma_stepper* s) {
+    ma::AdamArgs a{};
+    a.c = s->c;
+    a.skip = &s->d_st->flag;
+    a.st = s->d_st;
+    // the first update after a check demotes the lines that check kept
+    a.demote = s->kept_lo;
+    a.demote_lines = s->kept_lines;
+    s->kept_lines = 0;
+    return a;
+}
 
 // The bias-correction table is a window of t values: finish / prepare read
 // the entry of t = updates + 1, and the host only bounds `updates` (it is
@@ -816,7 +846,7 @@ int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void* strea
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (n && !g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
         launch_k1(g, n, s->g_dtype, &s->d_st->flag, nullptr, 0, true, as_stream(stream), nullptr,
-                  true);
+                  true, &s->kept_lo, &s->kept_lines);
         s->last = as_stream(stream);
     });
 }
@@ -849,7 +879,8 @@ int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, 
             CK(cudaEventRecord(landed, cs));
             CK(cudaStreamWaitEvent(st, landed, 0));
             launch_k1(static_cast<uint8_t*>(dev_g) + off * es, len, s->g_dtype, &s->d_st->flag,
-                      nullptr, 0, true, st, nullptr, off + len == n);
+                      nullptr, 0, true, st, nullptr, off + len == n,
+                      off + len == n ? &s->kept_lo : nullptr, &s->kept_lines);
         }
         s->last = st;
     });
@@ -995,7 +1026,7 @@ int ma_stepper_check_xchg_async(ma_stepper* s, const void* g, uint64_t n, ma_xch
         if (n && !g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
         alignas(16) static const uint32_t dummy[4] = {0, 0, 0, 0};  // never read (n == 0)
         launch_k1(n ? g : &dummy, n, s->g_dtype, &s->d_st->flag, nullptr, 0, true,
-                  as_stream(stream), x->d_desc, true);
+                  as_stream(stream), x->d_desc, true, &s->kept_lo, &s->kept_lines);
         s->last = as_stream(stream);
     });
 }
@@ -1048,10 +1079,7 @@ int ma_stepper_apply_async(ma_stepper* s, const ma_subgroup* groups, uint32_t co
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        ma::AdamArgs a{};
-        a.c = s->c;
-        a.skip = &s->d_st->flag;
-        a.st = s->d_st;
+        const ma::AdamArgs a = stepper_args(s);
         launch_k2(groups, count, s->g_dtype, s->w_dtype, a, as_stream(stream));
         s->last = as_stream(stream);
     });
@@ -1063,10 +1091,7 @@ int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups, u
     return guarded([&] {
         if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        ma::AdamArgs a{};
-        a.c = s->c;
-        a.skip = &s->d_st->flag;
-        a.st = s->d_st;
+        const ma::AdamArgs a = stepper_args(s);
         std::vector<ma_subgroup> gs(count);
         for (uint32_t k = 0; k < count; ++k) {
             gs[k] = ma_subgroup{reinterpret_cast<float*>(groups[k].p),
@@ -1333,14 +1358,6 @@ void run_swapped(ma_stepper* s, ma_swap* e, const SwapPlan& plan, void* h_stagin
     }
     stop_writer();
     if (werr_code) fail(werr_code, werr);
-}
-
-ma::AdamArgs stepper_args(ma_stepper* s) {
-    ma::AdamArgs a{};
-    a.c = s->c;
-    a.skip = &s->d_st->flag;
-    a.st = s->d_st;
-    return a;
 }
 
 }  // namespace
@@ -1935,10 +1952,7 @@ int ma_stepper_apply_allgather_async(ma_stepper* s, const ma_subgroup* groups, u
                                                   "rank's shared weight buffer");
         }
         const cudaStream_t st = as_stream(stream);
-        ma::AdamArgs a{};
-        a.c = s->c;
-        a.skip = &s->d_st->flag;
-        a.st = s->d_st;
+        ma::AdamArgs a = stepper_args(s);
         for (int k = 0; k < world; ++k)
             if (k != rank)
                 a.peers.delta[a.peers.n++] =

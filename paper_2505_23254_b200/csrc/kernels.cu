@@ -29,6 +29,20 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// K1's kept gradient tail back to normal L2 priority (applypriority only
+// re-tags a line that is present; it neither evicts nor moves data), spread
+// over the grid's first threads.  Measured without it: an L2-resident
+// workload right after the step ran 12-17% slower
+// (tools/l2_pollution_probe.py).
+__device__ __forceinline__ void demote_kept(const char* base, uint64_t lines) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < lines;
+         i += stride) {
+        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(base + i * 128)
+                     : "memory");
+    }
+}
+
 // ============================================================== K1
 // One pass over the raw bits; each thread ORs (w & MASK) + INC over its
 // 16-byte vectors, one warp vote at the end, one plain store of 1 by the
@@ -162,11 +176,12 @@ __global__ void k_peer_barrier(const XchgDev* xp) {
 // that starts after the flag is already set skips its loads (the reference's
 // cooperative early exit); with an exchange it still takes part in it.
 // K1 load flavour for the vectors from keep_from on (the buffer's last
-// MA_K1_KEEP_MB, default 32 MiB, of a stepper check; keep_from = nvec
-// otherwise): 1 = L2 evict_last policy (production) — those gradients stay
-// in L2 while K2 streams p/m/v through it with evict-first accesses, and K2's
-// last tiles read them from L2 (configs[0]: K2 282.6 -> 274.5 us); A/B:
-// MA_K1_LDK=0 (everything ld.global.cs) / 2 (default caching for the tail).
+// MA_K1_KEEP_MB of a stepper check — an A/B option, default 0 = off;
+// keep_from = nvec otherwise): 1 = L2 evict_last policy — those gradients
+// stay in L2 while K2 streams p/m/v through it with evict-first accesses and
+// K2's last tiles read them from L2; the update then demotes them
+// (demote_kept).  2 = default caching for the tail.  Why it is off:
+// DESIGN.md §3.5.
 template <int LDK>
 __device__ __forceinline__ uint4 k1_load(const uint4* p, uint64_t pol) {
     if constexpr (LDK == 0) return __ldcs(p);
@@ -787,6 +802,9 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k2_oneshot(SegTable tab, Ada
     StepScalars sc;
     if constexpr (PDL != 0) pdl_trigger();
     if constexpr (PDL == 1) pdl_wait();
+    if constexpr (PDL != 2) {
+        if (a.demote_lines) demote_kept(a.demote, a.demote_lines);
+    }
     // REV (A/B): tiles back to front, so the first tiles read the gradients
     // K1 touched last (still in L2)
     const uint64_t t = REV && blockIdx.x < tab.total_tiles ? tab.total_tiles - 1 - blockIdx.x
@@ -1500,6 +1518,7 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
     // before the previous grid has completed (no-ops on a plain launch)
     pdl_trigger();
     pdl_wait();
+    if (a.demote_lines) demote_kept(a.demote, a.demote_lines);
     StepScalars sc;
     if (!resolve_step(a, sc)) return;
     const AdamConsts c = a.c;

@@ -93,6 +93,11 @@ struct AdamArgs {
     // (st != nullptr: the step scalars are read from st, precomputed by
     //  k_step_prepare / k_step_finish from the bias-correction table)
     PeerW peers;             // fused all-gather targets (launch_k2_allgather only)
+    // 128-byte gradient lines the preceding stepper check left under an L2
+    // evict_last policy: the update returns them to normal
+    // priority so they do not outlive the step in L2
+    const char* demote;
+    uint64_t demote_lines;
 };
 
 // Host-side launchers (defined next to the kernels in kernels.cu so every
