@@ -1509,7 +1509,9 @@ __device__ __forceinline__ void k3_probe8(const K3Raw<GK>& r, uint4& po, uint4& 
 // COLD (with DEFER), bit 0: k3_fast8's early warp-uniform reject; bit 1: a
 // listed slot whose eight elements all take the M == 0 shortcut of
 // cold_elem (m = g = 0: an untouched row) is finished in one vector step
-// instead of eight adam_any calls.
+// instead of eight adam_any calls; bit 2: the vector second chance (the
+// fast, M == 0 and scaled routes over the slot, all-M == 0 slots without
+// the sequences) before the per-element path.
 template <int GK, int U, int MINB, bool PROBE = false, int GUARD = 0, int TPC = 1,
           bool DEFER = false, int COLD = 0>
 __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs a) {
@@ -1637,6 +1639,72 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
                             wm[k >> 1] = narrow2<kBF16>(M[0], M[1]);
                             wv[k >> 1] = narrow2<kBF16>(V[0], V[1]);
                         }
+                        __stcs(P0 + sl, make_uint4(wp[0], wp[1], wp[2], wp[3]));
+                        __stcs(M0 + sl, make_uint4(wm[0], wm[1], wm[2], wm[3]));
+                        __stcs(V0 + sl, make_uint4(wv[0], wv[1], wv[2], wv[3]));
+                        continue;
+                    }
+                }
+                if constexpr ((COLD & 4) != 0) {
+                    // the vector second chance: every element takes one of
+                    // adam_any's non-IEEE routes — the fast sequences, the
+                    // M == 0 shortcut or the 2^64-scaled sequences for
+                    // |M| in [2^-100, 2^-50) (cold_elem) — packed pair by
+                    // pair; any element outside them sends the whole slot
+                    // to the per-element path below.  A slot that is all
+                    // M == 0 (an untouched row) skips the sequences.
+                    bool ok = sc.fast;
+                    // on the raw bits (no values to keep): m = g = +-0 gives
+                    // M = +-0 exactly, and v >= 0 then gives V >= 0
+                    uint32_t zm = (r.m.x | r.m.y | r.m.z | r.m.w) & 0x7FFF7FFFu;
+                    if constexpr (GK == kF32) {
+                        zm |= (r.g[0].x | r.g[0].y | r.g[0].z | r.g[0].w | r.g[1].x | r.g[1].y |
+                               r.g[1].z | r.g[1].w) & 0x7FFFFFFFu;
+                    } else {
+                        zm |= (r.g[0].x | r.g[0].y | r.g[0].z | r.g[0].w) & 0x7FFF7FFFu;  // bf16 / fp16 +-0
+                    }
+                    bool allzero = ok && zm == 0u;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        allzero &= (bf16_lane(r.v, k) >= 0.0f) & fast_p_ok(bf16_lane(r.p, k));
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; k += 2) {
+                        if (!ok) break;  // also keeps the pairs' live ranges apart
+                        float P[2], M[2], V[2];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const float p = bf16_lane(r.p, k + h);
+                            const float g = __fmul_rn(k3_grad<GK>(r, k + h), sc.inv_scale);
+                            M[h] = __fadd_rn(__fmul_rn(c.beta1, bf16_lane(r.m, k + h)),
+                                             __fmul_rn(c.one_minus_b1, g));
+                            V[h] = __fadd_rn(__fmul_rn(c.beta2, bf16_lane(r.v, k + h)),
+                                             __fmul_rn(c.one_minus_b2, __fmul_rn(g, g)));
+                            float q = M[h];  // the M == 0 route
+                            if (!allzero) {
+                                const float am = fabsf(M[h]);
+                                const bool vok = fast_v_ok(V[h]);
+                                const bool fastr = fast_m_ok(M[h]) & vok;
+                                const bool zero = (M[h] == 0.0f) & (V[h] >= 0.0f);
+                                const bool scaled = (am >= 0x1p-100f) & (am < 0x1p-50f) & vok;
+                                const float ms = scaled ? __fmul_rn(M[h], 0x1p64f) : M[h];
+                                const float mh = div_by(ms, sc.bc1, sc.y1);
+                                // M == 0: q = M for any positive den; V = 1 keeps it finite
+                                const float vh = div_by(zero ? 1.0f : V[h], sc.bc2, sc.y2);
+                                const float den = __fadd_rn(sqrt_fast(vh), c.eps);
+                                const float qs = div_by(mh, den, rcp_refined(den));
+                                q = zero ? M[h] : scaled ? __fmul_rn(qs, 0x1p-64f) : qs;
+                                ok &= fast_p_ok(p) &
+                                      (fastr | zero | (scaled & (fabsf(qs) >= 0x1p-61f)));
+                            }
+                            P[h] = __fsub_rn(__fsub_rn(p, __fmul_rn(c.lr, q)),
+                                             __fmul_rn(c.lr_wd, p));
+                        }
+                        wp[k >> 1] = narrow2<kBF16>(P[0], P[1]);
+                        wm[k >> 1] = narrow2<kBF16>(M[0], M[1]);
+                        wv[k >> 1] = narrow2<kBF16>(V[0], V[1]);
+                    }
+                    if (ok) {
                         __stcs(P0 + sl, make_uint4(wp[0], wp[1], wp[2], wp[3]));
                         __stcs(M0 + sl, make_uint4(wm[0], wm[1], wm[2], wm[3]));
                         __stcs(V0 + sl, make_uint4(wv[0], wv[1], wv[2], wv[3]));
@@ -2555,6 +2623,7 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 22: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 2>);
         case 23: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 1>);
         case 24: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 0>);  // production until the cold routes
+        case 25: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 5>);  // early reject + vector second chance
         default: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 3>);
     }
 }
