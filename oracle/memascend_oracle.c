@@ -431,7 +431,10 @@ int ora_train_sample(const ora_train_cfg* c, const uint64_t* idx, uint64_t k,
                      const uint8_t* decisions, float* po, float* mo, float* vo, uint16_t* wo) {
     const int bad = cfg_valid(c);
     if (bad) return bad;
-    if (!c->mixed) return -5; /* sampled replay covers the fp32-state mode */
+    /* pure-bf16 mode (simulator.cpp:470-486): bf16 weights / m / v per
+     * element, the same route as ora_train's !mixed branch; outputs are the
+     * exact fp32 widenings of the bf16 state (wo = the weight bits) */
+    if (!c->mixed && c->w_kind != ORA_BF16) return -5;
     /* the scale / t sequence is fixed by the decisions */
     float* scales = (float*)malloc((c->steps + 1) * sizeof(float));
     uint64_t* tsteps = (uint64_t*)malloc((c->steps + 1) * sizeof(uint64_t));
@@ -455,12 +458,29 @@ int ora_train_sample(const ora_train_cfg* c, const uint64_t* idx, uint64_t k,
         const uint64_t gi = idx[j];
         float p = ora_seeded_weight(c->seed, gi), m = 0.0f, v = 0.0f;
         uint16_t w = narrow(p, c->w_kind);
+        uint16_t m16 = 0, v16 = 0;
         for (uint64_t s = 0; s < c->steps; ++s) {
             if (decisions[s]) continue;
             const uint32_t b = stored_grad_bits(c, s, gi, widen(w, c->w_kind), scales[s]);
-            adam_elem(&p, &m, &v, grad_value(c->g_kind, b), &c->hyper, scales[s], bc1s[s],
-                      bc2s[s]);
-            w = narrow(p, c->w_kind);
+            if (c->mixed) {
+                adam_elem(&p, &m, &v, grad_value(c->g_kind, b), &c->hyper, scales[s], bc1s[s],
+                          bc2s[s]);
+                w = narrow(p, c->w_kind);
+            } else {
+                float pf = ora_bf16_to_float(w);
+                float mf = ora_bf16_to_float(m16);
+                float vf = ora_bf16_to_float(v16);
+                adam_elem_ord(&pf, &mf, &vf, grad_value(c->g_kind, b), &c->hyper, scales[s],
+                              bc1s[s], bc2s[s], ORD_BF16);
+                w = ora_bf16_from_float(pf);
+                m16 = ora_bf16_from_float(mf);
+                v16 = ora_bf16_from_float(vf);
+            }
+        }
+        if (!c->mixed) {
+            p = ora_bf16_to_float(w);
+            m = ora_bf16_to_float(m16);
+            v = ora_bf16_to_float(v16);
         }
         if (po) po[j] = p;
         if (mo) mo[j] = m;

@@ -245,10 +245,13 @@ def train(n, steps, seed, mixed=True, g_kind="bf16", w_kind="bf16", base=0, hyp=
 
 
 def train_sample(indices, decisions, steps, seed, g_kind="bf16", w_kind="bf16", hyp=None,
-                 scale=65536.0, growth=2000):
+                 scale=65536.0, growth=2000, mixed=True):
+    """Elementwise replay of train() at the given global indices under the
+    given step decisions (simulator.cpp:427-492 per element).  mixed=False:
+    the pure-bf16 mode; p/m/v are then the exact widenings of the bf16 state."""
     idx = np.ascontiguousarray(indices, dtype=np.uint64)
     dec = np.ascontiguousarray(decisions, dtype=np.uint8)
-    cfg, keep = _cfg(1, steps, seed, True, g_kind, w_kind, 0, hyp, scale, growth)
+    cfg, keep = _cfg(1, steps, seed, mixed, g_kind, w_kind, 0, hyp, scale, growth)
     k = idx.size
     p, m, v = (np.empty(k, np.float32) for _ in range(3))
     w = np.empty(k, np.uint16)

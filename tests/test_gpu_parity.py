@@ -570,3 +570,49 @@ def test_cfg2_full_size_sampled_parity():
     assert (host_bits16(w[it]) == smp["w"]).all()
     del p, m, v, w, st
     torch.cuda.empty_cache()
+
+
+def test_cfg2_full_size_pure_bf16_sampled_parity():
+    """The pure-bf16 mode (OptimPrecision::pure_bf16, simulator.cpp:470-486)
+    on configs[1]'s full partition — the `bench.py --precision pure_bf16`
+    workload: 8,030,261,248 bf16 weights / m / v in HBM, 81 sub-groups, bf16
+    gradients, K1 -> K3 -> scaler, a NaN planted past 2^32 at step 1, scale
+    growth every 2 clean steps.  Decisions exact; 100k random elements plus
+    the 2^32 / sub-group boundaries bit-exact against the oracle's
+    elementwise replay."""
+    torch.cuda.empty_cache()
+    n, steps, seed, sub = 8_030_261_248, 4, 1, 100_000_000
+    if torch.cuda.mem_get_info()[0] < n * 8 + (2 << 30):
+        pytest.skip("needs 66 GB of free HBM")
+    w = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    m = torch.zeros(n, dtype=torch.bfloat16, device=DEV)
+    v = torch.zeros(n, dtype=torch.bfloat16, device=DEV)
+    g = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    mab.gen_seeded_weights(None, w, seed=seed)
+    h = mab.AdamHyper(weight_decay=0.01)
+    st = mab.Stepper(h, 65536.0, 2, "bf16", "bf16")
+    groups = [(w[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub]) for o in range(0, n, sub)]
+    for s in range(steps):
+        mab.gen_pseudo_grads(g, w, step=s, seed=seed, d_scale=st.scale_t)
+        if s == 1:
+            mab.plant_bits(g, (1 << 32) + 12345, 0x7FC0)
+        st.check(g)
+        st.apply_bf16(groups)
+        st.finish()
+    torch.cuda.synchronize()
+    of, sc = st.history()
+    assert of.tolist() == [False, True, False, False]
+    assert sc.tolist() == [65536.0, 32768.0, 32768.0, 65536.0]
+    rs = np.random.default_rng(2)
+    edge = [0, (1 << 31) - 1, 1 << 31, (1 << 32) - 1, 1 << 32, (1 << 32) + 1, (1 << 32) + 12345,
+            n - 1, 99_999_999, 100_000_000]
+    idx = np.unique(np.concatenate([rs.integers(0, n, 100_000), edge]).astype(np.uint64))
+    smp = ora.train_sample(idx, of.astype(np.uint8), steps, seed, g_kind="bf16", w_kind="bf16",
+                           hyp=ora.hyper(weight_decay=0.01), growth=2, mixed=False)
+    it = torch.from_numpy(idx.astype(np.int64)).to(DEV)
+    top = lambda x: (x.view(np.uint32) >> 16).astype(np.uint16)  # noqa: E731
+    assert (host_bits16(w[it]) == smp["w"]).all()
+    assert (host_bits16(m[it]) == top(smp["m"])).all()
+    assert (host_bits16(v[it]) == top(smp["v"])).all()
+    del w, m, v, g, st
+    torch.cuda.empty_cache()
