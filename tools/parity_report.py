@@ -4,6 +4,8 @@ decisions — the north star's "<= 2 ulp per step, also reported after 100
 steps".  Writes profiles/<tag>_parity_report.json.
 
     python tools/parity_report.py [--tag r1] [--n 4000037] [--steps 100]
+        [--precision pure_bf16]   (bf16 weights / m / v through K3; ulps in bf16 units,
+                                   writes <tag>_parity_report_pure_bf16.json)
 """
 import argparse
 import json
@@ -24,6 +26,15 @@ def ulps(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.abs(ia - ib)
 
 
+def ulps16(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """ulp distance between bf16 bit patterns (uint16)."""
+    ia = a.view(np.int16).astype(np.int64)
+    ib = b.view(np.int16).astype(np.int64)
+    ia = np.where(ia < 0, -(ia & 0x7FFF), ia)
+    ib = np.where(ib < 0, -(ib & 0x7FFF), ib)
+    return np.abs(ia - ib)
+
+
 def hist(d: np.ndarray) -> dict:
     return {"0": int((d == 0).sum()), "1": int((d == 1).sum()), "2": int((d == 2).sum()),
             ">2": int((d > 2).sum()), "max": int(d.max(initial=0))}
@@ -35,7 +46,10 @@ def main():
     ap.add_argument("--n", type=int, default=4_000_037)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--precision", choices=["mixed", "pure_bf16"], default="mixed")
     args = ap.parse_args()
+    if args.precision == "pure_bf16":
+        return pure_bf16(args)
 
     import torch
 
@@ -112,6 +126,82 @@ def main():
         json.dump(report, f, indent=1)
     print(json.dumps({k: report[k] for k in ("n", "steps", "decisions_equal", "scales_equal",
                                              "max_ulp_any_step", "w_mismatches_any_step")}))
+
+
+def pure_bf16(args):
+    """The pure-bf16 mode (OptimPrecision::pure_bf16, simulator.cpp:470-486):
+    bf16 weights / m / v through K3 and the device scaler, against the oracle's
+    adam_step_bf16 (pinned to the reference's pure-bf16 digest) in lockstep."""
+    import torch
+
+    import paper_2505_23254_b200 as mab
+    from oracle import oracle as ora
+
+    n, steps, seed = args.n, args.steps, args.seed
+    pats = (0x7F80, 0xFF80, 0x7F81, 0x7FC0, 0xFFC1)
+    faults = [(s, (s * 7919) % n, pats[s % 5]) for s in range(5, steps, 17)]
+    hyp = dict(lr=1e-3, weight_decay=0.01)
+    dev = torch.device("cuda", 0)
+    w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    m = torch.zeros(n, dtype=torch.bfloat16, device=dev)
+    v = torch.zeros(n, dtype=torch.bfloat16, device=dev)
+    g = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    mab.gen_seeded_weights(None, w, seed=seed)
+    st = mab.Stepper(mab.AdamHyper(**hyp), 65536.0, 25, "bf16", "bf16", device=dev)
+    sub = 1_000_000
+    groups = [(w[o:o + sub], m[o:o + sub], v[o:o + sub], g[o:o + sub]) for o in range(0, n, sub)]
+    _, ow = ora.fill_weights(n, seed=seed)
+    om = np.zeros(n, np.uint16)
+    ov = np.zeros(n, np.uint16)
+    scaler = ora.Scaler(65536.0, 25, 0)
+    updates = 0
+    bits = lambda t: t.view(torch.int16).cpu().numpy().view(np.uint16)  # noqa: E731
+    per_step = []
+    for s in range(steps):
+        mab.gen_pseudo_grads(g, w, step=s, seed=seed, d_scale=st.scale_t)
+        og, og32 = ora.fill_grads(ow, s, seed=seed, scale=scaler.scale)
+        for fs, idx, b in faults:
+            if fs == s:
+                mab.plant_bits(g, idx, b)
+                og[idx] = b
+                og32[idx] = np.array([b << 16], np.uint32).view(np.float32)[0]
+        st.check(g)
+        st.apply_bf16(groups)
+        st.finish()
+        skip = ora.overflow_check(og, "bf16")[0]
+        if skip:
+            ora.lib().ora_scaler_on_overflow(ora.C.byref(scaler))
+        else:
+            updates += 1
+            ora.adam_step_bf16(ow, om, ov, og32, updates, ora.hyper(**hyp), scaler.scale)
+            ora.lib().ora_scaler_on_clean_step(ora.C.byref(scaler))
+        torch.cuda.synchronize()
+        state = st.state()
+        dp, dm, dv = (ulps16(bits(t), o) for t, o in ((w, ow), (m, om), (v, ov)))
+        per_step.append({"step": s, "skip_gpu": bool(state["last_overflow"]), "skip_oracle": skip,
+                         "scale_gpu": state["scale"], "scale_oracle": scaler.scale,
+                         "w_max_ulp": int(dp.max()), "m_max_ulp": int(dm.max()),
+                         "v_max_ulp": int(dv.max())})
+    final = {k: hist(d) for k, d in (("w", dp), ("m", dm), ("v", dv))}
+    report = {
+        "what": "B200 C-ABI stepper in the pure-bf16 mode (K3) vs CPU oracle adam_step_bf16 "
+                "(pinned to the reference), bf16 grads, bf16 weights/m/v, AdamW lr=1e-3 wd=0.01, "
+                "growth_interval 25, faults every 17 steps; ulps in bf16 units",
+        "n": n, "steps": steps, "faults": faults,
+        "decisions_equal": all(r["skip_gpu"] == r["skip_oracle"] for r in per_step),
+        "scales_equal": all(r["scale_gpu"] == r["scale_oracle"] for r in per_step),
+        "max_ulp_any_step": max(max(r["w_max_ulp"], r["m_max_ulp"], r["v_max_ulp"])
+                                for r in per_step),
+        "after_final_step_ulp_histogram": final,
+        "tolerance": "bit-exact required by tests (0 ulp)",
+        "per_step": per_step,
+    }
+    out = os.path.join(ROOT, "profiles", f"{args.tag}_parity_report_pure_bf16.json")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    with open(out, "w") as f:
+        json.dump(report, f, indent=1)
+    print(json.dumps({k: report[k] for k in ("n", "steps", "decisions_equal", "scales_equal",
+                                             "max_ulp_any_step")}))
 
 
 if __name__ == "__main__":
