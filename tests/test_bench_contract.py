@@ -105,13 +105,15 @@ def test_gpus_flag_two_ranks_on_one_gpu_without_torchrun():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nproc", [1, 2])
-def test_cfg3_injection_line(nproc):
+@pytest.mark.parametrize("nproc,precision", [(1, "mixed"), (2, "mixed"), (2, "pure_bf16")])
+def test_cfg3_injection_line(nproc, precision):
     """configs[2]: the seeded inf/NaN plan over nproc ranks; bench.py itself
-    asserts every rank's decisions and scales against the committed plan."""
+    asserts every rank's decisions and scales against the committed plan (the
+    decisions depend only on the gradients, so the pure-bf16 mode — K3 on bf16
+    weights — must meet the same plan)."""
     env = {"MA_BENCH_BACKEND": "gloo", "MA_BENCH_DEVICE": "0"} if nproc > 1 else None
     j = run(["--config", "cfg3", "--params", "100000000", "--steps", "12", "--warmup", "3",
-             "--no-cpu-baseline"], nproc=nproc, env=env)
+             "--no-cpu-baseline", "--precision", precision], nproc=nproc, env=env)
     c = j["cfg3_check"]
     assert c["decisions_match"] and c["scales_match"] and c["steps_checked"] == 15
     assert 0 < c["skipped"] < 15 and j["n_gpus"] == nproc
