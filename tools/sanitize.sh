@@ -9,7 +9,8 @@
 #               barrier, K2 all-gather + barriers), all in ONE process;
 #   racecheck + synccheck — the last-CTA completion-counter protocols (K1's
 #               fused exchange, K4's exit barrier) in the same single-process
-#               tests;
+#               tests; memcheck + racecheck over the cold-parameter suite (K3's
+#               shared-memory deferred-slot list and its drains);
 #   ranks     — two ranks on one GPU where EACH rank process runs under the
 #               tool (torchrun launches compute-sanitizer as the rank
 #               program): bench.py with the fused p2p exchange inside a
@@ -31,6 +32,10 @@ run() {
 }
 run memcheck_parity $CS --tool memcheck python -m pytest -x -q -p no:cacheprovider tests/test_gpu_parity.py tests/test_gpu_nan.py tests/test_gpu_stepper_runtime.py tests/test_ingest.py tests/test_zero_step.py::test_fused_zero_step_single_process -k "$HEAVY"
 run memcheck_fuzz $CS --tool memcheck python -m pytest -x -q -p no:cacheprovider tests/test_fuzz_hyper.py
+# the cold routes: K3's shared-memory deferred list (atomicAdd + __syncthreads)
+# and its vector / per-element drains, K2's inline second chance
+run memcheck_cold $CS --tool memcheck python -m pytest -x -q -p no:cacheprovider tests/test_gpu_cold.py
+run racecheck_cold $CS --tool racecheck --racecheck-report all python -m pytest -x -q -p no:cacheprovider tests/test_gpu_cold.py
 run racecheck_protocols $CS --tool racecheck --racecheck-report all python -m pytest -x -q -p no:cacheprovider $SINGLE
 run synccheck_protocols $CS --tool synccheck python -m pytest -x -q -p no:cacheprovider $SINGLE
 ranks() {
