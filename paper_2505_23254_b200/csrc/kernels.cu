@@ -1597,6 +1597,67 @@ __global__ void __launch_bounds__(kK2Threads, MINB) k3_v2(SegTable tab, AdamArgs
             uint4* M0 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sd.m) + b0);
             uint4* V0 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sd.v) + b0);
             const uint4* G0 = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(sd.g) + b0 * kGB);
+            // split drain (COLD bit 3, A/B variant 27): two threads per
+            // listed slot, four elements (8-byte accesses) each, so a tile
+            // with a few listed slots ends after half the serial tail; the
+            // M == 0 route per half (helps scattered cold
+            // slots, costs dense cold tiles; also when chosen at run time by
+            // the list length)
+            if constexpr ((COLD & 8) != 0) {
+                for (uint32_t d2 = threadIdx.x; d2 < 2 * nd; d2 += kK2Threads) {
+                    const uint32_t sl = dlist[d2 >> 1];
+                    const uint32_t hf = d2 & 1u;
+                    uint2* Ph = reinterpret_cast<uint2*>(P0 + sl) + hf;
+                    uint2* Mh = reinterpret_cast<uint2*>(M0 + sl) + hf;
+                    uint2* Vh = reinterpret_cast<uint2*>(V0 + sl) + hf;
+                    const uint2 rp = __ldcs(Ph), rm = __ldcs(Mh), rv = __ldcs(Vh);
+                    float gq[4];
+                    if constexpr (GK == kF32) {
+                        const uint4 t4 = __ldcs(G0 + sl * 2 + hf);
+                        gq[0] = __uint_as_float(t4.x);
+                        gq[1] = __uint_as_float(t4.y);
+                        gq[2] = __uint_as_float(t4.z);
+                        gq[3] = __uint_as_float(t4.w);
+                    } else {
+                        const uint2 t2 = __ldcs(reinterpret_cast<const uint2*>(G0 + sl) + hf);
+                        const uint32_t gw[2] = {t2.x, t2.y};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t hb = (k & 1) ? (gw[k >> 1] >> 16) : (gw[k >> 1] & 0xFFFFu);
+                            gq[k] = GK == kBF16 ? __uint_as_float(hb << 16) : widen_f16(hb);
+                        }
+                    }
+                    const uint32_t pw[2] = {rp.x, rp.y}, mw[2] = {rm.x, rm.y}, vw[2] = {rv.x, rv.y};
+                    auto lane16 = [](const uint32_t (&w)[2], int k) {
+                        return __uint_as_float((k & 1) ? (w[k >> 1] & 0xFFFF0000u) : (w[k >> 1] << 16));
+                    };
+                    float P[4], M[4], V[4];
+                    bool cold = sc.fast;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float p = lane16(pw, k);
+                        const float g = __fmul_rn(gq[k], sc.inv_scale);
+                        M[k] = __fadd_rn(__fmul_rn(c.beta1, lane16(mw, k)), __fmul_rn(c.one_minus_b1, g));
+                        V[k] = __fadd_rn(__fmul_rn(c.beta2, lane16(vw, k)),
+                                         __fmul_rn(c.one_minus_b2, __fmul_rn(g, g)));
+                        cold &= (M[k] == 0.0f) & (V[k] >= 0.0f) & fast_p_ok(p);
+                        P[k] = __fsub_rn(__fsub_rn(p, __fmul_rn(c.lr, M[k])), __fmul_rn(c.lr_wd, p));
+                    }
+                    if (!cold) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            P[k] = lane16(pw, k);
+                            M[k] = lane16(mw, k);
+                            V[k] = lane16(vw, k);
+                            adam_any<kOrdBf16>(P[k], M[k], V[k], gq[k], c, sc);
+                        }
+                    }
+                    __stcs(Ph, make_uint2(narrow2<kBF16>(P[0], P[1]), narrow2<kBF16>(P[2], P[3])));
+                    __stcs(Mh, make_uint2(narrow2<kBF16>(M[0], M[1]), narrow2<kBF16>(M[2], M[3])));
+                    __stcs(Vh, make_uint2(narrow2<kBF16>(V[0], V[1]), narrow2<kBF16>(V[2], V[3])));
+                }
+                continue;
+            }
             for (uint32_t d = threadIdx.x; d < nd; d += kK2Threads) {
                 const uint32_t sl = dlist[d];
                 K3Raw<GK> r;
@@ -2624,6 +2685,7 @@ void k3_dispatch(int gk, int variant, F&& f) {
         case 23: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 1>);
         case 24: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 0>);  // production until the cold routes
         case 25: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 5>);  // early reject + vector second chance
+        case 27: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 9>);  // early reject + split drain
         default: return f(k3_v2<kBF16, 2, 4, false, 1, 1, true, 3>);
     }
 }
