@@ -2385,12 +2385,23 @@ int k1_ldk() {
     return v;
 }
 
+// MA_PDL=0 turns every programmatic launch into a plain one (the kernels'
+// griddepcontrol instructions are then no-ops); MA_PDL_FINISH / MA_PDL_K3 =
+// 0 do it for the scaler / K3 alone (A/B).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MA_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool pdl_finish() {
     static const bool on = [] {
         const char* e = std::getenv("MA_PDL_FINISH");  // A/B only (0 = plain launch)
         return !(e && e[0] == '0');
     }();
-    return on;
+    return on && pdl_enabled();
 }
 
 void launch_k1(const K1Args& a, bool track, int unroll, bool oneshot, unsigned grid,
@@ -2595,7 +2606,11 @@ void launch_k2(int gk, int wk, int variant, const SegTable& tab, const AdamArgs&
         constexpr int v = decltype(V)::value;
         auto fn = K2Kernel<decltype(G)::value, decltype(W)::value, v>::fn;
         if constexpr (v == 20 || v == 21) {
-            launch_pdl(fn, grid, kK2Threads, st, tab, a);
+            if (pdl_enabled()) {
+                launch_pdl(fn, grid, kK2Threads, st, tab, a);
+            } else {
+                fn<<<grid, kK2Threads, 0, st>>>(tab, a);
+            }
         } else {
             fn<<<grid, kK2Threads, 0, st>>>(tab, a);
         }
@@ -2704,7 +2719,7 @@ void launch_k3(int gk, int variant, const SegTable& tab, const AdamArgs& a, unsi
     // dependent (MA_PDL_K3=0: plain launch, A/B); the older A/B kernels do not
     static const bool pdl = [] {
         const char* e = std::getenv("MA_PDL_K3");
-        return !(e && e[0] == '0');
+        return !(e && e[0] == '0') && pdl_enabled();
     }();
     const bool production = gk != kBF16 || variant == 0 || variant >= 21;
     k3_dispatch(gk, variant, [&](auto fn) {
