@@ -616,3 +616,35 @@ def test_cfg2_full_size_pure_bf16_sampled_parity():
     assert (host_bits16(v[it]) == top(smp["v"])).all()
     del w, m, v, g, st
     torch.cuda.empty_cache()
+
+
+def test_empty_inputs():
+    """n == 0 everywhere the reference accepts it: fused_overflow_check
+    returns no overflow (overflow.cpp:77-79); adam_step_fp32 / _bf16 are
+    no-ops but still reject t == 0 (optimizer.cpp:49-51); a stepper step over
+    an empty partition is a clean step (t advances, the scaler counts it)."""
+    for kind, dt in (("f32", torch.float32), ("bf16", torch.bfloat16), ("f16", torch.float16)):
+        e = torch.empty(0, dtype=dt, device=DEV)
+        r = mab.fused_overflow_check(e, track_first_index=True, kind=kind)
+        assert r.overflow is False and r.first_offending_index is None
+    z = torch.empty(0, dtype=torch.float32, device=DEV)
+    z16 = torch.empty(0, dtype=torch.int16, device=DEV)
+    mab.adam_step_fp32(z, z.clone(), z.clone(), z.clone(), 1, mab.AdamHyper(), 65536.0)
+    mab.adam_step_fp32(z, z.clone(), z.clone(), z16.view(torch.bfloat16), 3, mab.AdamHyper(),
+                       65536.0, w_out=z16.clone(), grad_kind="bf16", w_kind="bf16")
+    with pytest.raises(mab.MemAscendError):
+        mab.adam_step_fp32(z, z.clone(), z.clone(), z.clone(), 0, mab.AdamHyper(), 1.0)
+    mab.adam_step_bf16(z16, z16.clone(), z16.clone(), z, 1, mab.AdamHyper(), 1.0)
+    with pytest.raises(mab.MemAscendError):
+        mab.adam_step_bf16(z16, z16.clone(), z16.clone(), z, 0, mab.AdamHyper(), 1.0)
+    st = mab.Stepper(mab.AdamHyper(), 1024.0, 2, "bf16", "bf16")
+    g = torch.empty(0, dtype=torch.bfloat16, device=DEV)
+    for _ in range(3):
+        st.check(g)
+        st.apply([])
+        st.apply_bf16([])
+        st.finish()
+    torch.cuda.synchronize()
+    s = st.state()
+    assert s["updates"] == 3 and s["last_overflow"] == 0 and s["scale"] == 2048.0
+    st.close()
