@@ -321,10 +321,32 @@ class Exchange:
 
         self.mode, self.world = mode, world
         self.comm = self.xchg = None
-        if world > 1 and mode == "nccl":
+        self.fallback = None
+        if world > 1 and mode == "nccl" and not self._library_nccl_everywhere(mab):
+            # every rank must take the same path (the communicator's creation is
+            # collective): all fall back to torch.distributed, and the line says so
+            self.mode, self.fallback = "torch", "libnccl.so.2 not resolvable on every rank"
+        if world > 1 and self.mode == "nccl":
             self.comm = mab.NcclComm(world, rank, mab.torch_broadcast_bytes())
         elif world > 1 and mode == "p2p":
             self.xchg = mab.api.FlagExchange(world, rank, mab.api.torch_all_gather_bytes())
+
+    @staticmethod
+    def _library_nccl_everywhere(mab):
+        """Whether every rank resolves libnccl.so.2 for ma_comm (one MIN
+        all-reduce over torch.distributed before any rank enters the
+        communicator's collective creation)."""
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        buf = (ctypes.c_ubyte * mab.capi.NCCL_ID_BYTES)()
+        ok = mab.capi.lib().ma_comm_unique_id(buf) == 0
+        dev = torch.cuda.current_device() if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
 
     def after_check(self, st, stream):
         import torch
@@ -345,9 +367,10 @@ class Exchange:
     def describe(self):
         if self.world == 1:
             return "none (1 rank)"
-        return {"nccl": "ma_comm ncclAllReduce(max) of the flag (library NCCL)",
-                "torch": "torch.distributed all_reduce(max) of the flag",
-                "p2p": "fused into K1's last CTA over peer memory (CUDA IPC)"}[self.mode]
+        d = {"nccl": "ma_comm ncclAllReduce(max) of the flag (library NCCL)",
+             "torch": "torch.distributed all_reduce(max) of the flag",
+             "p2p": "fused into K1's last CTA over peer memory (CUDA IPC)"}[self.mode]
+        return d if self.fallback is None else f"{d} (fallback: {self.fallback})"
 
     def close(self):
         if self.comm is not None:

@@ -217,3 +217,27 @@ def test_cfg4_line_pool_roofline_e2e():
     assert "memascend::Pool" in j["config"]["state_pool"]
     assert j["pinned_host_bytes"]["pool_payload"] == 12 * 250000000
     assert j["e2e"]["h2d_bytes_per_step"] == 14 * 250000000 and j["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_library_nccl_agreement_world1():
+    """The N>1 guard of bench.py's NCCL exchange (every rank must resolve
+    libnccl before any enters the communicator's collective creation), run
+    on a world-1 NCCL process group."""
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2505_23254_b200 as mab
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port()}", world_size=1, rank=0,
+                            device_id=torch.device("cuda", 0))
+    try:
+        assert bench.Exchange._library_nccl_everywhere(mab) is True
+        x = bench.Exchange("nccl", 1, 0)
+        assert x.describe() == "none (1 rank)" and x.fallback is None
+        x.close()
+    finally:
+        dist.destroy_process_group()
