@@ -641,6 +641,8 @@ def test_empty_inputs():
     g = torch.empty(0, dtype=torch.bfloat16, device=DEV)
     for _ in range(3):
         st.check(g)
+        st.ingest(torch.empty(0, dtype=torch.float32, device=DEV), g)   # producer-side check
+        st.reduce_check([g, g.clone()], g.clone())                       # K4
         st.apply([])
         st.apply_bf16([])
         st.finish()
