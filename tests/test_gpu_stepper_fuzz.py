@@ -209,3 +209,33 @@ def test_random_scenario_vs_oracle(case):
             assert np.array_equal(bits(getattr(r, k)), ref[k].view(np.uint32)), (k, info)
         assert np.array_equal(bits(r.w), ref["w"]), info
     r.st.close()
+
+
+@pytest.mark.parametrize("mode", ["eager", "graph", "pure", "streamed"])
+def test_more_subgroups_than_one_launch_holds(mode):
+    """300 ragged sub-groups (a launch takes at most 96: the update is then
+    split over four launches; the streamed path runs them slot by slot),
+    misaligned views, faults and scale growth, vs the oracle bit for bit."""
+    rs = np.random.default_rng(77)
+    n = 300 * 137 + 5
+    cuts = sorted(set(int(x) for x in rs.choice(np.arange(1, n), 299, replace=False)))
+    assert len(cuts) == 299
+    c = dict(mode=mode, n=n, bounds=list(zip([0] + cuts, cuts + [n])), g_kind="bf16",
+             w_kind="bf16", hyp=dict(lr=1e-3, weight_decay=0.01), scale=65536.0, growth=3,
+             steps=6, faults=[(1, 12345, 0x7FC0), (4, n - 1, 0x7F7F)], offs=[1, 2, 3, 0, 1],
+             seed=4242, cut=3, slots=3, slot_elems=4096)
+    r, of, sc = run(c)
+    ref = ora.train(n, c["steps"], c["seed"], mixed=mode != "pure", g_kind="bf16", w_kind="bf16",
+                    hyp=ora.hyper(**c["hyp"]), scale=c["scale"], growth=c["growth"],
+                    faults=c["faults"])
+    assert of == ref["overflow"].astype(bool).tolist()
+    assert sc == ref["scale_after"].tolist()
+    if mode == "pure":
+        assert np.array_equal(bits(r.w), ref["w"])
+        assert np.array_equal(bits(r.m), ref["m16"])
+        assert np.array_equal(bits(r.v), ref["v16"])
+    else:
+        for k in "pmv":
+            assert np.array_equal(bits(getattr(r, k)), ref[k].view(np.uint32)), k
+        assert np.array_equal(bits(r.w), ref["w"])
+    r.st.close()
