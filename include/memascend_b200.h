@@ -173,6 +173,22 @@ MA_API int ma_stepper_check_async(ma_stepper* s, const void* g, uint64_t n, void
  * (the staged H2D of PAPER.md §4.4 / north-star item (1)). */
 MA_API int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
                                        uint64_t chunk_elems, void* stream, void* copy_stream);
+/* The same check, with the update of every sub-group whose gradients have
+ * landed started at once while the flag is still clear (its p/m/v/w first
+ * copied to `backup`, device memory of backup_bytes; sub-groups in order
+ * while it has room, at most 64, their g tiling dev_g contiguously), so the
+ * update overlaps the PCIe transfer.  Complete the step with
+ * ma_stepper_apply_spec_async (same groups; after any flag exchange), which
+ * updates the rest and, when the step's flag is set, restores the
+ * speculated sub-groups from their backups — bit for bit the plain
+ * check -> apply result either way — then ma_stepper_finish_async. */
+MA_API int ma_stepper_check_host_spec_async(ma_stepper* s, const void* host_g, void* dev_g,
+                                            uint64_t n, uint64_t chunk_elems,
+                                            const ma_subgroup* groups, uint32_t count,
+                                            void* backup, uint64_t backup_bytes, void* stream,
+                                            void* copy_stream);
+MA_API int ma_stepper_apply_spec_async(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
+                                       void* stream);
 /* Cross-rank skip decision fused into K1 (replaces the all-reduce(max) of
  * the flag).  Each rank creates an exchange object, publishes its 64-byte
  * CUDA IPC handle, and opens everybody's handles (rank order); then, per

@@ -242,6 +242,28 @@ class Stepper:
             self._h, host_g.data_ptr(), dev_g.data_ptr(), dev_g.numel(), chunk_elems,
             _stream_ptr(stream), _stream_ptr(copy_stream)))
 
+    def check_from_host_spec(self, host_g, dev_g, groups, backup, chunk_elems=64 << 20,
+                             stream=None, copy_stream=None):
+        """check_from_host with the update of each sub-group started as soon
+        as its gradients have landed (p/m/v/w backed up into `backup`, a
+        device tensor); finish the step with apply_spec(groups) (after any
+        flag exchange), then finish().  groups: a subgroups() array whose g
+        views tile dev_g in order."""
+        arr = self._groups(groups)
+        if copy_stream is None:
+            copy_stream = self._copy_stream = getattr(self, "_copy_stream", None) or \
+                torch.cuda.Stream(device=dev_g.device)
+        bp, nb = (backup.data_ptr(), backup.numel() * backup.element_size()) \
+            if backup is not None else (None, 0)
+        check(capi.lib().ma_stepper_check_host_spec_async(
+            self._h, host_g.data_ptr(), dev_g.data_ptr(), dev_g.numel(), chunk_elems, arr,
+            len(arr), bp, nb, _stream_ptr(stream), _stream_ptr(copy_stream)))
+
+    def apply_spec(self, groups, stream=None):
+        """The step's decision after check_from_host_spec (same groups)."""
+        arr = self._groups(groups)
+        check(capi.lib().ma_stepper_apply_spec_async(self._h, arr, len(arr), _stream_ptr(stream)))
+
     @staticmethod
     def subgroups(groups, g_dtype=None, w_dtype=None):
         """ma_subgroup array of (p, m, v, g, w) tensors.  Every tensor must be

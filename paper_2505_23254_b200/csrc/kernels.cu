@@ -2359,7 +2359,58 @@ __global__ void k_mask_sweep(int kind, unsigned long long* mismatches) {
     if (bad) atomicAdd(mismatches, bad);
 }
 
+// ============================================================== speculation
+__global__ void k_spec_mark(const StepDev* st, uint32_t* marker, uint32_t value) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 &&
+        *reinterpret_cast<const volatile uint32_t*>(&st->flag) == 0u)
+        *marker = value;
+}
+
+// Copies back the backups of the first *marker speculated sub-groups when
+// the step's flag is set; the last CTA to finish re-arms the marker.
+__global__ void __launch_bounds__(256) k_spec_restore(SpecRestore r, const StepDev* st,
+                                                      uint32_t* marker) {
+    const uint32_t applied = *reinterpret_cast<const volatile uint32_t*>(marker);
+    if (st->flag != 0u) {
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        for (uint32_t k = 0; k < r.count; ++k) {
+            if (r.c[k].group >= applied) continue;
+            const uint64_t first = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+            if (((reinterpret_cast<uintptr_t>(r.c[k].src) | reinterpret_cast<uintptr_t>(r.c[k].dst) |
+                  r.c[k].bytes) & 15u) == 0) {
+                const uint4* src = static_cast<const uint4*>(r.c[k].src);
+                uint4* dst = static_cast<uint4*>(r.c[k].dst);
+                for (uint64_t i = first; i < r.c[k].bytes / 16; i += stride) __stcs(dst + i, __ldcs(src + i));
+            } else {  // a misaligned view (rare): byte by byte
+                const uint8_t* src = static_cast<const uint8_t*>(r.c[k].src);
+                uint8_t* dst = static_cast<uint8_t*>(r.c[k].dst);
+                for (uint64_t i = first; i < r.c[k].bytes; i += stride) dst[i] = src[i];
+            }
+        }
+    }
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(marker + 1, 1u) == gridDim.x - 1;  // marker[1]: CTA counter
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        marker[0] = 0u;
+        marker[1] = 0u;
+    }
+}
+
 // ============================================================== launchers
+void launch_spec_mark(const StepDev* st, uint32_t* marker, uint32_t value, cudaStream_t s) {
+    k_spec_mark<<<1, 32, 0, s>>>(st, marker, value);
+}
+
+void launch_spec_restore(const SpecRestore& r, const StepDev* st, uint32_t* marker, unsigned grid,
+                         cudaStream_t s) {
+    k_spec_restore<<<grid, 256, 0, s>>>(r, st, marker);
+}
+
 // Launch as a programmatic dependent of the previous kernel in the stream
 // (the kernel must pdl_wait() before consuming that kernel's results).
 template <typename... P, typename... A>

@@ -171,6 +171,26 @@ void launch_gen_grads(int gk, int wk, void* g, const uint16_t* w, uint64_t n, ui
                       uint64_t seed, uint64_t step, const float* d_scale, float scale,
                       unsigned grid, cudaStream_t st);
 void launch_plant(void* buf, int dtype, uint64_t index, uint32_t bits, cudaStream_t st);
+// Speculative update during the host-gradient transfer
+// (ma_stepper_check_host_spec_async): after a sub-group's speculative K2,
+// marker = value if this step's flag is still clear (the applied sub-groups
+// are then exactly the first `marker` speculated ones); at the end of the
+// step, when the (exchanged) flag is set, the backups of those sub-groups
+// are copied back, and the marker is re-armed either way.
+constexpr int kMaxSpecCopies = 256;  // 64 sub-groups x (p, m, v, w)
+struct SpecCopy {
+    const void* src;
+    void* dst;
+    uint64_t bytes;
+    uint32_t group;  // index among the speculated sub-groups
+};
+struct SpecRestore {
+    SpecCopy c[kMaxSpecCopies];
+    uint32_t count;
+};
+void launch_spec_mark(const StepDev* st, uint32_t* marker, uint32_t value, cudaStream_t s);
+void launch_spec_restore(const SpecRestore& r, const StepDev* st, uint32_t* marker, unsigned grid,
+                         cudaStream_t s);
 // producer-side check: one tile of ingest_units(sk) x 256 eight-element
 // units per CTA over [head, head + 8 * nvec), trailing CTAs for the rest
 struct IngestArgs {
