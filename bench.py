@@ -72,6 +72,8 @@ def parse():
                          "(OptimPrecision::pure_bf16, K3) — in HBM for cfg1/cfg2/cfg3, "
                          "swapped for cfg5")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e-spec", action="store_true",
+                    help="e2e without speculative updates during the gradient transfer")
     ap.add_argument("--flag-exchange", choices=["nccl", "torch", "p2p"], default="nccl",
                     help="N>1: all-reduce the skip flag with the library's own NCCL "
                          "communicator (ma_comm, default), with torch.distributed, or fuse "
@@ -576,13 +578,31 @@ def ours(args, n, rank, world, local_rank):
         g_host.copy_(g.view(torch.int16), non_blocking=False)
         g_host = g_host.view(torch.bfloat16)
         res_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
+        # speculative updates while the gradients stream in (fp32 state):
+        # the leading sub-groups whose state fits a backup in the free HBM
+        spec_groups, backup = 0, None
+        if not bf16_state and not args.no_e2e_spec:
+            al = lambda b: (b + 255) // 256 * 256  # noqa: E731
+            need = [3 * al(4 * min(sub, n - o)) + al(2 * min(sub, n - o))
+                    for o in range(0, n, sub)][:64]
+            room = torch.cuda.mem_get_info()[0] - (2 << 30)
+            while spec_groups < len(need) and sum(need[:spec_groups + 1]) <= room:
+                spec_groups += 1
+            if spec_groups:
+                backup = torch.empty(sum(need[:spec_groups]), dtype=torch.uint8, device=dev)
 
         def e2e_step():
-            st.check_from_host(g_host, g, stream=stream)
+            if backup is not None:
+                st.check_from_host_spec(g_host, g, groups, backup, stream=stream)
+            else:
+                st.check_from_host(g_host, g, stream=stream)
             if xc.xchg is not None:
                 st.check(None, stream=stream, xchg=xc.xchg)  # exchange-only K1 launch
             xc.after_check(st, stream)
-            apply_step(stream)
+            if backup is not None:
+                st.apply_spec(groups, stream=stream)
+            else:
+                apply_step(stream)
             st.finish(stream=stream)
             with torch.cuda.stream(stream):
                 res_host.copy_(st.state_t[:16], non_blocking=True)  # flag/scale readback
@@ -607,9 +627,16 @@ def ours(args, n, rank, world, local_rank):
                "h2d_bytes_per_step": n * 2, "d2h_bytes_per_step": 16,
                "ms_per_step": e2e_ms,
                "path": "pinned host bf16 grads -> chunked H2D overlapped with K1 "
-                       "(ma_stepper_check_host_async) -> flag exchange -> "
-                       f"{'K3' if bf16_state else 'K2'} over HBM-resident "
-                       "state -> D2H of the step's flag/loss-scale"}
+                       + ("and with the speculative K2 of every landed sub-group whose state "
+                          "fits the backup (ma_stepper_check_host_spec_async) -> flag exchange "
+                          "-> K2 over the rest, restore on a skip (ma_stepper_apply_spec_async)"
+                          if backup is not None else
+                          "(ma_stepper_check_host_async) -> flag exchange -> "
+                          f"{'K3' if bf16_state else 'K2'} over HBM-resident state")
+                       + " -> D2H of the step's flag/loss-scale",
+               "speculated_subgroups": spec_groups, "subgroups": len(groups),
+               "backup_bytes": 0 if backup is None else backup.numel()}
+        del backup
         del g_host
         mab.host_unregister(g_buf)
     if graph is not None:
