@@ -581,9 +581,10 @@ def ours(args, n, rank, world, local_rank):
         # speculative updates while the gradients stream in (fp32 state):
         # the leading sub-groups whose state fits a backup in the free HBM
         spec_groups, backup = 0, None
-        if not bf16_state and not args.no_e2e_spec:
+        if not args.no_e2e_spec:
             al = lambda b: (b + 255) // 256 * 256  # noqa: E731
-            need = [3 * al(4 * min(sub, n - o)) + al(2 * min(sub, n - o))
+            need = [3 * al(2 * min(sub, n - o)) if bf16_state else
+                    3 * al(4 * min(sub, n - o)) + al(2 * min(sub, n - o))
                     for o in range(0, n, sub)][:64]
             room = torch.cuda.mem_get_info()[0] - (2 << 30)
             while spec_groups < len(need) and sum(need[:spec_groups + 1]) <= room:
@@ -591,16 +592,22 @@ def ours(args, n, rank, world, local_rank):
             if spec_groups:
                 backup = torch.empty(sum(need[:spec_groups]), dtype=torch.uint8, device=dev)
 
+        spec_arr = st.subgroups_bf16(groups) if bf16_state else groups
+
         def e2e_step():
-            if backup is not None:
-                st.check_from_host_spec(g_host, g, groups, backup, stream=stream)
+            if backup is not None and bf16_state:
+                st.check_from_host_spec_bf16(g_host, g, spec_arr, backup, stream=stream)
+            elif backup is not None:
+                st.check_from_host_spec(g_host, g, spec_arr, backup, stream=stream)
             else:
                 st.check_from_host(g_host, g, stream=stream)
             if xc.xchg is not None:
                 st.check(None, stream=stream, xchg=xc.xchg)  # exchange-only K1 launch
             xc.after_check(st, stream)
-            if backup is not None:
-                st.apply_spec(groups, stream=stream)
+            if backup is not None and bf16_state:
+                st.apply_spec_bf16(spec_arr, stream=stream)
+            elif backup is not None:
+                st.apply_spec(spec_arr, stream=stream)
             else:
                 apply_step(stream)
             st.finish(stream=stream)
@@ -628,8 +635,9 @@ def ours(args, n, rank, world, local_rank):
                "ms_per_step": e2e_ms,
                "path": "pinned host bf16 grads -> chunked H2D overlapped with K1 "
                        + ("and with the speculative K2 of every landed sub-group whose state "
-                          "fits the backup (ma_stepper_check_host_spec_async) -> flag exchange "
-                          "-> K2 over the rest, restore on a skip (ma_stepper_apply_spec_async)"
+                          "fits the backup (ma_stepper_check_host_spec[_bf16]_async) -> flag "
+                          f"exchange -> {'K3' if bf16_state else 'K2'} over the rest, restore on "
+                          "a skip (ma_stepper_apply_spec[_bf16]_async)"
                           if backup is not None else
                           "(ma_stepper_check_host_async) -> flag exchange -> "
                           f"{'K3' if bf16_state else 'K2'} over HBM-resident state")

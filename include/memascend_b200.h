@@ -284,6 +284,16 @@ typedef struct ma_subgroup_bf16 {
 } ma_subgroup_bf16;
 MA_API int ma_stepper_apply_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups,
                                        uint32_t count, void* stream);
+/* The speculative host-gradient check / decision (see
+ * ma_stepper_check_host_spec_async) in the pure-bf16 mode: K3 on bf16
+ * weights / m / v, which are what the backup holds. */
+MA_API int ma_stepper_check_host_spec_bf16_async(ma_stepper* s, const void* host_g, void* dev_g,
+                                                 uint64_t n, uint64_t chunk_elems,
+                                                 const ma_subgroup_bf16* groups, uint32_t count,
+                                                 void* backup, uint64_t backup_bytes,
+                                                 void* stream, void* copy_stream);
+MA_API int ma_stepper_apply_spec_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups,
+                                            uint32_t count, void* stream);
 
 /* Streamed update (configs 4/5: state offloaded to the pinned host pool).
  * groups[k].p/m/v live in registered host memory, .g/.w on the device.

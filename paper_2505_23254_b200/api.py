@@ -317,6 +317,14 @@ class Stepper:
 
     def apply_bf16(self, groups, stream=None):
         """Pure-bf16 mode: groups of (p_bf16, m_bf16, v_bf16, g) tensors (K3)."""
+        arr = self.subgroups_bf16(groups)
+        check(capi.lib().ma_stepper_apply_bf16_async(self._h, arr, len(arr), _stream_ptr(stream)))
+
+    def subgroups_bf16(self, groups):
+        """ma_subgroup_bf16 array of (p_bf16, m_bf16, v_bf16, g) tensors, checked
+        (kinds, lengths, contiguity); a prebuilt array passes through."""
+        if isinstance(groups, C.Array):
+            return groups
         arr = (capi.SubgroupBf16 * len(groups))()
         for k, (p, m, v, g) in enumerate(groups):
             n = p.numel()
@@ -333,7 +341,27 @@ class Stepper:
                 raise MemAscendError(1, f"sub-group {k}: gradients are {g.dtype}, the stepper's "
                                         f"gradient kind is {self.g_dtype}")
             arr[k] = capi.SubgroupBf16(p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), n)
-        check(capi.lib().ma_stepper_apply_bf16_async(self._h, arr, len(arr), _stream_ptr(stream)))
+        return arr
+
+    def check_from_host_spec_bf16(self, host_g, dev_g, groups, backup, chunk_elems=64 << 20,
+                                  stream=None, copy_stream=None):
+        """check_from_host_spec in the pure-bf16 mode (K3; groups of
+        (p_bf16, m_bf16, v_bf16, g) whose g views tile dev_g in order)."""
+        arr = self.subgroups_bf16(groups)
+        if copy_stream is None:
+            copy_stream = self._copy_stream = getattr(self, "_copy_stream", None) or \
+                torch.cuda.Stream(device=dev_g.device)
+        bp, nb = (backup.data_ptr(), backup.numel() * backup.element_size()) \
+            if backup is not None else (None, 0)
+        check(capi.lib().ma_stepper_check_host_spec_bf16_async(
+            self._h, host_g.data_ptr(), dev_g.data_ptr(), dev_g.numel(), chunk_elems, arr,
+            len(arr), bp, nb, _stream_ptr(stream), _stream_ptr(copy_stream)))
+
+    def apply_spec_bf16(self, groups, stream=None):
+        """The step's decision after check_from_host_spec_bf16 (same groups)."""
+        arr = self.subgroups_bf16(groups)
+        check(capi.lib().ma_stepper_apply_spec_bf16_async(self._h, arr, len(arr),
+                                                          _stream_ptr(stream)))
 
     def apply_streamed(self, groups, staging, slot_elems, slots=2, stream=None,
                        h2d_stream=None, d2h_stream=None) -> bool:

@@ -127,6 +127,9 @@ SIGNATURES = [
     ("ma_stepper_check_host_spec_async", _I, [_VP, _VP, _VP, _U64, _U64, _VP, _U32, _VP, _U64,
                                               _VP, _VP]),
     ("ma_stepper_apply_spec_async", _I, [_VP, _VP, _U32, _VP]),
+    ("ma_stepper_check_host_spec_bf16_async", _I, [_VP, _VP, _VP, _U64, _U64, _VP, _U32, _VP,
+                                                   _U64, _VP, _VP]),
+    ("ma_stepper_apply_spec_bf16_async", _I, [_VP, _VP, _U32, _VP]),
     ("ma_xchg_create", _I, [_I, _I, C.POINTER(_VP), _VP]),
     ("ma_xchg_open", _I, [_VP, _VP]),
     ("ma_xchg_error", _I, [_VP, C.POINTER(_I)]),

@@ -906,94 +906,167 @@ int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, 
 // PCIe transfer hides.  Sub-groups are speculated in order while `backup`
 // has room (and at most 64); their g must tile dev_g contiguously, else
 // nothing is speculated.
+}  // extern "C"
+
+namespace {
+
+// Shared by the fp32-state (K2) and pure-bf16 (K3) forms.  bf16: groups'
+// p/m/v are uint16 arrays (as ma_stepper_apply_bf16_async passes them) and
+// there are no working weights.
+void check_host_spec(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
+                     uint64_t chunk_elems, const ma_subgroup* groups, uint32_t count, bool bf16,
+                     void* backup, uint64_t backup_bytes, void* stream, void* copy_stream) {
+    if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+    if (!s->spec_groups.empty())
+        fail(MA_ERR_LIFECYCLE, "speculative step pending: call ma_stepper_apply_spec_async");
+    if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
+    if (n == 0) return;
+    if (!host_g || !dev_g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
+    const void* alias;
+    if (classify(host_g, &alias) != 2)
+        fail(MA_ERR_INVALID_ARGUMENT, "host gradients must be pinned (registered) memory");
+    if (chunk_elems == 0) chunk_elems = 64ull << 20;
+    const uint64_t es = elem_bytes(s->g_dtype);
+    const uint64_t state_es = bf16 ? 2 : 4;
+    const int ntens = bf16 || s->w_dtype == MA_DT_NONE ? 3 : 4;
+    auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
+    // plan: the leading sub-groups that tile dev_g and fit the backup
+    std::vector<uint64_t> ends, boff;
+    {
+        uint64_t cum = 0, used = 0;
+        bool tiles = true;
+        for (uint32_t k = 0; k < count && tiles; ++k) {
+            tiles = groups[k].g == static_cast<const uint8_t*>(dev_g) + cum * es;
+            cum += groups[k].n;
+        }
+        tiles = tiles && cum == n;
+        cum = 0;
+        for (uint32_t k = 0; tiles && backup && k < count && k < ma::kMaxSpecCopies / 4; ++k) {
+            const uint64_t gn = groups[k].n;
+            const uint64_t need = 3 * al(gn * state_es) + (ntens == 4 ? al(gn * 2) : 0);
+            if (used + need > backup_bytes) break;
+            boff.push_back(used);
+            used += need;
+            cum += gn;
+            ends.push_back(cum);
+        }
+    }
+    if (!ends.empty() && !s->d_spec) {
+        CK(cudaMalloc(&s->d_spec, 2 * sizeof(uint32_t)));
+        CK(cudaMemset(s->d_spec, 0, 2 * sizeof(uint32_t)));
+    }
+    cudaStream_t cs = as_stream(copy_stream);
+    cudaStream_t st = as_stream(stream);
+    cudaEvent_t ready = s->event(0);
+    CK(cudaEventRecord(ready, st));
+    CK(cudaStreamWaitEvent(cs, ready, 0));
+    ma::SpecRestore rs{};
+    std::vector<ma_subgroup> spec;
+    size_t next = 0;  // next sub-group to speculate
+    uint64_t k = 0;
+    for (uint64_t off = 0; off < n; off += chunk_elems, ++k) {
+        const uint64_t len = std::min(chunk_elems, n - off);
+        CK(cudaMemcpyAsync(static_cast<uint8_t*>(dev_g) + off * es,
+                           static_cast<const uint8_t*>(host_g) + off * es, len * es,
+                           cudaMemcpyHostToDevice, cs));
+        cudaEvent_t landed = s->event(1 + k);
+        CK(cudaEventRecord(landed, cs));
+        CK(cudaStreamWaitEvent(st, landed, 0));
+        launch_k1(static_cast<uint8_t*>(dev_g) + off * es, len, s->g_dtype, &s->d_st->flag,
+                  nullptr, 0, true, st, nullptr, off + len == n,
+                  off + len == n ? &s->kept_lo : nullptr, &s->kept_lines);
+        while (next < ends.size() && ends[next] <= off + len) {
+            const ma_subgroup& g = groups[next];
+            const uint64_t gn = g.n;
+            void* src[4] = {g.p, g.m, g.v, g.w};
+            const uint64_t bytes[4] = {gn * state_es, gn * state_es, gn * state_es, gn * 2};
+            char* dst = static_cast<char*>(backup) + boff[next];
+            for (int t = 0; t < ntens; ++t) {
+                CK(cudaMemcpyAsync(dst, src[t], bytes[t], cudaMemcpyDeviceToDevice, st));
+                rs.c[rs.count++] = ma::SpecCopy{dst, src[t], bytes[t], static_cast<uint32_t>(next)};
+                dst += al(bytes[t]);
+            }
+            if (bf16)
+                launch_k3(&g, 1, s->g_dtype, stepper_args(s), st);
+            else
+                launch_k2(&g, 1, s->g_dtype, s->w_dtype, stepper_args(s), st);
+            ma::launch_spec_mark(s->d_st, s->d_spec, static_cast<uint32_t>(next + 1), st);
+            CK(cudaGetLastError());
+            spec.push_back(g);
+            ++next;
+        }
+    }
+    s->spec_groups = std::move(spec);
+    s->spec_restore = rs;
+    s->last = st;
+}
+
+void apply_spec(ma_stepper* s, const ma_subgroup* groups, uint32_t count, bool bf16,
+                void* stream) {
+    if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
+    if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
+    const uint32_t S = static_cast<uint32_t>(s->spec_groups.size());
+    if (S > count) fail(MA_ERR_INVALID_ARGUMENT, "fewer sub-groups than were speculated");
+    for (uint32_t k = 0; k < S; ++k) {
+        const ma_subgroup& a = groups[k];
+        const ma_subgroup& b = s->spec_groups[k];
+        if (a.p != b.p || a.m != b.m || a.v != b.v || a.g != b.g || a.w != b.w || a.n != b.n)
+            fail(MA_ERR_INVALID_ARGUMENT, "sub-groups differ from the speculative check's");
+    }
+    cudaStream_t st = as_stream(stream);
+    if (count > S) {
+        if (bf16)
+            launch_k3(groups + S, count - S, s->g_dtype, stepper_args(s), st);
+        else
+            launch_k2(groups + S, count - S, s->g_dtype, s->w_dtype, stepper_args(s), st);
+    }
+    if (S) {
+        const DeviceInfo d = device_info();
+        ma::launch_spec_restore(s->spec_restore, s->d_st, s->d_spec,
+                                static_cast<unsigned>(d.sms) * 4, st);
+        CK(cudaGetLastError());
+    }
+    s->spec_groups.clear();
+    s->spec_restore.count = 0;
+    s->last = st;
+}
+
+std::vector<ma_subgroup> as_subgroups(const ma_subgroup_bf16* groups, uint32_t count) {
+    std::vector<ma_subgroup> gs(count);
+    for (uint32_t k = 0; k < count; ++k)
+        gs[k] = ma_subgroup{reinterpret_cast<float*>(groups[k].p),
+                            reinterpret_cast<float*>(groups[k].m),
+                            reinterpret_cast<float*>(groups[k].v), groups[k].g, nullptr,
+                            groups[k].n};
+    return gs;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Speculative update while the host gradients stream in.  The reference
+// decides a step on the whole flat buffer first (simulator.cpp:431-440); on
+// the host-buffer path that decision waits for the last PCIe chunk, and the
+// update would follow the transfer instead of overlapping it.  Here each
+// sub-group whose gradients have all landed (and passed K1) while the flag
+// is still clear is updated at once — after copying its state to `backup`
+// — and the step's final decision is applied in ma_stepper_apply_spec_async:
+// a clear flag keeps the updates, a set one copies the backups back.  The
+// bits equal the plain check -> apply path either way (an update is a pure
+// function of the old state, and a skip leaves the old state); only the
+// HBM traffic of the speculated groups grows (the backup copy), which the
+// PCIe transfer hides.  Sub-groups are speculated in order while `backup`
+// has room (and at most 64); their g must tile dev_g contiguously, else
+// nothing is speculated.
 int ma_stepper_check_host_spec_async(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
                                      uint64_t chunk_elems, const ma_subgroup* groups,
                                      uint32_t count, void* backup, uint64_t backup_bytes,
                                      void* stream, void* copy_stream) {
     NvtxRange nvtx_range("ma_stepper_check_host_spec_async");
     return guarded([&] {
-        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
-        if (!s->spec_groups.empty())
-            fail(MA_ERR_LIFECYCLE, "speculative step pending: call ma_stepper_apply_spec_async");
-        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        if (n == 0) return;
-        if (!host_g || !dev_g) fail(MA_ERR_INVALID_ARGUMENT, "null gradient pointer");
-        const void* alias;
-        if (classify(host_g, &alias) != 2)
-            fail(MA_ERR_INVALID_ARGUMENT, "host gradients must be pinned (registered) memory");
-        if (chunk_elems == 0) chunk_elems = 64ull << 20;
-        const uint64_t es = elem_bytes(s->g_dtype);
-        // plan: the leading sub-groups that tile dev_g and fit the backup
-        std::vector<uint64_t> ends;
-        std::vector<uint64_t> boff;
-        {
-            uint64_t cum = 0, used = 0;
-            bool tiles = true;
-            for (uint32_t k = 0; k < count && tiles; ++k) {
-                tiles = groups[k].g == static_cast<const uint8_t*>(dev_g) + cum * es;
-                cum += groups[k].n;
-            }
-            tiles = tiles && cum == n;
-            auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
-            cum = 0;
-            for (uint32_t k = 0; tiles && backup && k < count && k < ma::kMaxSpecCopies / 4; ++k) {
-                const uint64_t gn = groups[k].n;
-                const uint64_t need = 3 * al(gn * 4) + (s->w_dtype == MA_DT_NONE ? 0 : al(gn * 2));
-                if (used + need > backup_bytes) break;
-                boff.push_back(used);
-                used += need;
-                cum += gn;
-                ends.push_back(cum);
-            }
-        }
-        if (!ends.empty() && !s->d_spec) {
-            CK(cudaMalloc(&s->d_spec, 2 * sizeof(uint32_t)));
-            CK(cudaMemset(s->d_spec, 0, 2 * sizeof(uint32_t)));
-        }
-        cudaStream_t cs = as_stream(copy_stream);
-        cudaStream_t st = as_stream(stream);
-        cudaEvent_t ready = s->event(0);
-        CK(cudaEventRecord(ready, st));
-        CK(cudaStreamWaitEvent(cs, ready, 0));
-        ma::SpecRestore rs{};
-        std::vector<ma_subgroup> spec;
-        size_t next = 0;  // next sub-group to speculate
-        auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
-        uint64_t k = 0;
-        for (uint64_t off = 0; off < n; off += chunk_elems, ++k) {
-            const uint64_t len = std::min(chunk_elems, n - off);
-            CK(cudaMemcpyAsync(static_cast<uint8_t*>(dev_g) + off * es,
-                               static_cast<const uint8_t*>(host_g) + off * es, len * es,
-                               cudaMemcpyHostToDevice, cs));
-            cudaEvent_t landed = s->event(1 + k);
-            CK(cudaEventRecord(landed, cs));
-            CK(cudaStreamWaitEvent(st, landed, 0));
-            launch_k1(static_cast<uint8_t*>(dev_g) + off * es, len, s->g_dtype, &s->d_st->flag,
-                      nullptr, 0, true, st, nullptr, off + len == n,
-                      off + len == n ? &s->kept_lo : nullptr, &s->kept_lines);
-            while (next < ends.size() && ends[next] <= off + len) {
-                const ma_subgroup& g = groups[next];
-                char* b = static_cast<char*>(backup) + boff[next];
-                const uint64_t gn = g.n;
-                void* src[4] = {g.p, g.m, g.v, g.w};
-                const uint64_t bytes[4] = {gn * 4, gn * 4, gn * 4, gn * 2};
-                char* dst = b;
-                for (int t = 0; t < (s->w_dtype == MA_DT_NONE ? 3 : 4); ++t) {
-                    CK(cudaMemcpyAsync(dst, src[t], bytes[t], cudaMemcpyDeviceToDevice, st));
-                    rs.c[rs.count++] = ma::SpecCopy{dst, src[t], bytes[t],
-                                                   static_cast<uint32_t>(next)};
-                    dst += al(bytes[t]);
-                }
-                launch_k2(&g, 1, s->g_dtype, s->w_dtype, stepper_args(s), st);
-                ma::launch_spec_mark(s->d_st, s->d_spec, static_cast<uint32_t>(next + 1), st);
-                CK(cudaGetLastError());
-                spec.push_back(g);
-                ++next;
-            }
-        }
-        s->spec_groups = std::move(spec);
-        s->spec_restore = rs;
-        s->last = st;
+        check_host_spec(s, host_g, dev_g, n, chunk_elems, groups, count, false, backup,
+                        backup_bytes, stream, copy_stream);
     });
 }
 
@@ -1004,28 +1077,31 @@ int ma_stepper_check_host_spec_async(ma_stepper* s, const void* host_g, void* de
 int ma_stepper_apply_spec_async(ma_stepper* s, const ma_subgroup* groups, uint32_t count,
                                 void* stream) {
     NvtxRange nvtx_range("ma_stepper_apply_spec_async");
+    return guarded([&] { apply_spec(s, groups, count, false, stream); });
+}
+
+// The pure-bf16 forms (K3; bf16 weights / m / v backed up).
+int ma_stepper_check_host_spec_bf16_async(ma_stepper* s, const void* host_g, void* dev_g,
+                                          uint64_t n, uint64_t chunk_elems,
+                                          const ma_subgroup_bf16* groups, uint32_t count,
+                                          void* backup, uint64_t backup_bytes, void* stream,
+                                          void* copy_stream) {
+    NvtxRange nvtx_range("ma_stepper_check_host_spec_bf16_async");
     return guarded([&] {
-        if (!s) fail(MA_ERR_INVALID_ARGUMENT, "null stepper");
         if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
-        const uint32_t S = static_cast<uint32_t>(s->spec_groups.size());
-        if (S > count) fail(MA_ERR_INVALID_ARGUMENT, "fewer sub-groups than were speculated");
-        for (uint32_t k = 0; k < S; ++k) {
-            const ma_subgroup& a = groups[k];
-            const ma_subgroup& b = s->spec_groups[k];
-            if (a.p != b.p || a.m != b.m || a.v != b.v || a.g != b.g || a.w != b.w || a.n != b.n)
-                fail(MA_ERR_INVALID_ARGUMENT, "sub-groups differ from the speculative check's");
-        }
-        cudaStream_t st = as_stream(stream);
-        if (count > S) launch_k2(groups + S, count - S, s->g_dtype, s->w_dtype, stepper_args(s), st);
-        if (S) {
-            const DeviceInfo d = device_info();
-            ma::launch_spec_restore(s->spec_restore, s->d_st, s->d_spec,
-                                    static_cast<unsigned>(d.sms) * 4, st);
-            CK(cudaGetLastError());
-        }
-        s->spec_groups.clear();
-        s->spec_restore.count = 0;
-        s->last = st;
+        const std::vector<ma_subgroup> gs = as_subgroups(groups, count);
+        check_host_spec(s, host_g, dev_g, n, chunk_elems, gs.data(), count, true, backup,
+                        backup_bytes, stream, copy_stream);
+    });
+}
+
+int ma_stepper_apply_spec_bf16_async(ma_stepper* s, const ma_subgroup_bf16* groups,
+                                     uint32_t count, void* stream) {
+    NvtxRange nvtx_range("ma_stepper_apply_spec_bf16_async");
+    return guarded([&] {
+        if (count && !groups) fail(MA_ERR_INVALID_ARGUMENT, "null sub-group list");
+        const std::vector<ma_subgroup> gs = as_subgroups(groups, count);
+        apply_spec(s, gs.data(), count, true, stream);
     });
 }
 

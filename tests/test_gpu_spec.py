@@ -96,6 +96,47 @@ def test_spec_fp16_weights_and_one_chunk():
     assert np.array_equal(got["w"], ref["w"])
 
 
+@pytest.mark.parametrize("backup_groups", [8, 2])
+def test_spec_pure_bf16_equals_reference(backup_groups):
+    """The pure-bf16 form (K3 on bf16 weights / m / v) against the
+    reference's pure-bf16 composition."""
+    n, steps, seed = N, 6, 11
+    faults = [(1, 40_000, 0x7FC0), (3, N - 1, 0x7F80)]
+    bounds = list(zip([0] + CUTS, CUTS + [n]))
+    w = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    m = torch.zeros(n, dtype=torch.bfloat16, device=DEV)
+    v = torch.zeros(n, dtype=torch.bfloat16, device=DEV)
+    g = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    tmp = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    host = torch.empty(n, dtype=torch.bfloat16).pin_memory()
+    mab.gen_seeded_weights(None, w, seed=seed)
+    st = mab.Stepper(mab.AdamHyper(weight_decay=0.01), 65536.0, 2, "bf16", "bf16")
+    groups = st.subgroups_bf16([(w[a:b], m[a:b], v[a:b], g[a:b]) for a, b in bounds])
+    al = lambda x: (x + 255) // 256 * 256  # noqa: E731
+    nb = sum(3 * al(2 * (b - a)) for a, b in bounds[:backup_groups])
+    backup = torch.empty(nb, dtype=torch.uint8, device=DEV)
+    for s in range(steps):
+        mab.gen_pseudo_grads(tmp, w, step=s, seed=seed, d_scale=st.scale_t)
+        for fs, idx, b in faults:
+            if fs == s:
+                mab.plant_bits(tmp, idx, b)
+        torch.cuda.synchronize()
+        host.copy_(tmp.cpu())
+        st.check_from_host_spec_bf16(host, g, groups, backup, chunk_elems=30_000)
+        st.apply_spec_bf16(groups)
+        st.finish()
+    torch.cuda.synchronize()
+    of, sc = st.history()
+    ref = ora.train(n, steps, seed, mixed=False, g_kind="bf16", w_kind="bf16",
+                    hyp=ora.hyper(weight_decay=0.01), growth=2, faults=faults)
+    assert of.tolist() == ref["overflow"].astype(bool).tolist()
+    assert sc.tolist() == ref["scale_after"].tolist()
+    assert np.array_equal(bits(w), ref["w"])
+    assert np.array_equal(bits(m), ref["m16"])
+    assert np.array_equal(bits(v), ref["v16"])
+    st.close()
+
+
 def test_spec_lifecycle():
     n = 4096
     p, m, v = (torch.zeros(n, device=DEV) for _ in range(3))
