@@ -36,6 +36,11 @@ run memcheck_fuzz $CS --tool memcheck python -m pytest -x -q -p no:cacheprovider
 # and its vector / per-element drains, K2's inline second chance
 run memcheck_cold $CS --tool memcheck python -m pytest -x -q -p no:cacheprovider tests/test_gpu_cold.py
 run racecheck_cold $CS --tool racecheck --racecheck-report all python -m pytest -x -q -p no:cacheprovider tests/test_gpu_cold.py
+# the speculative update during the transfer: backups, the applied-count
+# marker and the restore kernel's last-CTA re-arm
+run memcheck_spec $CS --tool memcheck python -m pytest -x -q -p no:cacheprovider tests/test_gpu_spec.py
+run racecheck_spec $CS --tool racecheck --racecheck-report all python -m pytest -x -q -p no:cacheprovider tests/test_gpu_spec.py
+run synccheck_spec $CS --tool synccheck python -m pytest -x -q -p no:cacheprovider tests/test_gpu_spec.py
 run racecheck_protocols $CS --tool racecheck --racecheck-report all python -m pytest -x -q -p no:cacheprovider $SINGLE
 run synccheck_protocols $CS --tool synccheck python -m pytest -x -q -p no:cacheprovider $SINGLE
 ranks() {
