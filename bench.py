@@ -585,7 +585,7 @@ def ours(args, n, rank, world, local_rank):
             al = lambda b: (b + 255) // 256 * 256  # noqa: E731
             need = [3 * al(2 * min(sub, n - o)) if bf16_state else
                     3 * al(4 * min(sub, n - o)) + al(2 * min(sub, n - o))
-                    for o in range(0, n, sub)][:64]
+                    for o in range(0, n, sub)][:96]
             room = torch.cuda.mem_get_info()[0] - (2 << 30)
             while spec_groups < len(need) and sum(need[:spec_groups + 1]) <= room:
                 spec_groups += 1

@@ -176,7 +176,7 @@ MA_API int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* 
 /* The same check, with the update of every sub-group whose gradients have
  * landed started at once while the flag is still clear (its p/m/v/w first
  * copied to `backup`, device memory of backup_bytes; sub-groups in order
- * while it has room, at most 64, their g tiling dev_g contiguously), so the
+ * while it has room, at most 96, their g tiling dev_g contiguously), so the
  * update overlaps the PCIe transfer.  Complete the step with
  * ma_stepper_apply_spec_async (same groups; after any flag exchange), which
  * updates the rest and, when the step's flag is set, restores the

@@ -904,7 +904,7 @@ int ma_stepper_check_host_async(ma_stepper* s, const void* host_g, void* dev_g, 
 // function of the old state, and a skip leaves the old state); only the
 // HBM traffic of the speculated groups grows (the backup copy), which the
 // PCIe transfer hides.  Sub-groups are speculated in order while `backup`
-// has room (and at most 64); their g must tile dev_g contiguously, else
+// has room (and at most 96); their g must tile dev_g contiguously, else
 // nothing is speculated.
 }  // extern "C"
 
@@ -1057,7 +1057,7 @@ extern "C" {
 // function of the old state, and a skip leaves the old state); only the
 // HBM traffic of the speculated groups grows (the backup copy), which the
 // PCIe transfer hides.  Sub-groups are speculated in order while `backup`
-// has room (and at most 64); their g must tile dev_g contiguously, else
+// has room (and at most 96); their g must tile dev_g contiguously, else
 // nothing is speculated.
 int ma_stepper_check_host_spec_async(ma_stepper* s, const void* host_g, void* dev_g, uint64_t n,
                                      uint64_t chunk_elems, const ma_subgroup* groups,

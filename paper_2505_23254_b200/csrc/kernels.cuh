@@ -177,7 +177,7 @@ void launch_plant(void* buf, int dtype, uint64_t index, uint32_t bits, cudaStrea
 // are then exactly the first `marker` speculated ones); at the end of the
 // step, when the (exchanged) flag is set, the backups of those sub-groups
 // are copied back, and the marker is re-armed either way.
-constexpr int kMaxSpecCopies = 256;  // 64 sub-groups x (p, m, v, w)
+constexpr int kMaxSpecCopies = 384;  // 96 sub-groups x (p, m, v, w) (12 KB of kernel parameters)
 struct SpecCopy {
     const void* src;
     void* dst;
